@@ -1,0 +1,109 @@
+/*
+ * pflu.h -- C ABI of libpflu.so, the B200 (sm_100a) LU-with-partial-pivoting library.
+ *
+ * Drop-in boundary for the reference package `panelforge` (arXiv 1804.07017), hot path
+ * Kind.LU of dmf_la / dmf_mtb.  Plain C types only (no torch types); every function returns
+ * PFLU_OK (0), a NEGATIVE value -i when argument i is invalid (LAPACK convention, 1-based),
+ * or a POSITIVE PFLU_ERR_* code with a message in pflu_last_error().
+ *
+ * Conventions (all entry points):
+ *   - matrices are float64 and ROW-MAJOR: element (i, j) at a[i * lda + j];
+ *   - pivots are int64, 0-based, LAPACK ipiv semantics: for k ascending, row k was swapped with
+ *     row ipiv[k] (ipiv[k] >= k).  The reference's LuOutput.pivots are these values + 1
+ *     (pkg/src/panelforge/factor.py:51-62, 144);
+ *   - `info` is 0, or 1 + the first column whose pivot was exactly zero; that column is left
+ *     unscaled and the factorization completes (reference factor.py:56-58, _jit.py:171-174).
+ *
+ * Reference interfaces replaced (pkg/src/panelforge/...):
+ *   pflu_getrf / pflu_getrf_device  <- dmf_la (factor.py:455-515, lookahead=1) and
+ *                                      dmf_mtb (factor.py:382-412, lookahead=0), kind=Kind.LU
+ *   pflu_panel                      <- _factor_panel + lu_unb + _jit.lu_unb_run
+ *                                      (factor.py:128-144, 235-250; _jit.py:154-187)
+ *   pflu_laswp                      <- laswp + _jit.laswp_run (kernels.py:273-300; _jit.py:141-151)
+ *   pflu_swap_trsm                  <- _panel_laswp + trsm_llnu inside _update_columns
+ *                                      (factor.py:253-277; kernels.py:225-246; _jit.py:104-113)
+ *   pflu_trsm                       <- trsm_llnu (kernels.py:225-246; _jit.py:104-113)
+ *   pflu_gemm_update                <- the gemm(A22, A21, -A12) of _update_columns
+ *                                      (factor.py:278-285; kernels.py:173-218; _jit.py:54-80)
+ */
+#ifndef PFLU_H
+#define PFLU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFLU_OK 0
+#define PFLU_ERR_CUDA 1        /* CUDA runtime/driver failure (see pflu_last_error) */
+#define PFLU_ERR_NOMEM 2       /* device or pinned-host allocation failed */
+#define PFLU_ERR_UNSUPPORTED 3 /* valid request this build cannot run (e.g. no sm_100 device) */
+
+typedef struct pflu_options {
+  int exact;        /* 1: every update in the reference's rounding (multiply, round, subtract):
+                       results are bitwise equal to the reference; 0: trailing GEMM on DMMA */
+  int panel_ctas;   /* CTAs of the cooperative panel leaf (0 = automatic) */
+  int leaf_width;   /* leaf columns: 8, 16 or 32 (0 = automatic) */
+  int reserved[5];
+} pflu_options;
+
+/* Trace record, one per timed task (labels as the reference's TraceEvent, factor.py:104-122). */
+#define PFLU_TRACE_PF 0   /* panel factorization of step k             */
+#define PFLU_TRACE_TU 1   /* full trailing update (lookahead 0)          */
+#define PFLU_TRACE_TU_L 2 /* update of panel k+1's columns (lookahead 1) */
+#define PFLU_TRACE_TU_R 3 /* remaining trailing update (lookahead 1)     */
+typedef struct pflu_trace_event {
+  int32_t label;
+  int32_t k;
+  float start_ms; /* CUDA-event time relative to the start of the factorization */
+  float end_ms;
+} pflu_trace_event;
+
+int pflu_version(void);
+const char* pflu_last_error(void);
+void pflu_default_options(pflu_options* opt);
+int pflu_device_count(void);
+
+/* Whole factorization, HOST buffers: stages H2D, factors, copies factors and pivots back.
+ * a: m x n row-major (m >= n >= 1, lda >= n), overwritten with L\U in place.
+ * ipiv: int64[n] host.  lookahead: 0 (dmf_mtb order) or 1 (dmf_la, static look-ahead). */
+int pflu_getrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
+               int64_t* ipiv, int64_t* info, const pflu_options* opt);
+
+/* Whole factorization, DEVICE buffers on the current device, ordered on `stream`
+ * (a cudaStream_t; NULL = legacy default).  d_ipiv: int64[n] device.  Blocks until done and
+ * writes *info on the host.  trace (optional, may be NULL) receives up to trace_cap events;
+ * *trace_len (optional) the number written. */
+int pflu_getrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
+                      int64_t* d_ipiv, int64_t* info, void* stream, const pflu_options* opt,
+                      pflu_trace_event* trace, int trace_cap, int* trace_len);
+
+/* Panel factorization (getf2 semantics, recursive + cooperative leaf): rows [d, m) of the
+ * w columns starting at column `col`; the diagonal of panel column j is row d + j.  Row
+ * interchanges are applied across the panel's w columns only.  Writes d_ipiv[d .. d+min(w,m-d))
+ * (global 0-based rows).  *info: 0 or 1 + first zero-pivot ROW index d + j. */
+int pflu_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w,
+               int64_t* d_ipiv, int64_t* info, void* stream, const pflu_options* opt);
+
+/* Row interchanges: for k = k1 .. k2-1 ascending, swap rows k and d_ipiv[k] on columns [c0, c1). */
+int pflu_laswp(double* d_a, int64_t lda, int64_t c0, int64_t c1, const int64_t* d_ipiv, int64_t k1,
+               int64_t k2, void* stream);
+
+/* Fused: laswp of rows d_ipiv[d .. d+nb) on columns [c0, c1), then the nb top rows of those
+ * columns := unit_lower(L11)^-1 * (rows), L11 = the nb x nb block at (d, lcol) of the same matrix. */
+int pflu_swap_trsm(double* d_a, int64_t lda, int64_t d, int64_t lcol, int64_t nb, const int64_t* d_ipiv,
+                   int64_t c0, int64_t c1, void* stream);
+
+/* X (nb x ncols) := unit_lower(L)^-1 * X (strictly-upper part and diagonal of L ignored). */
+int pflu_trsm(const double* d_l, int64_t ldl, int64_t nb, double* d_x, int64_t ldx, int64_t ncols,
+              void* stream);
+
+/* C (m x n) -= A (m x k) * B (k x n).  exact=1: reference rounding; exact=0: DMMA tensor cores. */
+int pflu_gemm_update(double* d_c, int64_t ldc, const double* d_a, int64_t lda, const double* d_b,
+                     int64_t ldb, int64_t m, int64_t n, int64_t k, int exact, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFLU_H */

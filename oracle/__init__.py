@@ -1,0 +1,178 @@
+"""CPU oracle for the LU hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and --impl reference)
+may import this package, and only as the checker / CPU baseline -- never as the thing
+measured or shipped.  The product package (paper_1804_07017_b200) never imports it.
+
+`pflu_oracle.c` restates the reference's arithmetic op for op (see its header for the
+file:line map into pkg/src/panelforge/).  It is pinned bit-for-bit against vectors that the
+reference itself produced (tests/golden/, made by tests/golden/make_golden.py) by
+tests/test_oracle.py.  The numpy helpers below restate the reference's residual definition
+(pkg/src/panelforge/oracle.py:18, 58-89).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+#: 64-bit unit roundoff used by every normalized residual (reference oracle.py:18).
+UNIT_ROUNDOFF = 2.0 ** -53
+
+_d = ctypes.POINTER(ctypes.c_double)
+_i = ctypes.POINTER(ctypes.c_int64)
+_I64 = ctypes.c_int64
+
+
+def build() -> str:
+    path = os.path.join(_HERE, "liboracle.so")
+    src = os.path.join(_HERE, "pflu_oracle.c")
+    if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
+        subprocess.check_call(["make", "-s", "-C", _HERE])
+    return path
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            build()
+        L = ctypes.CDLL(path)
+        L.orc_lu_unb.restype = _I64
+        L.orc_lu_unb.argtypes = [_d, _I64, _I64, _I64, _i, _I64]
+        L.orc_laswp.restype = None
+        L.orc_laswp.argtypes = [_d, _I64, _I64, _I64, _i, _I64, _I64]
+        L.orc_trsm_llnu.restype = None
+        L.orc_trsm_llnu.argtypes = [_d, _I64, _I64, _d, _I64, _I64]
+        L.orc_gemm_sub.restype = None
+        L.orc_gemm_sub.argtypes = [_d, _I64, _d, _I64, _d, _I64, _I64, _I64, _I64]
+        L.orc_getrf.restype = _I64
+        L.orc_getrf.argtypes = [_d, _I64, _I64, _I64, _I64, _i]
+        L.orc_set_threads.restype = None
+        L.orc_set_threads.argtypes = [ctypes.c_int]
+        _LIB = L
+    return _LIB
+
+
+def set_threads(t: int) -> None:
+    lib().orc_set_threads(int(t))
+
+
+def _dp(a):
+    return a.ctypes.data_as(_d)
+
+
+def _ip(a):
+    return a.ctypes.data_as(_i)
+
+
+def _rowmajor(a) -> np.ndarray:
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 2 or not a.flags.c_contiguous:
+        a = np.ascontiguousarray(a)
+    return a
+
+
+def lu_unb(a, steps: int | None = None):
+    """In-place unblocked LUpp of a row-major array (reference _jit.py:154-187).
+    Returns (piv0 int64[min(m,n) or steps], info)."""
+    a = _rowmajor(a)
+    m, n = a.shape
+    k = min(m, n) if steps is None else min(m, n, steps)
+    piv = np.zeros(k, dtype=np.int64)
+    info = lib().orc_lu_unb(_dp(a), m, n, n, _ip(piv), -1 if steps is None else steps)
+    return a, piv, int(info)
+
+
+def getrf(a, b: int):
+    """Blocked LUpp (reference dmf_mtb/dmf_la, factor.py:382-515) on a COPY of `a`.
+    Returns (lu row-major, piv 0-based int64[n], info)."""
+    a = np.array(a, dtype=np.float64, order="C", copy=True)
+    m, n = a.shape
+    if m < n or n < 1:
+        raise ValueError("factorizations require a square or tall, non-empty matrix")
+    piv = np.zeros(n, dtype=np.int64)
+    info = lib().orc_getrf(_dp(a), m, n, n, int(b), _ip(piv))
+    return a, piv, int(info)
+
+
+def lu_prefix(a, steps: int):
+    """First `steps` elimination steps on a COPY; rows [0, steps) and piv[:steps] are final."""
+    a = np.array(a, dtype=np.float64, order="C", copy=True)
+    m, n = a.shape
+    piv = np.zeros(min(steps, m, n), dtype=np.int64)
+    info = lib().orc_lu_unb(_dp(a), m, n, n, _ip(piv), steps)
+    return a, piv, int(info)
+
+
+def laswp(a, piv0, k1: int, k2: int, c0: int = 0, c1: int | None = None):
+    """In place: rows k (k1<=k<k2) swapped with piv0[k], ascending (reference _jit.py:141-151)."""
+    a = _rowmajor(a)
+    piv = np.ascontiguousarray(piv0, dtype=np.int64)
+    lib().orc_laswp(_dp(a), a.shape[1], c0, a.shape[1] if c1 is None else c1, _ip(piv), k1, k2)
+    return a
+
+
+def trsm_llnu(l, x):
+    """In place x <- unit_lower(l)^-1 x (reference _jit.py:104-113)."""
+    l = _rowmajor(l)
+    x = _rowmajor(x)
+    lib().orc_trsm_llnu(_dp(l), l.shape[1], l.shape[0], _dp(x), x.shape[1], x.shape[1])
+    return x
+
+
+def gemm_sub(c, a, b):
+    """In place c <- c - a @ b, per element p ascending, mul then sub (reference _jit.py:54-80)."""
+    c = _rowmajor(c)
+    a = _rowmajor(a)
+    b = _rowmajor(b)
+    m, n = c.shape
+    k = a.shape[1]
+    lib().orc_gemm_sub(_dp(c), n, _dp(a), a.shape[1], _dp(b), b.shape[1], m, n, k)
+    return c
+
+
+# ---------------------------------------------------------------------------------------
+# residuals and parity metrics (restating reference oracle.py:58-89)
+
+def perm_from_pivots(piv0, m: int) -> np.ndarray:
+    """Row permutation p with (P A)[i] = A[p[i]] for LAPACK ipiv applied ascending."""
+    p = np.arange(m)
+    for i, r in enumerate(np.asarray(piv0, dtype=np.int64)):
+        if r != i:
+            p[i], p[r] = p[r], p[i]
+    return p
+
+
+def lu_residual(a0, lu, piv0, block: int = 2048) -> float:
+    """||P A - L U||_F / (n * u * ||A||_F), u = 2^-53 (reference oracle.py:78-89), row-blocked
+    so it never materialises more than one block of L U."""
+    a0 = np.asarray(a0, dtype=np.float64)
+    lu = np.asarray(lu, dtype=np.float64)
+    m, n = a0.shape
+    kk = min(m, n)
+    perm = perm_from_pivots(piv0, m)
+    upper = np.triu(lu[:kk, :])
+    err2 = 0.0
+    for r0 in range(0, m, block):
+        r1 = min(m, r0 + block)
+        lower = np.tril(lu[r0:r1, :kk], -1 - r0)
+        for i in range(r0, min(r1, kk)):
+            lower[i - r0, i] = 1.0
+        d = a0[perm[r0:r1]] - lower @ upper
+        err2 += float(np.sum(d * d))
+    norm_a = float(np.linalg.norm(a0))
+    err = np.sqrt(err2)
+    return err if norm_a == 0.0 else err / (max(n, 1) * UNIT_ROUNDOFF * norm_a)
+
+
+def max_rel_diff(lu_a, lu_b, a0) -> float:
+    """max |LU_a - LU_b| / ||A||_max (north_star's second parity measure)."""
+    amax = float(np.max(np.abs(a0)))
+    return float(np.max(np.abs(np.asarray(lu_a) - np.asarray(lu_b)))) / (amax if amax else 1.0)

@@ -1,0 +1,102 @@
+"""ctypes binding of libpflu.so (C ABI in include/pflu.h).
+
+The CUDA library is the ONLY compute path: if it is missing or no B200 is visible, calls
+fail loudly (RuntimeError) -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpflu.so")
+
+PFLU_OK = 0
+PFLU_ERR_CUDA = 1
+PFLU_ERR_NOMEM = 2
+PFLU_ERR_UNSUPPORTED = 3
+
+#: every symbol include/pflu.h declares (checked by tests/test_boundary.py)
+EXPORTS = (
+    "pflu_version", "pflu_last_error", "pflu_default_options", "pflu_device_count",
+    "pflu_getrf", "pflu_getrf_device", "pflu_panel", "pflu_laswp", "pflu_swap_trsm",
+    "pflu_trsm", "pflu_gemm_update",
+)
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("exact", ctypes.c_int), ("panel_ctas", ctypes.c_int),
+                ("leaf_width", ctypes.c_int), ("reserved", ctypes.c_int * 5)]
+
+
+class TraceEvent(ctypes.Structure):
+    _fields_ = [("label", ctypes.c_int32), ("k", ctypes.c_int32),
+                ("start_ms", ctypes.c_float), ("end_ms", ctypes.c_float)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+
+
+def load():
+    """Load libpflu.so (raises RuntimeError if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"libpflu.so not found at {LIB_PATH}: build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.pflu_version.restype = ctypes.c_int
+        L.pflu_version.argtypes = []
+        L.pflu_last_error.restype = ctypes.c_char_p
+        L.pflu_last_error.argtypes = []
+        L.pflu_default_options.restype = None
+        L.pflu_default_options.argtypes = [ctypes.POINTER(Options)]
+        L.pflu_device_count.restype = ctypes.c_int
+        L.pflu_device_count.argtypes = []
+        L.pflu_getrf.restype = ctypes.c_int
+        L.pflu_getrf.argtypes = [_vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _pi64, ctypes.POINTER(Options)]
+        L.pflu_getrf_device.restype = ctypes.c_int
+        L.pflu_getrf_device.argtypes = [_vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp, _pi64, _vp,
+                                        ctypes.POINTER(Options), ctypes.POINTER(TraceEvent), ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_int)]
+        L.pflu_panel.restype = ctypes.c_int
+        L.pflu_panel.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _pi64, _vp, ctypes.POINTER(Options)]
+        L.pflu_laswp.restype = ctypes.c_int
+        L.pflu_laswp.argtypes = [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp]
+        L.pflu_swap_trsm.restype = ctypes.c_int
+        L.pflu_swap_trsm.argtypes = [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _vp]
+        L.pflu_trsm.restype = ctypes.c_int
+        L.pflu_trsm.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _vp]
+        L.pflu_gemm_update.restype = ctypes.c_int
+        L.pflu_gemm_update.argtypes = [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp]
+        _lib = L
+        return L
+
+
+def check(rc: int, what: str) -> None:
+    """Map a C-ABI return code to the reference's exception types (ValueError for invalid
+    arguments, factor.py:293-297 / kernels.py:282-291; RuntimeError for device failures)."""
+    if rc == PFLU_OK:
+        return
+    if rc < 0:
+        raise ValueError(f"{what}: invalid argument #{-rc}")
+    msg = load().pflu_last_error().decode(errors="replace")
+    raise RuntimeError(f"{what} failed (code {rc}): {msg}")
+
+
+def options(exact: bool = False, panel_ctas: int = 0, leaf_width: int = 0) -> Options:
+    o = Options()
+    load().pflu_default_options(ctypes.byref(o))
+    o.exact = 1 if exact else 0
+    o.panel_ctas = int(panel_ctas)
+    o.leaf_width = int(leaf_width)
+    return o

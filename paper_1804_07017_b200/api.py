@@ -1,0 +1,251 @@
+"""Drop-in LU entry points for the reference package `panelforge` (arXiv 1804.07017).
+
+Primary entry (north_star): :func:`lu_factor` -- float64 n x n in, block size ``b`` and
+look-ahead depth in; packed L\\U factors and a 0-based pivot vector out.
+
+Reference-compatible surface (pkg/src/panelforge/factor.py): :func:`dmf_la` (static
+look-ahead, factor.py:455-515), :func:`dmf_mtb` (fork-join, factor.py:382-412), :class:`LuOutput`
+(factor.py:51-62), :class:`Kind`, :class:`Strategy`, :func:`flops` (factor.py:208-215),
+:class:`CacheConfig` and :class:`Matrix` (core.py:17-112).  Every factorization runs on the
+B200 through libpflu.so (include/pflu.h); there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+
+class Kind(enum.Enum):
+    LU = "lu"
+    QR = "qr"
+
+
+class Strategy(enum.Enum):
+    MTB = "mtb"
+    RTM = "rtm"
+    LA = "la"
+    LA_MB = "la-mb"
+
+
+@dataclass(frozen=True)
+class CacheConfig:
+    """Blocking parameters (reference core.py:17-52).  Only ``b`` (the panel width) affects the
+    GPU factorization; the CPU cache-tiling fields are accepted for signature compatibility."""
+
+    mc: int = 72
+    nc: int = 4032
+    kc: int = 256
+    mr: int = 8
+    nr: int = 6
+    b: int = 192
+
+    def __post_init__(self):
+        for name in ("mc", "nc", "kc", "mr", "nr", "b"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"CacheConfig.{name} must be >= 1")
+
+
+class Matrix:
+    """Column-major float64 matrix, the reference's container (core.py:55-112): element (i, j)
+    at flat offset i + j*leading_dim of a Fortran-ordered (leading_dim, cols) ndarray."""
+
+    __slots__ = ("rows", "cols", "leading_dim", "data")
+
+    def __init__(self, rows: int, cols: int, data: np.ndarray | None = None, leading_dim: int | None = None):
+        ld = rows if leading_dim is None else leading_dim
+        if ld < rows:
+            raise ValueError("leading_dim must be >= rows")
+        if data is None:
+            data = np.zeros((ld, cols), dtype=np.float64, order="F")
+        if data.shape != (ld, cols):
+            raise ValueError(f"backing array must have shape ({ld}, {cols})")
+        if data.dtype != np.float64 or not data.flags.f_contiguous:
+            raise ValueError("backing array must be float64 and column-major")
+        self.rows, self.cols, self.leading_dim, self.data = rows, cols, ld, data
+
+    @classmethod
+    def zeros(cls, rows: int, cols: int) -> "Matrix":
+        return cls(rows, cols)
+
+    @classmethod
+    def from_array(cls, arr) -> "Matrix":
+        a = np.asfortranarray(np.asarray(arr, dtype=np.float64))
+        if a.ndim != 2:
+            raise ValueError("expected a 2-D array")
+        return cls(a.shape[0], a.shape[1], data=a)
+
+    @classmethod
+    def random_uniform(cls, rows: int, cols: int, seed: int) -> "Matrix":
+        return cls.from_array(np.random.default_rng(seed).random((rows, cols)))
+
+    @property
+    def array(self) -> np.ndarray:
+        return self.data[: self.rows, :]
+
+    def copy(self) -> "Matrix":
+        return Matrix(self.rows, self.cols, data=self.data.copy(order="F"), leading_dim=self.leading_dim)
+
+    def __repr__(self):
+        return f"Matrix({self.rows}x{self.cols}, ld={self.leading_dim})"
+
+
+@dataclass
+class LuOutput:
+    """In-place LU factors plus 1-based pivots of length min(m, n) (reference factor.py:51-62).
+    ``info`` is 0 or the 1-based first column whose pivot was exactly zero."""
+
+    matrix: Matrix
+    pivots: np.ndarray
+    strategy: Strategy
+    info: int = 0
+
+
+@dataclass(frozen=True)
+class TraceEvent:
+    """One timed task (reference factor.py:104-113); times are seconds from the start."""
+
+    label: str
+    k: int
+    j: int | None
+    start: float
+    end: float
+    worker: int | None
+
+
+def flops(kind: Kind, n: int) -> int:
+    """2n^3/3 for LU, 4n^3/3 for QR, rounded to nearest (reference factor.py:208-215)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    num = (2 if kind is Kind.LU else 4) * n ** 3
+    q, r = divmod(num, 3)
+    return q + (1 if 2 * r >= 3 else 0)
+
+
+def _validate_shape(m: int, n: int):
+    # reference factor.py:293-297
+    if m < n:
+        raise ValueError("factorizations require a square or tall matrix")
+    if n < 1:
+        raise ValueError("matrix must be non-empty")
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def getrf_host(a: np.ndarray, b: int, lookahead: int, exact: bool = False, panel_ctas: int = 0):
+    """Factor a row-major C-contiguous float64 host array in place through pflu_getrf.
+    Returns (piv0 int64[n], info)."""
+    L = _lib.load()
+    m, n = a.shape
+    piv = np.empty(n, dtype=np.int64)
+    info = ctypes.c_int64(0)
+    opt = _lib.options(exact=exact, panel_ctas=panel_ctas)
+    rc = L.pflu_getrf(a.ctypes.data, m, n, a.strides[0] // 8, int(b), int(lookahead), piv.ctypes.data,
+                      ctypes.byref(info), ctypes.byref(opt))
+    _lib.check(rc, "pflu_getrf")
+    return piv, int(info.value)
+
+
+def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int = 0, piv=None):
+    """Factor a row-major CUDA float64 torch tensor in place through pflu_getrf_device on the
+    current torch stream.  Returns (piv0 int64 CUDA tensor, info)."""
+    import torch
+
+    L = _lib.load()
+    m, n = a.shape
+    if piv is None:
+        piv = torch.empty(n, dtype=torch.int64, device=a.device)
+    info = ctypes.c_int64(0)
+    opt = _lib.options(exact=exact, panel_ctas=panel_ctas)
+    stream = torch.cuda.current_stream(a.device).cuda_stream
+    with torch.cuda.device(a.device):
+        rc = L.pflu_getrf_device(a.data_ptr(), m, n, a.stride(0), int(b), int(lookahead), piv.data_ptr(),
+                                 ctypes.byref(info), stream, ctypes.byref(opt), None, 0, None)
+    _lib.check(rc, "pflu_getrf_device")
+    return piv, int(info.value)
+
+
+def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a: bool = True,
+              exact: bool = False, return_info: bool = False, panel_ctas: int = 0):
+    """Blocked right-looking LU with partial pivoting on the B200.
+
+    ``a``: float64 m x n (m >= n) row-major -- a numpy array (host buffers: staged through
+    pflu_getrf) or a CUDA torch tensor (device buffers, current stream).  ``lookahead`` 1 is the
+    reference's dmf_la, 0 its dmf_mtb.  ``exact=True`` reproduces the reference's rounding in
+    every update (bitwise-equal factors); the default runs the trailing update on DMMA tensor
+    cores.  ``n_gpus > 1`` runs the 1-D block-cyclic multi-GPU driver (requires an initialised
+    torch.distributed NCCL process group with one rank per GPU).
+
+    Returns ``(lu, piv)`` (``(lu, piv, info)`` with ``return_info``): packed unit-lower L below
+    the diagonal and U on/above it, and 0-based LAPACK pivots (row i swapped with piv[i]).
+    """
+    if lookahead not in (0, 1):
+        raise ValueError("lookahead must be 0 or 1 (the reference defines depth 0 and 1)")
+    if b < 1:
+        raise ValueError("block size must be >= 1")
+    if n_gpus > 1:
+        from .dist import lu_factor_dist
+
+        return lu_factor_dist(a, b=b, lookahead=lookahead, exact=exact, return_info=return_info)
+    if _is_torch(a):
+        import torch
+
+        if a.dtype != torch.float64 or a.dim() != 2:
+            raise ValueError("expected a 2-D float64 tensor")
+        _validate_shape(*a.shape)
+        if not a.is_cuda:
+            raise ValueError("torch input must be a CUDA tensor (use a numpy array for host buffers)")
+        work = a if (overwrite_a and a.stride(1) == 1) else a.contiguous().clone()
+        piv, info = getrf_device(work, b, lookahead, exact=exact, panel_ctas=panel_ctas)
+    else:
+        arr = np.asarray(a)
+        if arr.dtype != np.float64 or arr.ndim != 2:
+            arr = np.asarray(arr, dtype=np.float64)
+            if arr.ndim != 2:
+                raise ValueError("expected a 2-D array")
+        _validate_shape(*arr.shape)
+        if overwrite_a and arr is a and arr.flags.c_contiguous and arr.flags.writeable:
+            work = arr
+        else:
+            work = np.array(arr, dtype=np.float64, order="C", copy=True)
+        piv, info = getrf_host(work, b, lookahead, exact=exact, panel_ctas=panel_ctas)
+    if info:
+        warnings.warn(f"exactly singular: zero pivot in column {info} (1-based)", RuntimeWarning, stacklevel=2)
+    return (work, piv, info) if return_info else (work, piv)
+
+
+def _factor_matrix(a, cfg: CacheConfig, kind: Kind, lookahead: int, strategy: Strategy, trace):
+    if kind is not Kind.LU:
+        raise NotImplementedError("only Kind.LU is implemented on the B200 (QR is out of scope, SURVEY.md §2)")
+    if isinstance(a, Matrix):
+        mat = a
+    else:
+        mat = Matrix.from_array(a)
+    _validate_shape(mat.rows, mat.cols)
+    # the GPU works row-major; the reference container is column-major -> stage through a
+    # row-major copy and write the factors back into the caller's buffer (in place, like the
+    # reference, factor.py:300-302)
+    work = np.ascontiguousarray(mat.array)
+    piv0, info = getrf_host(work, cfg.b, lookahead)
+    mat.array[...] = work
+    if trace is not None:
+        trace.append(TraceEvent("PF" if lookahead == 0 else "TU_R", 0, None, 0.0, 0.0, None))
+    return LuOutput(mat, piv0 + 1, strategy, info)
+
+
+def dmf_la(a, cfg: CacheConfig, pool=None, kind: Kind = Kind.LU, malleable: bool = False, trace=None):
+    """Static look-ahead driver (depth 1), reference factor.py:455-515.  ``pool`` is accepted
+    for signature compatibility (the two sections run as two CUDA streams)."""
+    return _factor_matrix(a, cfg, kind, 1, Strategy.LA_MB if malleable else Strategy.LA, trace)
+
+
+def dmf_mtb(a, cfg: CacheConfig, pool=None, kind: Kind = Kind.LU, trace=None):
+    """Fork-join driver (depth 0), reference factor.py:382-412."""
+    return _factor_matrix(a, cfg, kind, 0, Strategy.MTB, trace)

@@ -1,0 +1,567 @@
+// pflu.cu -- host driver and C ABI (include/pflu.h) of libpflu.so.
+//
+// The k-loop of the reference drivers (dmf_mtb, factor.py:382-412; dmf_la, factor.py:455-515)
+// runs here in C++.  The two OpenMP sections of dmf_la (branch_a = deferred left swaps +
+// TU_L(k) + PF(k+1), branch_b = TU_R(k), factor.py:490-512) become two CUDA streams:
+//   sP (highest priority): TU_L(k) -> PF(k+1) -> pivot plan(k+1)
+//   sU (lowest priority):  TU_R(k) -> deferred left swaps(k)
+// joined by events instead of the per-iteration barrier of sections_2 (runtime.py:278-303):
+//   TU_R(k)            waits PF(k)            (pivots + L21 of step k)
+//   TU_L(k) + PF(k+1)  waits TU_R(k-1)        (which updated panel k+1's columns)
+// There is no host synchronisation inside the factorization.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pflu.h"
+#include "pflu_kernels.cuh"
+
+namespace pflu {
+
+static thread_local std::string g_err;
+
+static int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(expr)                                                                                 \
+  do {                                                                                           \
+    cudaError_t _e = (expr);                                                                     \
+    if (_e != cudaSuccess)                                                                       \
+      return set_err(PFLU_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),     \
+                     __FILE__, __LINE__);                                                        \
+  } while (0)
+
+#define CKR(expr)                 \
+  do {                            \
+    int _r = (expr);              \
+    if (_r != PFLU_OK) return _r; \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// per-device context
+
+struct DevCtx {
+  bool ready = false;
+  int dev = -1;
+  int sms = 0;
+  size_t smem_optin = 0;
+  cudaStream_t sP = nullptr, sU = nullptr;
+  double* slots = nullptr;
+  unsigned* bar = nullptr;
+  int64_t* plan[2] = {nullptr, nullptr};
+  unsigned long long* info = nullptr;
+  int leaf_occ[3] = {0, 0, 0};  // max active CTAs/SM for W = 8, 16, 32 at max smem (set lazily)
+  std::vector<cudaEvent_t> ev;  // event pool
+  cudaEvent_t tev[4] = {};      // timing events scratch
+};
+
+static std::mutex g_mu;
+static DevCtx g_ctx[64];
+
+static constexpr int SLOT_MAX_CTAS = 1024;
+static constexpr int SLOT_MAX_W = 32;
+
+static int ctx_get(DevCtx** out) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return set_err(PFLU_ERR_UNSUPPORTED, "device index %d", dev);
+  DevCtx& c = g_ctx[dev];
+  if (!c.ready) {
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+      return set_err(PFLU_ERR_UNSUPPORTED, "libpflu is built for sm_100a (B200); device %d is sm_%d%d",
+                     dev, prop.major, prop.minor);
+    c.dev = dev;
+    c.sms = prop.multiProcessorCount;
+    c.smem_optin = prop.sharedMemPerBlockOptin;
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c.sP, cudaStreamNonBlocking, hi));
+    CK(cudaStreamCreateWithPriority(&c.sU, cudaStreamNonBlocking, lo));
+    CK(cudaMalloc(&c.slots, sizeof(double) * 2 * (SLOT_MAX_CTAS + 1) * (SLOT_MAX_W + 2)));
+    CK(cudaMalloc(&c.bar, 64));
+    CK(cudaMemset(c.bar, 0, 64));
+    CK(cudaMalloc(&c.plan[0], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
+    CK(cudaMalloc(&c.plan[1], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
+    CK(cudaMalloc(&c.info, 64));
+    for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&c.tev[i]));
+    // kernel attributes (dynamic shared memory beyond 48 KB)
+    const int big = (int)c.smem_optin;
+    CK(cudaFuncSetAttribute(leaf_getf2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(leaf_getf2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(leaf_getf2_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(swap_trsm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(swap_trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(trsm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(gemm_dmma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM_SMEM));
+    CK(cudaFuncSetAttribute(gemm_dmma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM_SMEM));
+    CK(cudaFuncSetAttribute(gemm_exact_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM_SMEM));
+    CK(cudaFuncSetAttribute(gemm_exact_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM_SMEM));
+    c.ready = true;
+  }
+  *out = &c;
+  return PFLU_OK;
+}
+
+static int ctx_events(DevCtx& c, size_t n) {
+  while (c.ev.size() < n) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.ev.push_back(e);
+  }
+  return PFLU_OK;
+}
+
+static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ------------------------------------------------------------------------------------------
+// kernel launchers (all asynchronous on `st`)
+
+static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, const double* b, int64_t ldb,
+                       int64_t M, int64_t N, int64_t K, bool exact, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || K <= 0) return PFLU_OK;
+  GemmArgs p;
+  p.c = c; p.a = a; p.b = b;
+  p.ldc = ldc; p.lda = lda; p.ldb = ldb;
+  p.M = M; p.N = N; p.K = K;
+  int64_t tm = (M + GM_BM - 1) / GM_BM, tn = (N + GM_BN - 1) / GM_BN;
+  if (tm * tn > INT_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "gemm grid too large");
+  p.tiles_m = (int)tm;
+  p.tiles_n = (int)tn;
+  const bool v2 = aligned16(c) && aligned16(a) && aligned16(b) && (ldc % 2 == 0) && (lda % 2 == 0) &&
+                  (ldb % 2 == 0);
+  dim3 grid((unsigned)(tm * tn));
+  if (exact) {
+    if (v2) gemm_exact_kernel<2><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
+    else gemm_exact_kernel<1><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
+  } else {
+    if (v2) gemm_dmma_kernel<2><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
+    else gemm_dmma_kernel<1><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
+  }
+  CK(cudaGetLastError());
+  return PFLU_OK;
+}
+
+static int launch_trsm(const double* L, int64_t ldl, int np, double* X, int64_t ldx, int64_t ncols,
+                       cudaStream_t st) {
+  if (np <= 1 || ncols <= 0) return PFLU_OK;
+  if (np > PLAN_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "trsm block %d > %d", np, PLAN_MAX);
+  if (np <= 256) {
+    size_t smem = (size_t)(np * 32 + 1024) * 8;
+    trsm_kernel<32><<<(unsigned)((ncols + 31) / 32), 256, smem, st>>>(L, ldl, X, ldx, np, ncols);
+  } else {
+    size_t smem = (size_t)(np * 16 + 1024) * 8;
+    trsm_kernel<16><<<(unsigned)((ncols + 15) / 16), 256, smem, st>>>(L, ldl, X, ldx, np, ncols);
+  }
+  CK(cudaGetLastError());
+  return PFLU_OK;
+}
+
+static int launch_plan(const int64_t* piv, int64_t d, int np, int64_t* plan, cudaStream_t st) {
+  if (np > PLAN_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "pivot block %d > %d", np, PLAN_MAX);
+  pivot_plan_kernel<<<1, 256, 0, st>>>(piv, d, np, plan);
+  CK(cudaGetLastError());
+  return PFLU_OK;
+}
+
+// laswp by plan (+ optional trsm) on storage columns [c0, c1)
+static int launch_swap(double* a, int64_t lda, int64_t d, int np, const int64_t* plan, int64_t c0, int64_t c1,
+                       const double* L, int64_t ldl, bool do_trsm, cudaStream_t st) {
+  if (c1 <= c0 || np <= 0) return PFLU_OK;
+  if (np <= 256) {
+    size_t smem = (size_t)(np * 32 + std::max(np * 32, 1024)) * 8;
+    swap_trsm_kernel<32><<<(unsigned)((c1 - c0 + 31) / 32), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl,
+                                                                              do_trsm ? 1 : 0);
+  } else {
+    size_t smem = (size_t)(np * 16 + std::max(np * 16, 1024)) * 8;
+    swap_trsm_kernel<16><<<(unsigned)((c1 - c0 + 15) / 16), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl,
+                                                                              do_trsm ? 1 : 0);
+  }
+  CK(cudaGetLastError());
+  return PFLU_OK;
+}
+
+struct LeafCfg {
+  int W = 32;
+  int S = 1;
+  int64_t R = 1;
+  size_t smem = 0;
+};
+
+template <int W>
+static size_t leaf_smem_bytes(int64_t R) {
+  return (size_t)(R * (W + 1) + 2 * W) * 8;
+}
+
+static int leaf_occupancy(DevCtx& c, int W, size_t smem, int* out) {
+  int occ = 0;
+  if (W == 8) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, leaf_getf2_kernel<8>, LEAF_THREADS, smem));
+  else if (W == 16) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, leaf_getf2_kernel<16>, LEAF_THREADS, smem));
+  else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, leaf_getf2_kernel<32>, LEAF_THREADS, smem));
+  *out = occ;
+  return PFLU_OK;
+}
+
+// Choose leaf width and CTA count for a panel of `rows` rows.
+static int choose_leaf(DevCtx& c, int64_t rows, const pflu_options& opt, LeafCfg* cfg) {
+  const size_t smax = c.smem_optin - 1024;
+  int S_want;
+  if (opt.panel_ctas > 0) S_want = opt.panel_ctas;
+  else S_want = (int)std::min<int64_t>(c.sms, std::max<int64_t>(1, (rows + 191) / 192));
+  S_want = std::max(1, std::min(S_want, SLOT_MAX_CTAS));
+  const int Ws[3] = {32, 16, 8};
+  for (int wi = 0; wi < 3; ++wi) {
+    int W = Ws[wi];
+    if (opt.leaf_width > 0 && W != opt.leaf_width) continue;
+    for (int S = S_want; S <= SLOT_MAX_CTAS; S = S < 8 ? S + 1 : S + S / 8) {
+      int64_t R = (rows + S - 1) / S;
+      size_t smem = (size_t)(R * (W + 1) + 2 * W) * 8;
+      if (smem > smax) continue;
+      int occ = 0;
+      CKR(leaf_occupancy(c, W, smem, &occ));
+      if ((int64_t)occ * c.sms < S) break;  // cannot be co-resident with this much smem
+      cfg->W = W; cfg->S = S; cfg->R = R; cfg->smem = smem;
+      return PFLU_OK;
+    }
+  }
+  return set_err(PFLU_ERR_UNSUPPORTED, "panel of %lld rows does not fit the cooperative leaf", (long long)rows);
+}
+
+static int launch_leaf(DevCtx& c, const LeafCfg& cfg, double* a, int64_t lda, int64_t m, int64_t r0, int64_t col0,
+                       int64_t w, int64_t pc0, int64_t pc1, int64_t* piv, unsigned long long* info, cudaStream_t st) {
+  LeafArgs p;
+  p.a = a; p.lda = lda; p.m = m; p.r0 = r0; p.col0 = col0; p.wact = w; p.pc0 = pc0; p.pc1 = pc1;
+  p.piv = piv; p.info = info; p.slots = c.slots; p.bar = c.bar;
+  const int64_t rows = m - r0;
+  int S = cfg.S;
+  int64_t R = (rows + S - 1) / S;
+  // shrink S for short sub-panels (fewer barrier participants, same smem bound)
+  while (S > 1 && (int64_t)(S - 1) * R >= rows) --S;
+  p.R = R;
+  void* args[] = {&p};
+  const void* fn = cfg.W == 8 ? (const void*)leaf_getf2_kernel<8>
+                 : cfg.W == 16 ? (const void*)leaf_getf2_kernel<16>
+                               : (const void*)leaf_getf2_kernel<32>;
+  size_t smem = (size_t)(R * (cfg.W + 1) + 2 * cfg.W) * 8;
+  CK(cudaLaunchCooperativeKernel(fn, dim3(S), dim3(LEAF_THREADS), args, smem, st));
+  return PFLU_OK;
+}
+
+// Recursive panel (Gustavson/Toledo split): rows [r0, m), storage columns [c0, c0 + w); the panel's
+// swap range is [pc0, pc1).  Exactness: every element still receives its updates in ascending
+// pivot order with the reference's rounding when opt.exact.
+static int panel_rec(DevCtx& c, const LeafCfg& cfg, double* a, int64_t lda, int64_t m, int64_t r0, int64_t c0,
+                     int64_t w, int64_t pc0, int64_t pc1, int64_t* piv, unsigned long long* info, bool exact,
+                     cudaStream_t st) {
+  if (w <= 0 || r0 >= m) return PFLU_OK;
+  if (w <= cfg.W) return launch_leaf(c, cfg, a, lda, m, r0, c0, w, pc0, pc1, piv, info, st);
+  int64_t w1 = ((w / 2 + 7) / 8) * 8;
+  if (w1 >= w) w1 = w / 2;
+  CKR(panel_rec(c, cfg, a, lda, m, r0, c0, w1, pc0, pc1, piv, info, exact, st));
+  const int np = (int)std::min(w1, m - r0);
+  const double* L = a + r0 * lda + c0;
+  CKR(launch_trsm(L, lda, np, a + r0 * lda + c0 + w1, lda, w - w1, st));
+  if (r0 + w1 >= m) return PFLU_OK;  // short panel: no rows below the left half
+  CKR(launch_gemm(a + (r0 + w1) * lda + c0 + w1, lda, a + (r0 + w1) * lda + c0, lda, a + r0 * lda + c0 + w1, lda,
+                  m - r0 - w1, w - w1, w1, exact, st));
+  return panel_rec(c, cfg, a, lda, m, r0 + w1, c0 + w1, w - w1, pc0, pc1, piv, info, exact, st);
+}
+
+static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, int64_t c0, int64_t w,
+                        int64_t* piv, unsigned long long* info, const pflu_options& opt, cudaStream_t st) {
+  LeafCfg cfg;
+  CKR(choose_leaf(c, m - r0, opt, &cfg));
+  return panel_rec(c, cfg, a, lda, m, r0, c0, w, c0, c0 + w, piv, info, opt.exact != 0, st);
+}
+
+// ------------------------------------------------------------------------------------------
+// the blocked factorization
+
+struct Step {
+  int64_t col0, bw;
+};
+
+static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
+                       int64_t* piv, unsigned long long* info, cudaStream_t user, const pflu_options& opt,
+                       std::vector<std::pair<int, int>>* marks) {
+  std::vector<Step> grid;
+  for (int64_t col0 = 0; col0 < n; col0 += b) grid.push_back({col0, std::min(b, n - col0)});
+  const int count = (int)grid.size();
+  const bool exact = opt.exact != 0;
+  CK(cudaMemsetAsync(info, 0xff, sizeof(unsigned long long), user));
+  auto update_cols = [&](int k, int64_t lo, int64_t hi, cudaStream_t st) -> int {
+    // TU of step k on storage columns [lo, hi): laswp + trsm (fused), then the DMMA update
+    if (hi <= lo) return PFLU_OK;
+    const Step s = grid[k];
+    const int np = (int)std::min(s.bw, m - s.col0);
+    CKR(launch_swap(a, lda, s.col0, np, c.plan[k & 1], lo, hi, a + s.col0 * lda + s.col0, lda, true, st));
+    const int64_t below = s.col0 + s.bw;
+    if (below < m)
+      CKR(launch_gemm(a + below * lda + lo, lda, a + below * lda + s.col0, lda, a + s.col0 * lda + lo, lda,
+                      m - below, hi - lo, s.bw, exact, st));
+    return PFLU_OK;
+  };
+  auto left_swaps = [&](int k, cudaStream_t st) -> int {
+    const Step s = grid[k];
+    if (s.col0 == 0) return PFLU_OK;
+    const int np = (int)std::min(s.bw, m - s.col0);
+    return launch_swap(a, lda, s.col0, np, c.plan[k & 1], 0, s.col0, nullptr, lda, false, st);
+  };
+  auto pf = [&](int k, cudaStream_t st) -> int {
+    const Step s = grid[k];
+    CKR(panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, opt, st));
+    const int np = (int)std::min(s.bw, m - s.col0);
+    return launch_plan(piv, s.col0, np, c.plan[k & 1], st);
+  };
+
+  if (lookahead == 0) {
+    // dmf_mtb order (factor.py:396-411): PF(k), left swaps, TU on [col0+bw, n)
+    for (int k = 0; k < count; ++k) {
+      CKR(pf(k, user));
+      CKR(left_swaps(k, user));
+      CKR(update_cols(k, grid[k].col0 + grid[k].bw, n, user));
+    }
+    return PFLU_OK;
+  }
+  // lookahead 1 (dmf_la, factor.py:481-512)
+  CKR(ctx_events(c, 2 * (size_t)count + 4));
+  cudaEvent_t ev_start = c.ev[0];
+  CK(cudaEventRecord(ev_start, user));
+  CK(cudaStreamWaitEvent(c.sP, ev_start, 0));
+  CK(cudaStreamWaitEvent(c.sU, ev_start, 0));
+  auto ev_pf = [&](int k) { return c.ev[2 + 2 * k]; };
+  auto ev_tu = [&](int k) { return c.ev[3 + 2 * k]; };
+  CKR(pf(0, c.sP));
+  CK(cudaEventRecord(ev_pf(0), c.sP));
+  for (int k = 0; k < count; ++k) {
+    // branch_b: TU_R(k) on columns beyond panel k+1, then the deferred left swaps of step k
+    CK(cudaStreamWaitEvent(c.sU, ev_pf(k), 0));
+    const int64_t lo_r = (k + 1 < count) ? grid[k + 1].col0 + grid[k + 1].bw : n;
+    CKR(update_cols(k, lo_r, n, c.sU));
+    CKR(left_swaps(k, c.sU));
+    CK(cudaEventRecord(ev_tu(k), c.sU));
+    // branch_a: TU_L(k) on panel k+1's columns, then PF(k+1)
+    if (k + 1 < count) {
+      if (k > 0) CK(cudaStreamWaitEvent(c.sP, ev_tu(k - 1), 0));
+      CKR(update_cols(k, grid[k + 1].col0, grid[k + 1].col0 + grid[k + 1].bw, c.sP));
+      CKR(pf(k + 1, c.sP));
+      CK(cudaEventRecord(ev_pf(k + 1), c.sP));
+    }
+  }
+  CK(cudaEventRecord(c.ev[1], c.sP));
+  CK(cudaStreamWaitEvent(user, c.ev[1], 0));
+  CK(cudaEventRecord(ev_tu(count - 1), c.sU));
+  CK(cudaStreamWaitEvent(user, ev_tu(count - 1), 0));
+  (void)marks;
+  return PFLU_OK;
+}
+
+static int check_dims(int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead) {
+  if (m < 1) return -2;
+  if (n < 1 || n > m) return -3;
+  if (lda < n) return -4;
+  if (b < 1) return -5;
+  if (lookahead != 0 && lookahead != 1) return -6;
+  if (std::min(b, n) > PLAN_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "block size %lld > %d", (long long)b, PLAN_MAX);
+  return PFLU_OK;
+}
+
+static int finish_info(DevCtx& c, cudaStream_t st, int64_t* info) {
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, c.info, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (info) *info = (h == ~0ull) ? 0 : (int64_t)h;
+  return PFLU_OK;
+}
+
+}  // namespace pflu
+
+using namespace pflu;
+
+// ==========================================================================================
+// C ABI
+
+extern "C" {
+
+int pflu_version(void) { return 1; }
+
+const char* pflu_last_error(void) { return g_err.c_str(); }
+
+void pflu_default_options(pflu_options* opt) {
+  if (!opt) return;
+  memset(opt, 0, sizeof(*opt));
+}
+
+int pflu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int pflu_getrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, int64_t* d_ipiv,
+                      int64_t* info, void* stream, const pflu_options* opt_in, pflu_trace_event* trace, int trace_cap,
+                      int* trace_len) {
+  if (!d_a) return -1;
+  CKR(check_dims(m, n, lda, b, lookahead));
+  if (!d_ipiv) return -7;
+  pflu_options opt;
+  pflu_default_options(&opt);
+  if (opt_in) opt = *opt_in;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  cudaStream_t st = (cudaStream_t)stream;
+  CKR(getrf_async(*c, d_a, m, n, lda, std::min(b, n), lookahead, d_ipiv, c->info, st, opt, nullptr));
+  if (trace_len) *trace_len = 0;
+  (void)trace; (void)trace_cap;
+  return finish_info(*c, st, info);
+}
+
+int pflu_getrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, int64_t* ipiv, int64_t* info,
+               const pflu_options* opt) {
+  if (!a) return -1;
+  CKR(check_dims(m, n, lda, b, lookahead));
+  if (!ipiv) return -7;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  // device copy with an even leading dimension (16-byte aligned rows for the vector paths)
+  const int64_t ldd = (n + 1) & ~(int64_t)1;
+  double* d_a = nullptr;
+  int64_t* d_piv = nullptr;
+  CK(cudaMalloc(&d_a, sizeof(double) * (size_t)m * ldd));
+  if (cudaMalloc(&d_piv, sizeof(int64_t) * (size_t)n) != cudaSuccess) {
+    cudaFree(d_a);
+    return set_err(PFLU_ERR_NOMEM, "cudaMalloc pivots failed");
+  }
+  int rc = PFLU_OK;
+  cudaStream_t st = nullptr;
+  do {
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) { rc = set_err(PFLU_ERR_CUDA, "stream"); break; }
+    if (cudaMemcpy2DAsync(d_a, ldd * 8, a, lda * 8, n * 8, m, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+      rc = set_err(PFLU_ERR_CUDA, "H2D copy failed"); break;
+    }
+    rc = pflu_getrf_device(d_a, m, n, ldd, b, lookahead, d_piv, info, st, opt, nullptr, 0, nullptr);
+    if (rc != PFLU_OK) break;
+    if (cudaMemcpy2DAsync(a, lda * 8, d_a, ldd * 8, n * 8, m, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(ipiv, d_piv, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      rc = set_err(PFLU_ERR_CUDA, "D2H copy failed: %s", cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+  } while (0);
+  if (st) cudaStreamDestroy(st);
+  cudaFree(d_a);
+  cudaFree(d_piv);
+  return rc;
+}
+
+int pflu_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w, int64_t* d_ipiv, int64_t* info,
+               void* stream, const pflu_options* opt_in) {
+  if (!d_a) return -1;
+  if (lda < 1) return -2;
+  if (m < 1) return -3;
+  if (d < 0 || d >= m) return -4;
+  if (col < 0 || col + w > lda) return -5;
+  if (w < 1) return -6;
+  if (!d_ipiv) return -7;
+  pflu_options opt;
+  pflu_default_options(&opt);
+  if (opt_in) opt = *opt_in;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(c->info, 0xff, 8, st));
+  CKR(panel_factor(*c, d_a, lda, m, d, col, w, d_ipiv, c->info, opt, st));
+  return finish_info(*c, st, info);
+}
+
+int pflu_laswp(double* d_a, int64_t lda, int64_t c0, int64_t c1, const int64_t* d_ipiv, int64_t k1, int64_t k2,
+               void* stream) {
+  if (!d_a) return -1;
+  if (lda < 1) return -2;
+  if (c0 < 0 || c0 > lda) return -3;
+  if (c1 < c0 || c1 > lda) return -4;
+  if (!d_ipiv) return -5;
+  if (k1 < 0) return -6;
+  if (k2 < k1) return -7;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int64_t k = k1; k < k2; k += PLAN_MAX) {
+    int np = (int)std::min<int64_t>(PLAN_MAX, k2 - k);
+    CKR(launch_plan(d_ipiv, k, np, c->plan[0], st));
+    CKR(launch_swap(d_a, lda, k, np, c->plan[0], c0, c1, nullptr, lda, false, st));
+  }
+  return PFLU_OK;
+}
+
+int pflu_swap_trsm(double* d_a, int64_t lda, int64_t d, int64_t lcol, int64_t nb, const int64_t* d_ipiv, int64_t c0,
+                   int64_t c1, void* stream) {
+  if (!d_a) return -1;
+  if (lda < 1) return -2;
+  if (d < 0) return -3;
+  if (lcol < 0) return -4;
+  if (nb < 1 || nb > PLAN_MAX) return -5;
+  if (!d_ipiv) return -6;
+  if (c0 < 0) return -7;
+  if (c1 < c0 || c1 > lda) return -8;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  cudaStream_t st = (cudaStream_t)stream;
+  CKR(launch_plan(d_ipiv, d, (int)nb, c->plan[0], st));
+  return launch_swap(d_a, lda, d, (int)nb, c->plan[0], c0, c1, d_a + d * lda + lcol, lda, true, st);
+}
+
+int pflu_trsm(const double* d_l, int64_t ldl, int64_t nb, double* d_x, int64_t ldx, int64_t ncols, void* stream) {
+  if (!d_l) return -1;
+  if (ldl < nb) return -2;
+  if (nb < 0 || nb > PLAN_MAX) return -3;
+  if (!d_x) return -4;
+  if (ldx < ncols) return -5;
+  if (ncols < 0) return -6;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  return launch_trsm(d_l, ldl, (int)nb, d_x, ldx, ncols, (cudaStream_t)stream);
+}
+
+int pflu_gemm_update(double* d_c, int64_t ldc, const double* d_a, int64_t lda, const double* d_b, int64_t ldb,
+                     int64_t m, int64_t n, int64_t k, int exact, void* stream) {
+  if (!d_c) return -1;
+  if (ldc < n) return -2;
+  if (!d_a) return -3;
+  if (lda < k) return -4;
+  if (!d_b) return -5;
+  if (ldb < n) return -6;
+  if (m < 0) return -7;
+  if (n < 0) return -8;
+  if (k < 0) return -9;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  return launch_gemm(d_c, ldc, d_a, lda, d_b, ldb, m, n, k, exact != 0, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,202 @@
+"""Kernel-level parity of the sm_100a kernels against the pinned CPU oracle (GPU box).
+
+Every kernel that runs in the reference's rounding (laswp, trsm, panel, exact GEMM) must be
+BITWISE equal to the oracle; the DMMA GEMM must match within the FP64 accumulation bound
+|dC| <= 2 k u sum|a||b| (stated per test).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import bitwise_equal
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+
+
+def _lib():
+    from paper_1804_07017_b200 import _lib
+
+    return _lib
+
+
+def _t(x, dev):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+
+def _stream():
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _sync():
+    import torch
+
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (45, 38, 19), (128, 64, 16), (257, 131, 37), (1000, 700, 256),
+                                   (300, 4, 5), (3, 500, 64)])
+@pytest.mark.parametrize("exact", [True, False])
+def test_gemm_update(cuda, m, n, k, exact):
+    rng = np.random.default_rng(m * 7 + n * 3 + k)
+    c0 = rng.standard_normal((m, n))
+    a0 = rng.standard_normal((m, k))
+    b0 = rng.standard_normal((k, n))
+    want = oracle.gemm_sub(c0.copy(), a0, b0)
+    c, a, b = _t(c0, cuda), _t(a0, cuda), _t(b0, cuda)
+    L = _lib().load()
+    rc = L.pflu_gemm_update(c.data_ptr(), n, a.data_ptr(), k, b.data_ptr(), n, m, n, k, int(exact), _stream())
+    _lib().check(rc, "gemm")
+    got = c.cpu().numpy()
+    if exact:
+        assert bitwise_equal(got, want)
+    else:
+        bound = 2 * k * U * (np.abs(a0) @ np.abs(b0)) + 4 * U * np.abs(c0)
+        assert np.all(np.abs(got - want) <= bound)
+
+
+def test_gemm_update_strided_unaligned(cuda):
+    # odd leading dimensions and offsets force the 8-byte cp.async path
+    rng = np.random.default_rng(3)
+    big = rng.standard_normal((301, 211))
+    want = big.copy()
+    oracle.gemm_sub(want[40:301, 21:200], np.ascontiguousarray(want[40:301, 1:18]), np.ascontiguousarray(want[3:20, 21:200]))
+    # oracle on views needs contiguous copies -> recompute directly
+    want = big.copy()
+    cv = want[40:301, 21:200].copy()
+    oracle.gemm_sub(cv, big[40:301, 1:18].copy(), big[3:20, 21:200].copy())
+    want[40:301, 21:200] = cv
+    g = _t(big, cuda)
+    L = _lib().load()
+    base = g.data_ptr()
+    ld = 211
+    rc = L.pflu_gemm_update(base + (40 * ld + 21) * 8, ld, base + (40 * ld + 1) * 8, ld, base + (3 * ld + 21) * 8, ld,
+                            261, 179, 17, 1, _stream())
+    _lib().check(rc, "gemm")
+    assert bitwise_equal(g.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("nb,ncols", [(1, 5), (2, 3), (24, 37), (64, 1000), (256, 300), (512, 100), (130, 77)])
+def test_trsm_bitwise(cuda, nb, ncols):
+    rng = np.random.default_rng(nb + ncols)
+    l0 = rng.standard_normal((nb, nb))
+    x0 = rng.standard_normal((nb, ncols))
+    want = oracle.trsm_llnu(l0, x0.copy())
+    l, x = _t(l0, cuda), _t(x0, cuda)
+    rc = _lib().load().pflu_trsm(l.data_ptr(), nb, nb, x.data_ptr(), ncols, ncols, _stream())
+    _lib().check(rc, "trsm")
+    assert bitwise_equal(x.cpu().numpy(), want)
+
+
+def test_trsm_known_answer(cuda):
+    # reference test_kernels.py:241-286: L=[[1,0],[2,1]], x=[1,0] -> [1,-2]; upper/diag ignored
+    l = _t(np.array([[7.0, 9.0], [2.0, -3.0]]), cuda)
+    x = _t(np.array([[1.0], [0.0]]), cuda)
+    _lib().check(_lib().load().pflu_trsm(l.data_ptr(), 2, 2, x.data_ptr(), 1, 1, _stream()), "trsm")
+    assert x.cpu().numpy().ravel().tolist() == [1.0, -2.0]
+
+
+def test_trsm_golden(cuda, golden_small):
+    l0, x0, want = golden_small["trsm__l"], golden_small["trsm__x"], golden_small["trsm__out"]
+    l, x = _t(l0, cuda), _t(x0, cuda)
+    nb, ncols = x0.shape
+    _lib().check(_lib().load().pflu_trsm(l.data_ptr(), nb, nb, x.data_ptr(), ncols, ncols, _stream()), "trsm")
+    assert bitwise_equal(x.cpu().numpy(), want)
+
+
+def test_laswp_golden(cuda, golden_small):
+    import torch
+
+    x0, piv1, want = golden_small["laswp__a"], golden_small["laswp__piv1"], golden_small["laswp__out"]
+    x = _t(x0, cuda)
+    piv = torch.from_numpy(piv1 - 1).to(cuda)
+    rc = _lib().load().pflu_laswp(x.data_ptr(), x0.shape[1], 0, x0.shape[1], piv.data_ptr(), 0, len(piv1), _stream())
+    _lib().check(rc, "laswp")
+    assert bitwise_equal(x.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("seed,m,ncols,k1,k2", [(0, 50, 9, 0, 1), (1, 300, 200, 10, 90), (2, 2000, 33, 0, 512),
+                                               (3, 5000, 700, 100, 356), (4, 1100, 64, 0, 1024)])
+def test_laswp_random(cuda, seed, m, ncols, k1, k2):
+    import torch
+
+    rng = np.random.default_rng(seed)
+    x0 = rng.standard_normal((m, ncols))
+    piv0 = np.array([rng.integers(k, m) if rng.random() < 0.8 else k for k in range(k2)], dtype=np.int64)
+    # repeated targets (collisions) on purpose
+    if k2 - k1 > 4:
+        piv0[k1 + 3] = piv0[k1 + 1] = max(piv0[k1 + 1], k1 + 3)
+    want = oracle.laswp(x0.copy(), piv0, k1, k2)
+    x = _t(x0, cuda)
+    piv = torch.from_numpy(piv0).to(cuda)
+    rc = _lib().load().pflu_laswp(x.data_ptr(), ncols, 0, ncols, piv.data_ptr(), k1, k2, _stream())
+    _lib().check(rc, "laswp")
+    assert bitwise_equal(x.cpu().numpy(), want)
+
+
+def test_laswp_roundtrip_and_identity(cuda):
+    # reference test_kernels.py:335-396: identity is a no-op; applying inverse swaps restores
+    import torch
+
+    rng = np.random.default_rng(9)
+    x0 = rng.standard_normal((40, 24))
+    x = _t(x0, cuda)
+    ident = torch.arange(10, dtype=torch.int64, device=cuda)
+    L = _lib().load()
+    _lib().check(L.pflu_laswp(x.data_ptr(), 24, 0, 24, ident.data_ptr(), 0, 10, _stream()), "laswp")
+    assert bitwise_equal(x.cpu().numpy(), x0)
+    piv = torch.tensor([5, 7, 2, 39, 4], dtype=torch.int64, device=cuda)
+    _lib().check(L.pflu_laswp(x.data_ptr(), 24, 0, 24, piv.data_ptr(), 0, 5, _stream()), "laswp")
+    inv = oracle.laswp(x0.copy(), piv.cpu().numpy(), 0, 5)
+    assert bitwise_equal(x.cpu().numpy(), inv)
+    # undo: swaps in descending order are the inverse; express as ascending swaps of the reversed list
+    y = x.cpu().numpy()
+    for k in range(4, -1, -1):
+        p = int(piv[k])
+        y[[k, p]] = y[[p, k]]
+    assert bitwise_equal(y, x0)
+
+
+@pytest.mark.parametrize("m,w,ctas,leaf", [(64, 8, 0, 0), (300, 16, 0, 0), (1000, 64, 0, 0), (2048, 128, 3, 0),
+                                          (5000, 256, 0, 0), (777, 100, 5, 8), (4096, 256, 16, 16),
+                                          (20000, 256, 0, 0), (512, 512, 0, 0), (40, 40, 0, 32)])
+def test_panel_bitwise(cuda, m, w, ctas, leaf):
+    """Recursive panel + cooperative leaf == lu_unb_run on the panel (exact op order)."""
+    import torch
+    from paper_1804_07017_b200 import _lib as lb
+
+    rng = np.random.default_rng(m + w)
+    p0 = rng.uniform(-1, 1, (m, w))
+    want, wpiv, winfo = oracle.lu_unb(p0.copy())
+    x = _t(p0, cuda)
+    piv = torch.zeros(w, dtype=torch.int64, device=cuda)
+    info = ctypes.c_int64(0)
+    opt = lb.options(exact=True, panel_ctas=ctas, leaf_width=leaf)
+    rc = lb.load().pflu_panel(x.data_ptr(), w, m, 0, 0, w, piv.data_ptr(), ctypes.byref(info), _stream(), ctypes.byref(opt))
+    lb.check(rc, "panel")
+    assert np.array_equal(piv.cpu().numpy()[: len(wpiv)], wpiv)
+    assert info.value == winfo
+    assert bitwise_equal(x.cpu().numpy(), want)
+
+
+def test_panel_zero_column_info(cuda):
+    import torch
+    from paper_1804_07017_b200 import _lib as lb
+
+    p0 = np.array([[1.0, 0.0, 2.0], [2.0, 0.0, 1.0], [4.0, 0.0, 3.0]])
+    want, wpiv, winfo = oracle.lu_unb(p0.copy())
+    x = _t(p0, cuda)
+    piv = torch.zeros(3, dtype=torch.int64, device=cuda)
+    info = ctypes.c_int64(0)
+    rc = lb.load().pflu_panel(x.data_ptr(), 3, 3, 0, 0, 3, piv.data_ptr(), ctypes.byref(info), _stream(), None)
+    lb.check(rc, "panel")
+    assert info.value == 2 == winfo
+    assert bitwise_equal(x.cpu().numpy(), want)
+    assert np.all(x.cpu().numpy()[2:, 1] == 0.0)
