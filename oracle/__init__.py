@@ -162,7 +162,7 @@ def lu_residual(a0, lu, piv0, block: int = 2048) -> float:
     err2 = 0.0
     for r0 in range(0, m, block):
         r1 = min(m, r0 + block)
-        lower = np.tril(lu[r0:r1, :kk], -1 - r0)
+        lower = np.tril(lu[r0:r1, :kk], r0 - 1)   # global (i, j) kept iff j < i
         for i in range(r0, min(r1, kk)):
             lower[i - r0, i] = 1.0
         d = a0[perm[r0:r1]] - lower @ upper

@@ -100,19 +100,27 @@ static int ctx_get(DevCtx** out) {
     CK(cudaMalloc(&c.plan[1], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
     CK(cudaMalloc(&c.info, 64));
     for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&c.tev[i]));
-    // kernel attributes (dynamic shared memory beyond 48 KB)
-    const int big = (int)c.smem_optin;
-    CK(cudaFuncSetAttribute(leaf_getf2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(leaf_getf2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(leaf_getf2_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(swap_trsm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(swap_trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(trsm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(trsm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-    CK(cudaFuncSetAttribute(gemm_dmma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM_SMEM));
-    CK(cudaFuncSetAttribute(gemm_dmma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM_SMEM));
-    CK(cudaFuncSetAttribute(gemm_exact_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM_SMEM));
-    CK(cudaFuncSetAttribute(gemm_exact_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GM_SMEM));
+    // kernel attributes (dynamic shared memory beyond 48 KB; the limit excludes static smem)
+    auto allow = [&](const void* fn) -> cudaError_t {
+      cudaFuncAttributes fa;
+      cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+      if (e != cudaSuccess) return e;
+      return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(c.smem_optin - fa.sharedSizeBytes));
+    };
+    CK(allow((const void*)leaf_getf2_kernel<8>));
+    CK(allow((const void*)leaf_getf2_kernel<16>));
+    CK(allow((const void*)leaf_getf2_kernel<32>));
+    CK(allow((const void*)swap_trsm_kernel<8>));
+    CK(allow((const void*)swap_trsm_kernel<16>));
+    CK(allow((const void*)swap_trsm_kernel<32>));
+    CK(allow((const void*)trsm_kernel<8>));
+    CK(allow((const void*)trsm_kernel<16>));
+    CK(allow((const void*)trsm_kernel<32>));
+    CK(allow((const void*)gemm_dmma_kernel<1>));
+    CK(allow((const void*)gemm_dmma_kernel<2>));
+    CK(allow((const void*)gemm_exact_kernel<1>));
+    CK(allow((const void*)gemm_exact_kernel<2>));
     c.ready = true;
   }
   *out = &c;
@@ -165,9 +173,12 @@ static int launch_trsm(const double* L, int64_t ldl, int np, double* X, int64_t 
   if (np <= 256) {
     size_t smem = (size_t)(np * 32 + 1024) * 8;
     trsm_kernel<32><<<(unsigned)((ncols + 31) / 32), 256, smem, st>>>(L, ldl, X, ldx, np, ncols);
-  } else {
+  } else if (np <= 512) {
     size_t smem = (size_t)(np * 16 + 1024) * 8;
     trsm_kernel<16><<<(unsigned)((ncols + 15) / 16), 256, smem, st>>>(L, ldl, X, ldx, np, ncols);
+  } else {
+    size_t smem = (size_t)(np * 8 + 1024) * 8;
+    trsm_kernel<8><<<(unsigned)((ncols + 7) / 8), 256, smem, st>>>(L, ldl, X, ldx, np, ncols);
   }
   CK(cudaGetLastError());
   return PFLU_OK;
@@ -184,14 +195,16 @@ static int launch_plan(const int64_t* piv, int64_t d, int np, int64_t* plan, cud
 static int launch_swap(double* a, int64_t lda, int64_t d, int np, const int64_t* plan, int64_t c0, int64_t c1,
                        const double* L, int64_t ldl, bool do_trsm, cudaStream_t st) {
   if (c1 <= c0 || np <= 0) return PFLU_OK;
+  const int t = do_trsm ? 1 : 0;
   if (np <= 256) {
     size_t smem = (size_t)(np * 32 + std::max(np * 32, 1024)) * 8;
-    swap_trsm_kernel<32><<<(unsigned)((c1 - c0 + 31) / 32), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl,
-                                                                              do_trsm ? 1 : 0);
-  } else {
+    swap_trsm_kernel<32><<<(unsigned)((c1 - c0 + 31) / 32), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl, t);
+  } else if (np <= 512) {
     size_t smem = (size_t)(np * 16 + std::max(np * 16, 1024)) * 8;
-    swap_trsm_kernel<16><<<(unsigned)((c1 - c0 + 15) / 16), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl,
-                                                                              do_trsm ? 1 : 0);
+    swap_trsm_kernel<16><<<(unsigned)((c1 - c0 + 15) / 16), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl, t);
+  } else {
+    size_t smem = (size_t)(np * 8 + std::max(np * 8, 1024)) * 8;
+    swap_trsm_kernel<8><<<(unsigned)((c1 - c0 + 7) / 8), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl, t);
   }
   CK(cudaGetLastError());
   return PFLU_OK;

@@ -54,7 +54,7 @@ def gpu_residual(a0, lu, piv, block=4096):
     for r0 in range(0, a0.shape[0], block):
         r1 = min(a0.shape[0], r0 + block)
         Lb = torch.from_numpy(np.ascontiguousarray(lu[r0:r1, :n])).to(dev)
-        Lb = torch.tril(Lb, diagonal=-1 - r0)
+        Lb = torch.tril(Lb, diagonal=r0 - 1)   # global (i, j) kept iff j < i
         idx = torch.arange(r0, min(r1, n), device=dev)
         Lb[idx - r0, idx] = 1.0
         d = torch.from_numpy(np.ascontiguousarray(a0[perm[r0:r1]])).to(dev) - Lb @ U_
