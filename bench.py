@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark: LU with partial pivoting (BASELINE.json metric: FP64 GFLOP/s = (2/3 n^3)/t).
+
+Workload (BASELINE.json configs[3], "C4"): n = 32768 float64, entries U[-1,1) from
+numpy default_rng(3), b = 256, look-ahead depth 1.  One "step" = one full factorization of that
+matrix on the GPU, inputs already resident in HBM (the pristine matrix is restored with a
+device-to-device copy at the start of every step -- inside the timed region; 8.6 GB > L2, so
+no L2 flush is needed).  Timed with CUDA events on the launching stream.
+
+--gpus N > 1 (under torchrun, one rank per GPU): 1-D block-cyclic column distribution with an
+NCCL panel + pivot broadcast (paper_1804_07017_b200.dist); value = whole-job GFLOP/s.
+
+--impl reference: the reference algorithm's CPU implementation -- the oracle port
+(oracle/pflu_oracle.c, bit-for-bit the reference's arithmetic) with every host thread -- timed
+on a bounded sample of the same workload: the first blocked step of C4 (panel + laswp + trsm +
+trailing GEMM of the n=32768 matrix).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LU-pp FP64 GFLOP/s (2/3*n^3/t)"
+UNIT = "GFLOP/s"
+
+
+def lu_flops(n: int) -> float:
+    return 2.0 * n ** 3 / 3.0
+
+
+def fp64_peak() -> tuple[float, str]:
+    """FP64 roofline denominator: the measured DMMA peak (profiles/r01_fp64_peak.jsonl, measured
+    on this pool's B200 with tools/fp64_peak.cu; MEASURED_PEAKS.json carries no FP64 figure)."""
+    path = os.path.join(ROOT, "profiles", "r01_fp64_peak.jsonl")
+    best = 0.0
+    try:
+        for line in open(path):
+            d = json.loads(line)
+            if d.get("kind") in ("dmma", "dmma_sustained"):
+                best = max(best, float(d["tflops"]))
+    except OSError:
+        pass
+    if best > 0:
+        return best, "measured DMMA (profiles/r01_fp64_peak.jsonl)"
+    return 148 * 1.965e9 * 128 / 1e12, "nominal 148 SMs x 128 flop/clk x 1.965 GHz"
+
+
+def c4_matrix(n: int, seed: int = 3) -> np.ndarray:
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n, n))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+def load_traffic() -> tuple[float | None, str | None]:
+    """DRAM bytes per launch of the trailing-update GEMM from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    try:
+        d = json.load(open(path))
+        return float(d["dram_bytes_per_launch"]), d.get("source")
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
+def cpu_sample(n: int, b: int, threads: int | None = None) -> dict:
+    """The oracle port (bitwise the reference's arithmetic, all host threads) on the first blocked
+    step of the same matrix; GFLOP/s = that step's flops / wall time."""
+    import oracle
+
+    cores = threads or os.cpu_count() or 1
+    oracle.set_threads(cores)
+    a = c4_matrix(n)
+    piv = np.zeros(n, dtype=np.int64)
+    t0 = time.perf_counter()
+    oracle.getrf_steps_inplace(a, b, 1, piv)
+    dt = time.perf_counter() - t0
+    fl = oracle.step_flops(n, n, b, 0)
+    return {"value": fl / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"first blocked step (panel {n}x{b} + laswp + trsm + {n - b}^2x{b} gemm) of the n={n} "
+                      f"C4 matrix, {fl / 1e9:.1f} GFLOP in {dt:.2f} s, oracle/pflu_oracle.c -O3 OpenMP"}
+
+
+def run_reference(args) -> None:
+    """--impl reference: the reference algorithm's CPU implementation (oracle port) timed on the
+    host cores, on bounded samples of the same workload (the first blocked step of C4)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    n, b = args.n, args.b
+    cores = os.cpu_count() or 1
+    oracle.set_threads(cores)
+    pristine = c4_matrix(n)
+    work = np.empty_like(pristine)
+    piv = np.zeros(n, dtype=np.int64)
+    fl = oracle.step_flops(n, n, b, 0)
+    times = []
+    for it in range(args.warmup + args.steps):
+        np.copyto(work, pristine)
+        t0 = time.perf_counter()
+        oracle.getrf_steps_inplace(work, b, 1, piv)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = fl * len(times) / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C4: LUpp n={n} U[-1,1) seed 3, b={b}, look-ahead 1",
+                   "sample": "first blocked step of C4 per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"first blocked step of the n={n} C4 matrix ({fl / 1e9:.1f} GFLOP) per step; "
+                                   "oracle/pflu_oracle.c is op-for-op the reference (pinned bitwise, tests/test_oracle.py)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_single(args) -> None:
+    import torch
+
+    from paper_1804_07017_b200 import _lib, getrf_device, lu_factor
+
+    L = _lib.load()
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    n, b, la = args.n, args.b, args.lookahead
+    a_host = c4_matrix(n)
+    d_a0 = torch.from_numpy(a_host).to(dev)
+    d_a = torch.empty_like(d_a0)
+    piv = torch.empty(n, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(trace=None):
+        d_a.copy_(d_a0)
+        _, info = getrf_device(d_a, b, la, piv=piv, trace=trace)
+        return info
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = L.pflu_launch_count()
+    traces = []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        tr = []
+        step(trace=tr)
+        traces.append(tr)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = L.pflu_launch_count() - launches0
+    clk = clocks.stop()
+    total_ms = e0.elapsed_time(e1)
+    ms_step = total_ms / args.steps
+    value = lu_flops(n) / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel: the trailing-update DMMA GEMM, from the live trace
+    g_flops, g_ms, g_cnt = 0.0, 0.0, 0
+    for tr in traces:
+        for ev in tr:
+            if ev.label == "GEMM":
+                k = ev.k
+                mrows = n - (k + 1) * b
+                ncols = n - (k + 2) * b if la == 1 else n - (k + 1) * b
+                if mrows > 0 and ncols > 0:
+                    g_flops += 2.0 * mrows * ncols * b
+                    g_ms += (ev.end - ev.start) * 1e3
+                    g_cnt += 1
+    peak, peak_src = fp64_peak()
+    achieved = g_flops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else None
+    traffic, traffic_src = load_traffic()
+    pf_ms = sum((ev.end - ev.start) * 1e3 for ev in traces[-1] if ev.label == "PF")
+    gemm_share = (g_ms / args.steps) / ms_step if ms_step else None
+
+    # end to end through the public API with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        host = pinned.numpy()
+        ts = []
+        for it in range(args.e2e_steps + 1):
+            np.copyto(host, a_host)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            lu, pv = lu_factor(host, b=b, lookahead=la)
+            ts.append(time.perf_counter() - t0)
+        ts = ts[1:]
+        e2e = {"value": lu_flops(n) / statistics.mean(ts) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": n * n * 8 + n * 8,
+               "api": "paper_1804_07017_b200.lu_factor(numpy pinned host array) -> pflu_getrf",
+               "ms_per_step": 1e3 * statistics.mean(ts)}
+        del pinned, host
+
+    cpu = None if args.no_cpu else cpu_sample(n, b)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"C4: LUpp n={n} U[-1,1) numpy seed 3, b={b}, look-ahead {la}",
+                   "n": n, "b": b, "lookahead": la, "parallelism": "single GPU",
+                   "l2": "inputs (8.6 GB) larger than L2; pristine matrix restored by a D2D copy inside each step",
+                   "fp64_peak_frac": value / 1e3 / peak},
+        "roofline": {"bound": "tensor", "kernel": "gemm_dmma_kernel (trailing update A22 -= L21*U12)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "peak_source": peak_src, "traffic_source": traffic_src,
+                     "launches_timed": g_cnt, "gemm_share_of_step": gemm_share,
+                     "algorithmic": "2*(n-(k+1)b)*(n-(k+2)b)*b flop per TU_R launch of step k"},
+        "panel_ms_per_step": pf_ms,
+        "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--b", type=int, default=256)
+    ap.add_argument("--lookahead", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_1804_07017_b200.dist import bench_dist
+
+        bench_dist(args, lu_flops, METRIC, UNIT, ClockSampler, fp64_peak)
+        return
+    run_single(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -53,6 +53,7 @@ typedef struct pflu_options {
 #define PFLU_TRACE_TU 1   /* full trailing update (lookahead 0)          */
 #define PFLU_TRACE_TU_L 2 /* update of panel k+1's columns (lookahead 1) */
 #define PFLU_TRACE_TU_R 3 /* remaining trailing update (lookahead 1)     */
+#define PFLU_TRACE_GEMM 4 /* the DMMA GEMM inside TU / TU_R (roofline)   */
 typedef struct pflu_trace_event {
   int32_t label;
   int32_t k;
@@ -61,6 +62,8 @@ typedef struct pflu_trace_event {
 } pflu_trace_event;
 
 int pflu_version(void);
+/* Cumulative number of kernels this library has launched in the process (bench evidence). */
+long long pflu_launch_count(void);
 const char* pflu_last_error(void);
 void pflu_default_options(pflu_options* opt);
 int pflu_device_count(void);

@@ -54,6 +54,8 @@ def lib():
         L.orc_gemm_sub.argtypes = [_d, _I64, _d, _I64, _d, _I64, _I64, _I64, _I64]
         L.orc_getrf.restype = _I64
         L.orc_getrf.argtypes = [_d, _I64, _I64, _I64, _I64, _i]
+        L.orc_getrf_steps.restype = _I64
+        L.orc_getrf_steps.argtypes = [_d, _I64, _I64, _I64, _I64, _i, _I64]
         L.orc_set_threads.restype = None
         L.orc_set_threads.argtypes = [ctypes.c_int]
         _LIB = L
@@ -100,6 +102,29 @@ def getrf(a, b: int):
     piv = np.zeros(n, dtype=np.int64)
     info = lib().orc_getrf(_dp(a), m, n, n, int(b), _ip(piv))
     return a, piv, int(info)
+
+
+def getrf_steps_inplace(a: np.ndarray, b: int, nsteps: int, piv: np.ndarray | None = None) -> int:
+    """First `nsteps` blocked steps of the reference algorithm, in place on a row-major array
+    (the bounded CPU-baseline sample used by bench.py)."""
+    m, n = a.shape
+    if piv is None:
+        piv = np.zeros(n, dtype=np.int64)
+    return int(lib().orc_getrf_steps(_dp(a), m, n, a.strides[0] // 8, int(b), _ip(piv), int(nsteps)))
+
+
+def step_flops(m: int, n: int, b: int, k: int = 0) -> int:
+    """Flops of blocked step k (panel getf2 + trsm + gemm) as the reference executes them."""
+    col0 = k * b
+    bw = min(b, n - col0)
+    mp = m - col0
+    f = 0
+    for j in range(min(mp, bw)):
+        f += (mp - j - 1) + 2 * (mp - j - 1) * (bw - j - 1)
+    right = n - col0 - bw
+    f += bw * (bw - 1) * right                  # trsm: 2 flops x b(b-1)/2 x cols
+    f += 2 * (mp - bw) * right * bw             # gemm
+    return f
 
 
 def lu_prefix(a, steps: int):

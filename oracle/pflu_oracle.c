@@ -149,9 +149,10 @@ void orc_gemm_sub(double *c, int64_t ldc, const double *a, int64_t lda, const do
 /* Blocked right-looking LUpp (dmf_mtb order, factor.py:382-412): for each panel k: panel
  * factorization (lu_unb on rows col0.., panel width), left swaps on [0, col0), right swaps +
  * trsm + gemm on [col0+bw, n).  m >= n >= 1 (caller validates).  piv: 0-based global rows. */
-int64_t orc_getrf(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, int64_t *piv) {
+int64_t orc_getrf_steps(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, int64_t *piv, int64_t nsteps) {
   int64_t info = 0;
-  for (int64_t col0 = 0; col0 < n; col0 += b) {
+  int64_t step = 0;
+  for (int64_t col0 = 0; col0 < n && (nsteps < 0 || step < nsteps); col0 += b, ++step) {
     int64_t bw = n - col0 < b ? n - col0 : b;
     double *panel = a + IDX(col0, col0, lda);
     int64_t pinfo = orc_lu_unb(panel, m - col0, bw, lda, piv + col0, -1);
@@ -169,6 +170,10 @@ int64_t orc_getrf(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, int64
     }
   }
   return info;
+}
+
+int64_t orc_getrf(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, int64_t *piv) {
+  return orc_getrf_steps(a, m, n, lda, b, piv, -1);
 }
 
 /* First `steps` elimination steps of the unblocked algorithm on the full m x n matrix

@@ -17,9 +17,11 @@ PFLU_ERR_CUDA = 1
 PFLU_ERR_NOMEM = 2
 PFLU_ERR_UNSUPPORTED = 3
 
+TRACE_LABELS = {0: "PF", 1: "TU", 2: "TU_L", 3: "TU_R", 4: "GEMM"}
+
 #: every symbol include/pflu.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
-    "pflu_version", "pflu_last_error", "pflu_default_options", "pflu_device_count",
+    "pflu_version", "pflu_launch_count", "pflu_last_error", "pflu_default_options", "pflu_device_count",
     "pflu_getrf", "pflu_getrf_device", "pflu_panel", "pflu_laswp", "pflu_swap_trsm",
     "pflu_trsm", "pflu_gemm_update",
 )
@@ -56,6 +58,8 @@ def load():
         L = ctypes.CDLL(LIB_PATH)
         L.pflu_version.restype = ctypes.c_int
         L.pflu_version.argtypes = []
+        L.pflu_launch_count.restype = ctypes.c_longlong
+        L.pflu_launch_count.argtypes = []
         L.pflu_last_error.restype = ctypes.c_char_p
         L.pflu_last_error.argtypes = []
         L.pflu_default_options.restype = None

@@ -153,9 +153,11 @@ def getrf_host(a: np.ndarray, b: int, lookahead: int, exact: bool = False, panel
     return piv, int(info.value)
 
 
-def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int = 0, piv=None):
+def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int = 0, piv=None, trace=None):
     """Factor a row-major CUDA float64 torch tensor in place through pflu_getrf_device on the
-    current torch stream.  Returns (piv0 int64 CUDA tensor, info)."""
+    current torch stream.  Returns (piv0 int64 CUDA tensor, info).  If ``trace`` is a list, it
+    receives :class:`TraceEvent` records (labels PF / TU / TU_L / TU_R / GEMM, seconds from the
+    start, CUDA-event timed) -- the reference's trace hook (factor.py:104-122)."""
     import torch
 
     L = _lib.load()
@@ -165,10 +167,21 @@ def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int
     info = ctypes.c_int64(0)
     opt = _lib.options(exact=exact, panel_ctas=panel_ctas)
     stream = torch.cuda.current_stream(a.device).cuda_stream
+    tbuf, tcap, tlen = None, 0, ctypes.c_int(0)
+    if trace is not None:
+        steps = -(-n // max(1, min(b, n)))
+        tcap = 6 * steps + 16
+        tbuf = (_lib.TraceEvent * tcap)()
     with torch.cuda.device(a.device):
         rc = L.pflu_getrf_device(a.data_ptr(), m, n, a.stride(0), int(b), int(lookahead), piv.data_ptr(),
-                                 ctypes.byref(info), stream, ctypes.byref(opt), None, 0, None)
+                                 ctypes.byref(info), stream, ctypes.byref(opt), tbuf, tcap, ctypes.byref(tlen))
     _lib.check(rc, "pflu_getrf_device")
+    if trace is not None:
+        for i in range(tlen.value):
+            e = tbuf[i]
+            lab = _lib.TRACE_LABELS.get(e.label, str(e.label))
+            j = e.k + 1 if lab == "TU_L" else None
+            trace.append(TraceEvent(lab, int(e.k), j, e.start_ms * 1e-3, e.end_ms * 1e-3, None))
     return piv, int(info.value)
 
 

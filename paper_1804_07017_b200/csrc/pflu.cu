@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdarg>
 #include <cstdio>
@@ -65,8 +66,66 @@ struct DevCtx {
   int64_t* plan[2] = {nullptr, nullptr};
   unsigned long long* info = nullptr;
   int leaf_occ[3] = {0, 0, 0};  // max active CTAs/SM for W = 8, 16, 32 at max smem (set lazily)
-  std::vector<cudaEvent_t> ev;  // event pool
-  cudaEvent_t tev[4] = {};      // timing events scratch
+  std::vector<cudaEvent_t> ev;  // event pool (ordering only)
+  std::vector<cudaEvent_t> tev; // timing event pool (tracing)
+};
+
+static std::atomic<long long> g_launches{0};
+
+// Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.
+struct Tracer {
+  DevCtx* c = nullptr;
+  bool on = false;
+  size_t used = 0;
+  cudaEvent_t t0 = nullptr;
+  struct Rec { int label, k; cudaEvent_t e0, e1; };
+  std::vector<Rec> recs;
+  int ev(cudaEvent_t* out) {
+    if (used == c->tev.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->tev.push_back(e);
+    }
+    *out = c->tev[used++];
+    return PFLU_OK;
+  }
+  int start(cudaStream_t st) {
+    if (!on) return PFLU_OK;
+    CKR(ev(&t0));
+    CK(cudaEventRecord(t0, st));
+    return PFLU_OK;
+  }
+  int begin(int label, int k, cudaStream_t st, int* idx) {
+    *idx = -1;
+    if (!on) return PFLU_OK;
+    Rec r{label, k, nullptr, nullptr};
+    CKR(ev(&r.e0));
+    CKR(ev(&r.e1));
+    CK(cudaEventRecord(r.e0, st));
+    recs.push_back(r);
+    *idx = (int)recs.size() - 1;
+    return PFLU_OK;
+  }
+  int end(int idx, cudaStream_t st) {
+    if (!on || idx < 0) return PFLU_OK;
+    CK(cudaEventRecord(recs[idx].e1, st));
+    return PFLU_OK;
+  }
+  int collect(pflu_trace_event* out, int cap, int* len) {
+    int n = 0;
+    if (on && out) {
+      for (const Rec& r : recs) {
+        if (n >= cap) break;
+        float a = 0.f, b = 0.f;
+        CK(cudaEventElapsedTime(&a, t0, r.e0));
+        CK(cudaEventElapsedTime(&b, t0, r.e1));
+        out[n].label = r.label; out[n].k = r.k; out[n].start_ms = a; out[n].end_ms = b;
+        ++n;
+      }
+    }
+    if (len) *len = n;
+    return PFLU_OK;
+  }
 };
 
 static std::mutex g_mu;
@@ -99,7 +158,6 @@ static int ctx_get(DevCtx** out) {
     CK(cudaMalloc(&c.plan[0], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
     CK(cudaMalloc(&c.plan[1], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
     CK(cudaMalloc(&c.info, 64));
-    for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&c.tev[i]));
     // kernel attributes (dynamic shared memory beyond 48 KB; the limit excludes static smem)
     auto allow = [&](const void* fn) -> cudaError_t {
       cudaFuncAttributes fa;
@@ -163,6 +221,7 @@ static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, con
     else gemm_dmma_kernel<1><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
   }
   CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return PFLU_OK;
 }
 
@@ -181,6 +240,7 @@ static int launch_trsm(const double* L, int64_t ldl, int np, double* X, int64_t 
     trsm_kernel<8><<<(unsigned)((ncols + 7) / 8), 256, smem, st>>>(L, ldl, X, ldx, np, ncols);
   }
   CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return PFLU_OK;
 }
 
@@ -188,6 +248,7 @@ static int launch_plan(const int64_t* piv, int64_t d, int np, int64_t* plan, cud
   if (np > PLAN_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "pivot block %d > %d", np, PLAN_MAX);
   pivot_plan_kernel<<<1, 256, 0, st>>>(piv, d, np, plan);
   CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return PFLU_OK;
 }
 
@@ -207,6 +268,7 @@ static int launch_swap(double* a, int64_t lda, int64_t d, int np, const int64_t*
     swap_trsm_kernel<8><<<(unsigned)((c1 - c0 + 7) / 8), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl, t);
   }
   CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return PFLU_OK;
 }
 
@@ -273,6 +335,7 @@ static int launch_leaf(DevCtx& c, const LeafCfg& cfg, double* a, int64_t lda, in
                                : (const void*)leaf_getf2_kernel<32>;
   size_t smem = (size_t)(R * (cfg.W + 1) + 2 * cfg.W) * 8;
   CK(cudaLaunchCooperativeKernel(fn, dim3(S), dim3(LEAF_THREADS), args, smem, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return PFLU_OK;
 }
 
@@ -312,23 +375,29 @@ struct Step {
 
 static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
                        int64_t* piv, unsigned long long* info, cudaStream_t user, const pflu_options& opt,
-                       std::vector<std::pair<int, int>>* marks) {
+                       Tracer& tr) {
   std::vector<Step> grid;
   for (int64_t col0 = 0; col0 < n; col0 += b) grid.push_back({col0, std::min(b, n - col0)});
   const int count = (int)grid.size();
   const bool exact = opt.exact != 0;
   CK(cudaMemsetAsync(info, 0xff, sizeof(unsigned long long), user));
-  auto update_cols = [&](int k, int64_t lo, int64_t hi, cudaStream_t st) -> int {
+  CKR(tr.start(user));
+  auto update_cols = [&](int k, int64_t lo, int64_t hi, cudaStream_t st, int label) -> int {
     // TU of step k on storage columns [lo, hi): laswp + trsm (fused), then the DMMA update
     if (hi <= lo) return PFLU_OK;
     const Step s = grid[k];
     const int np = (int)std::min(s.bw, m - s.col0);
+    int t_tu = -1, t_g = -1;
+    CKR(tr.begin(label, k, st, &t_tu));
     CKR(launch_swap(a, lda, s.col0, np, c.plan[k & 1], lo, hi, a + s.col0 * lda + s.col0, lda, true, st));
     const int64_t below = s.col0 + s.bw;
-    if (below < m)
+    if (below < m) {
+      if (label != PFLU_TRACE_TU_L) CKR(tr.begin(PFLU_TRACE_GEMM, k, st, &t_g));
       CKR(launch_gemm(a + below * lda + lo, lda, a + below * lda + s.col0, lda, a + s.col0 * lda + lo, lda,
                       m - below, hi - lo, s.bw, exact, st));
-    return PFLU_OK;
+      CKR(tr.end(t_g, st));
+    }
+    return tr.end(t_tu, st);
   };
   auto left_swaps = [&](int k, cudaStream_t st) -> int {
     const Step s = grid[k];
@@ -338,9 +407,12 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   };
   auto pf = [&](int k, cudaStream_t st) -> int {
     const Step s = grid[k];
+    int t_pf = -1;
+    CKR(tr.begin(PFLU_TRACE_PF, k, st, &t_pf));
     CKR(panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, opt, st));
     const int np = (int)std::min(s.bw, m - s.col0);
-    return launch_plan(piv, s.col0, np, c.plan[k & 1], st);
+    CKR(launch_plan(piv, s.col0, np, c.plan[k & 1], st));
+    return tr.end(t_pf, st);
   };
 
   if (lookahead == 0) {
@@ -348,7 +420,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     for (int k = 0; k < count; ++k) {
       CKR(pf(k, user));
       CKR(left_swaps(k, user));
-      CKR(update_cols(k, grid[k].col0 + grid[k].bw, n, user));
+      CKR(update_cols(k, grid[k].col0 + grid[k].bw, n, user, PFLU_TRACE_TU));
     }
     return PFLU_OK;
   }
@@ -366,13 +438,13 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     // branch_b: TU_R(k) on columns beyond panel k+1, then the deferred left swaps of step k
     CK(cudaStreamWaitEvent(c.sU, ev_pf(k), 0));
     const int64_t lo_r = (k + 1 < count) ? grid[k + 1].col0 + grid[k + 1].bw : n;
-    CKR(update_cols(k, lo_r, n, c.sU));
+    CKR(update_cols(k, lo_r, n, c.sU, PFLU_TRACE_TU_R));
     CKR(left_swaps(k, c.sU));
     CK(cudaEventRecord(ev_tu(k), c.sU));
     // branch_a: TU_L(k) on panel k+1's columns, then PF(k+1)
     if (k + 1 < count) {
       if (k > 0) CK(cudaStreamWaitEvent(c.sP, ev_tu(k - 1), 0));
-      CKR(update_cols(k, grid[k + 1].col0, grid[k + 1].col0 + grid[k + 1].bw, c.sP));
+      CKR(update_cols(k, grid[k + 1].col0, grid[k + 1].col0 + grid[k + 1].bw, c.sP, PFLU_TRACE_TU_L));
       CKR(pf(k + 1, c.sP));
       CK(cudaEventRecord(ev_pf(k + 1), c.sP));
     }
@@ -381,7 +453,6 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   CK(cudaStreamWaitEvent(user, c.ev[1], 0));
   CK(cudaEventRecord(ev_tu(count - 1), c.sU));
   CK(cudaStreamWaitEvent(user, ev_tu(count - 1), 0));
-  (void)marks;
   return PFLU_OK;
 }
 
@@ -414,6 +485,8 @@ extern "C" {
 
 int pflu_version(void) { return 1; }
 
+long long pflu_launch_count(void) { return g_launches.load(); }
+
 const char* pflu_last_error(void) { return g_err.c_str(); }
 
 void pflu_default_options(pflu_options* opt) {
@@ -443,10 +516,12 @@ int pflu_getrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b,
   DevCtx* c = nullptr;
   CKR(ctx_get(&c));
   cudaStream_t st = (cudaStream_t)stream;
-  CKR(getrf_async(*c, d_a, m, n, lda, std::min(b, n), lookahead, d_ipiv, c->info, st, opt, nullptr));
-  if (trace_len) *trace_len = 0;
-  (void)trace; (void)trace_cap;
-  return finish_info(*c, st, info);
+  Tracer tr;
+  tr.c = c;
+  tr.on = trace != nullptr && trace_cap > 0;
+  CKR(getrf_async(*c, d_a, m, n, lda, std::min(b, n), lookahead, d_ipiv, c->info, st, opt, tr));
+  CKR(finish_info(*c, st, info));
+  return tr.collect(trace, trace_cap, trace_len);
 }
 
 int pflu_getrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, int64_t* ipiv, int64_t* info,
