@@ -16,6 +16,7 @@
 #include <climits>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -23,6 +24,7 @@
 
 #include "../../include/pflu.h"
 #include "pflu_kernels.cuh"
+#include "pflu_panel.cuh"
 
 namespace pflu {
 
@@ -65,12 +67,17 @@ struct DevCtx {
   unsigned* bar = nullptr;
   int64_t* plan[2] = {nullptr, nullptr};
   unsigned long long* info = nullptr;
+  unsigned long long* ll = nullptr;  // LL exchange words of the panel kernel
+  unsigned* epoch = nullptr;
   int leaf_occ[3] = {0, 0, 0};  // max active CTAs/SM for W = 8, 16, 32 at max smem (set lazily)
   std::vector<cudaEvent_t> ev;  // event pool (ordering only)
   std::vector<cudaEvent_t> tev; // timing event pool (tracing)
 };
 
 static std::atomic<long long> g_launches{0};
+static unsigned long long* g_prof = nullptr;
+static int g_pf_cap = []() { const char* e = getenv("PFLU_PANEL_CAP"); return e ? atoi(e) : 32; }();
+static int g_variant = []() { const char* e = getenv("PFLU_PANEL_VARIANT"); return e ? atoi(e) : 0; }();  // device buffer for panel-kernel phase clocks (tools only)
 
 // Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.
 struct Tracer {
@@ -133,6 +140,8 @@ static DevCtx g_ctx[64];
 
 static constexpr int SLOT_MAX_CTAS = 1024;
 static constexpr int SLOT_MAX_W = 32;
+static constexpr int PF_MAX_CTAS = PF_THREADS;
+static constexpr size_t LL_WORDS = PF_LL_WORDS;
 
 static int ctx_get(DevCtx** out) {
   int dev = 0;
@@ -158,6 +167,13 @@ static int ctx_get(DevCtx** out) {
     CK(cudaMalloc(&c.plan[0], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
     CK(cudaMalloc(&c.plan[1], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
     CK(cudaMalloc(&c.info, 64));
+    CK(cudaMalloc(&c.ll, sizeof(unsigned long long) * LL_WORDS));
+    CK(cudaMemset(c.ll, 0, sizeof(unsigned long long) * LL_WORDS));
+    CK(cudaMalloc(&c.epoch, 64));
+    {
+      unsigned one = 1;
+      CK(cudaMemcpy(c.epoch, &one, sizeof(one), cudaMemcpyHostToDevice));
+    }
     // kernel attributes (dynamic shared memory beyond 48 KB; the limit excludes static smem)
     auto allow = [&](const void* fn) -> cudaError_t {
       cudaFuncAttributes fa;
@@ -166,6 +182,9 @@ static int ctx_get(DevCtx** out) {
       return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(c.smem_optin - fa.sharedSizeBytes));
     };
+    CK(allow((const void*)panel_kernel<8>));
+    CK(allow((const void*)panel_kernel<16>));
+    CK(allow((const void*)panel_kernel<32>));
     CK(allow((const void*)leaf_getf2_kernel<8>));
     CK(allow((const void*)leaf_getf2_kernel<16>));
     CK(allow((const void*)leaf_getf2_kernel<32>));
@@ -230,13 +249,13 @@ static int launch_trsm(const double* L, int64_t ldl, int np, double* X, int64_t 
   if (np <= 1 || ncols <= 0) return PFLU_OK;
   if (np > PLAN_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "trsm block %d > %d", np, PLAN_MAX);
   if (np <= 256) {
-    size_t smem = (size_t)(np * 32 + 1024) * 8;
+    size_t smem = (size_t)(np * 32 + std::max(np, 32) * 32) * 8;
     trsm_kernel<32><<<(unsigned)((ncols + 31) / 32), 256, smem, st>>>(L, ldl, X, ldx, np, ncols);
   } else if (np <= 512) {
-    size_t smem = (size_t)(np * 16 + 1024) * 8;
+    size_t smem = (size_t)(np * 16 + std::max(np, 16) * 16) * 8;
     trsm_kernel<16><<<(unsigned)((ncols + 15) / 16), 256, smem, st>>>(L, ldl, X, ldx, np, ncols);
   } else {
-    size_t smem = (size_t)(np * 8 + 1024) * 8;
+    size_t smem = (size_t)(np * 8 + std::max(np, 8) * 8) * 8;
     trsm_kernel<8><<<(unsigned)((ncols + 7) / 8), 256, smem, st>>>(L, ldl, X, ldx, np, ncols);
   }
   CK(cudaGetLastError());
@@ -359,11 +378,55 @@ static int panel_rec(DevCtx& c, const LeafCfg& cfg, double* a, int64_t lda, int6
   return panel_rec(c, cfg, a, lda, m, r0 + w1, c0 + w1, w - w1, pc0, pc1, piv, info, exact, st);
 }
 
+static int pf_occupancy(int W, size_t smem, int* occ) {
+  if (W == 8) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, panel_kernel<8>, PF_THREADS, smem));
+  else if (W == 16) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, panel_kernel<16>, PF_THREADS, smem));
+  else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, panel_kernel<32>, PF_THREADS, smem));
+  return PFLU_OK;
+}
+
+static size_t pf_smem_bytes(int W, int64_t R, int w) {
+  if (W == 8) return PanelSmem<8>::bytes(R, w);
+  if (W == 16) return PanelSmem<16>::bytes(R, w);
+  return PanelSmem<32>::bytes(R, w);
+}
+
+// Persistent panel factorization: rows [r0, m) of storage columns [c0, c0 + w).
 static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, int64_t c0, int64_t w,
                         int64_t* piv, unsigned long long* info, const pflu_options& opt, cudaStream_t st) {
-  LeafCfg cfg;
-  CKR(choose_leaf(c, m - r0, opt, &cfg));
-  return panel_rec(c, cfg, a, lda, m, r0, c0, w, c0, c0 + w, piv, info, opt.exact != 0, st);
+  const int64_t rows = m - r0;
+  if (rows <= 0 || w <= 0) return PFLU_OK;
+  const size_t smax = c.smem_optin - 2048;
+  int Wpref = opt.leaf_width > 0 ? opt.leaf_width : (w > 16 ? 32 : (w > 8 ? 16 : 8));
+  const int Ws[3] = {32, 16, 8};
+  for (int wi = 0; wi < 3; ++wi) {
+    const int W = Ws[wi];
+    if (W > Wpref) continue;
+    int S = opt.panel_ctas > 0 ? opt.panel_ctas : (int)std::min<int64_t>(g_pf_cap, (rows + 255) / 256);
+    S = std::max(1, std::min(S, PF_MAX_CTAS));
+    for (; S <= PF_MAX_CTAS; ++S) {
+      const int64_t R = (rows + S - 1) / S;
+      const size_t smem = pf_smem_bytes(W, R, (int)w);
+      if (smem > smax) continue;
+      int occ = 0;
+      CKR(pf_occupancy(W, smem, &occ));
+      if ((int64_t)occ * c.sms < S) break;
+      int S_eff = (int)((rows + R - 1) / R);
+      PanelArgs p;
+      p.a = a; p.lda = lda; p.m = m; p.r0 = r0; p.col0 = c0; p.w = (int)w; p.R = R;
+      p.piv = piv; p.info = info; p.ll = c.ll; p.epoch = c.epoch; p.exact = opt.exact;
+      p.prof = g_prof;
+      p.variant = g_variant;
+      void* args[] = {&p};
+      const void* fn = W == 8 ? (const void*)panel_kernel<8> : W == 16 ? (const void*)panel_kernel<16>
+                                                                       : (const void*)panel_kernel<32>;
+      CK(cudaLaunchCooperativeKernel(fn, dim3(S_eff), dim3(PF_THREADS), args, smem, st));
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return PFLU_OK;
+    }
+  }
+  return set_err(PFLU_ERR_UNSUPPORTED, "panel of %lld rows x %lld does not fit the persistent panel kernel",
+                 (long long)rows, (long long)w);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -486,6 +549,12 @@ extern "C" {
 int pflu_version(void) { return 1; }
 
 long long pflu_launch_count(void) { return g_launches.load(); }
+
+// Developer hook (not in pflu.h): per-phase clock64 totals of the panel kernel's CTA 0.
+int pflu_debug_panel_profile(void* dev_buf) {
+  g_prof = (unsigned long long*)dev_buf;
+  return PFLU_OK;
+}
 
 const char* pflu_last_error(void) { return g_err.c_str(); }
 

@@ -288,19 +288,87 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_getf2_kernel(LeafArgs p)
 
 constexpr int PLAN_MAX = 1024;
 
+// Parallel composition.  With piv[i] >= i (LAPACK getrf), let g(i) be the original row whose data
+// sits in row d+i just before swap i.  Row d+i only changes before step i when an earlier swap
+// targets it, so g(i) = g(pt(i)) with pt(i) = last i' < i with piv[i'] = d+i, else g(i) = d+i.
+// Then (PA)[d+i] = A[src(i)] with src(i) = g(i) if piv[i] == d+i, else g(ps(i)) for
+// ps(i) = last i' < i with piv[i'] == piv[i], else the original row piv[i].  An extra row R >= d+np
+// finally holds g(last i with piv[i] == R).  pt() chains are resolved by pointer jumping.
+// General laswp (pflu_laswp) may pass piv[i] < d+i; then the sequential fallback is used.
 __global__ void __launch_bounds__(256) pivot_plan_kernel(const int64_t* __restrict__ piv, int64_t d,
                                                           int np, int64_t* __restrict__ plan) {
   __shared__ long long spiv[PLAN_MAX];
-  __shared__ int first_occ[PLAN_MAX];  // extra rows: first swap index with the same row; -1 for top rows
-  __shared__ int ext_id[PLAN_MAX];     // for first occurrences: their extra slot id (np + e)
-  __shared__ int ext_first[PLAN_MAX];  // extra slot e -> first swap index i
-  __shared__ int slot_of[PLAN_MAX];    // slot targeted by swap i
-  __shared__ int contents[2 * PLAN_MAX];
-  __shared__ int s_ne;
+  __shared__ int ptr_[PLAN_MAX];
+  __shared__ long long g[PLAN_MAX];
+  __shared__ int flags[2];
   const int tid = threadIdx.x;
   const long long top_end = d + np;
+  if (tid == 0) { flags[0] = 0; flags[1] = 0; }
   for (int i = tid; i < np; i += blockDim.x) spiv[i] = piv[d + i];
+  for (int i = tid; i < np; i += blockDim.x) ptr_[i] = -1;
   __syncthreads();
+  for (int i = tid; i < np; i += blockDim.x)
+    if (spiv[i] < d + i) flags[1] = 1;  // not a getrf pivot sequence
+  __syncthreads();
+  if (flags[1] == 0) {
+    // pt(i): atomicMax over earlier swaps targeting top row d+i (only i' <= i can target it)
+    for (int i = tid; i < np; i += blockDim.x) {
+      const long long r = spiv[i];
+      if (r < top_end && r != d + i) atomicMax(&ptr_[(int)(r - d)], i);
+    }
+    __syncthreads();
+    for (int i = tid; i < np; i += blockDim.x) g[i] = ptr_[i] < 0 ? d + i : -1;
+    __syncthreads();
+    // pointer jumping: g[i] = g[ptr[i]] until resolved (chains strictly decrease the index)
+    for (int round = 0; round < 12; ++round) {
+      if (tid == 0) flags[0] = 0;
+      __syncthreads();
+      for (int i = tid; i < np; i += blockDim.x) {
+        if (g[i] < 0) {
+          const int p = ptr_[i];
+          if (g[p] >= 0) g[i] = g[p];
+          else { ptr_[i] = ptr_[p]; flags[0] = 1; }
+        }
+      }
+      __syncthreads();
+      if (flags[0] == 0) break;
+      __syncthreads();
+    }
+    int ne_local = 0;
+    __shared__ int s_ne;
+    if (tid == 0) s_ne = 0;
+    __syncthreads();
+    for (int i = tid; i < np; i += blockDim.x) {
+      const long long r = spiv[i];
+      int ps = -1, nxt = -1;
+      for (int k = 0; k < np; ++k) {
+        if (spiv[k] == r) {
+          if (k < i) ps = k;
+          else if (k > i && nxt < 0) nxt = k;
+        }
+      }
+      long long src;
+      if (r == d + i) src = g[i];
+      else if (ps >= 0) src = g[ps];
+      else src = r;
+      plan[1 + i] = src;
+      if (r >= top_end && nxt < 0) {  // last swap into extra row r
+        const int e = atomicAdd(&s_ne, 1);
+        plan[1 + np + 2 * e] = r;
+        plan[1 + np + 2 * e + 1] = g[i];
+      }
+    }
+    (void)ne_local;
+    __syncthreads();
+    if (tid == 0) plan[0] = s_ne;
+    return;
+  }
+  // sequential fallback (general laswp pivots): slots for rows outside [d, d+np)
+  __shared__ int first_occ[PLAN_MAX];
+  __shared__ int ext_first[PLAN_MAX];
+  __shared__ int slot_of[PLAN_MAX];
+  __shared__ int contents[2 * PLAN_MAX];
+  __shared__ int s_ne2;
   for (int i = tid; i < np; i += blockDim.x) {
     const long long r = spiv[i];
     int fo = -1;
@@ -315,25 +383,25 @@ __global__ void __launch_bounds__(256) pivot_plan_kernel(const int64_t* __restri
   if (tid == 0) {
     int ne = 0;
     for (int i = 0; i < np; ++i)
-      if (first_occ[i] == i) { ext_first[ne] = i; ext_id[i] = np + ne; ++ne; }
-    s_ne = ne;
+      if (first_occ[i] == i) { ext_first[ne] = i; ptr_[i] = np + ne; ++ne; }
+    s_ne2 = ne;
   }
   __syncthreads();
-  const int ne = s_ne;
+  const int ne = s_ne2;
   for (int i = tid; i < np; i += blockDim.x) {
     const long long r = spiv[i];
-    slot_of[i] = (r >= d && r < top_end) ? (int)(r - d) : ext_id[first_occ[i]];
+    slot_of[i] = (r >= d && r < top_end) ? (int)(r - d) : ptr_[first_occ[i]];
   }
-  for (int s = tid; s < np + ne; s += blockDim.x) contents[s] = s;
+  for (int s2 = tid; s2 < np + ne; s2 += blockDim.x) contents[s2] = s2;
   __syncthreads();
   if (tid == 0) {
     for (int i = 0; i < np; ++i) {
-      const int s = slot_of[i];
-      if (s != i) { const int t = contents[i]; contents[i] = contents[s]; contents[s] = t; }
+      const int s2 = slot_of[i];
+      if (s2 != i) { const int t = contents[i]; contents[i] = contents[s2]; contents[s2] = t; }
     }
   }
   __syncthreads();
-  auto row_of = [&](int s) -> long long { return s < np ? d + s : spiv[ext_first[s - np]]; };
+  auto row_of = [&](int s2) -> long long { return s2 < np ? d + s2 : spiv[ext_first[s2 - np]]; };
   if (tid == 0) plan[0] = ne;
   for (int i = tid; i < np; i += blockDim.x) plan[1 + i] = row_of(contents[i]);
   for (int e = tid; e < ne; e += blockDim.x) {
@@ -343,10 +411,79 @@ __global__ void __launch_bounds__(256) pivot_plan_kernel(const int64_t* __restri
 }
 
 // ==========================================================================================
+// Unit-lower triangular solve of a TW-column tile held in shared memory:
+//   X (np x TW, row-major in smem) := unit_lower(L)^-1 X,  L global (leading dimension ldl).
+// Exact reference order (_jit.py:109-113): every x_r takes x_r -= L_ri * x_i for i ascending,
+// multiply then subtract.  Blocked by DB = TW rows: the DB x DB diagonal block is solved in
+// registers by TW threads (one column each, no barriers), then the rows below are updated from an
+// smem-staged L panel with 4 independent rows per thread in flight.  Lst: >= max(np, TW) * TW doubles.
+
+template <int TW>
+__device__ __forceinline__ void tile_trsm_smem(double* X, double* Lst, const double* __restrict__ L, int64_t ldl,
+                                               int np) {
+  constexpr int DB = TW;
+  constexpr int RL = 256 / TW;
+  const int tid = threadIdx.x, col = tid % TW, rl = tid / TW;
+  for (int ib = 0; ib < np; ib += DB) {
+    const int nb = min(DB, np - ib);
+    const int nrows = np - ib;
+    __syncthreads();  // previous readers of Lst / writers of X are done
+    for (int idx = tid; idx < nrows * DB; idx += 256) {
+      const int r = idx / DB, i = idx - r * DB;
+      Lst[idx] = (i < nb) ? L[(int64_t)(ib + r) * ldl + ib + i] : 0.0;
+    }
+    __syncthreads();
+    if (tid < TW) {
+      double x[DB];
+#pragma unroll
+      for (int i = 0; i < DB; ++i) x[i] = (i < nb) ? X[(ib + i) * TW + col] : 0.0;
+#pragma unroll
+      for (int i = 0; i < DB; ++i) {
+#pragma unroll
+        for (int r = i + 1; r < DB; ++r) x[r] = sub_mul_exact(x[r], Lst[r * DB + i], x[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < DB; ++i)
+        if (i < nb) X[(ib + i) * TW + col] = x[i];
+    }
+    __syncthreads();
+    if (ib + nb < np) {
+      double xi[DB];
+#pragma unroll
+      for (int i = 0; i < DB; ++i) xi[i] = (i < nb) ? X[(ib + i) * TW + col] : 0.0;
+      int r = ib + nb + rl;
+      for (; r + 3 * RL < np; r += 4 * RL) {
+        double y0 = X[r * TW + col], y1 = X[(r + RL) * TW + col];
+        double y2 = X[(r + 2 * RL) * TW + col], y3 = X[(r + 3 * RL) * TW + col];
+        const double* l0 = Lst + (r - ib) * DB;
+#pragma unroll
+        for (int i = 0; i < DB; ++i) {
+          y0 = sub_mul_exact(y0, l0[i], xi[i]);
+          y1 = sub_mul_exact(y1, l0[RL * DB + i], xi[i]);
+          y2 = sub_mul_exact(y2, l0[2 * RL * DB + i], xi[i]);
+          y3 = sub_mul_exact(y3, l0[3 * RL * DB + i], xi[i]);
+        }
+        X[r * TW + col] = y0;
+        X[(r + RL) * TW + col] = y1;
+        X[(r + 2 * RL) * TW + col] = y2;
+        X[(r + 3 * RL) * TW + col] = y3;
+      }
+      for (; r < np; r += RL) {
+        double y0 = X[r * TW + col];
+        const double* l0 = Lst + (r - ib) * DB;
+#pragma unroll
+        for (int i = 0; i < DB; ++i) y0 = sub_mul_exact(y0, l0[i], xi[i]);
+        X[r * TW + col] = y0;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // K2/K3: laswp by plan, optionally fused with the unit-lower triangular solve of the top block
 // (U12 := L11^-1 * P * A12).  One CTA per TW-column tile of [c0, c1).  All reads of original
 // values complete (barrier) before any write, so the in-place permutation is race free.
-// The solve follows _jit.py:109-113 exactly: x_r -= L_ri * x_i for i ascending, mul then sub.
+// Smem: X [np][TW] (new top block) + E [max(np, 1024/TW)][TW] (extra rows, then the L panel).
 
 template <int TW>
 __global__ void __launch_bounds__(256) swap_trsm_kernel(double* __restrict__ a, int64_t lda, int64_t d,
@@ -355,7 +492,7 @@ __global__ void __launch_bounds__(256) swap_trsm_kernel(double* __restrict__ a, 
                                                          const double* __restrict__ L, int64_t ldl,
                                                          int do_trsm) {
   extern __shared__ double st_smem[];
-  constexpr int RL = 256 / TW;  // row lanes
+  constexpr int RL = 256 / TW;
   const int tid = threadIdx.x;
   const int col = tid % TW;
   const int rl = tid / TW;
@@ -364,52 +501,25 @@ __global__ void __launch_bounds__(256) swap_trsm_kernel(double* __restrict__ a, 
   const bool cok = gc < c1;
   const int ne = (int)plan[0];
   double* X = st_smem;              // [np][TW] new top block
-  double* E = st_smem + np * TW;    // [max(ne*TW, 1024)] values for extra rows, then L11 blocks
+  double* E = st_smem + np * TW;    // [ne][TW] values for extra rows, later the staged L panel
   for (int i = rl; i < np; i += RL) {
-    int64_t src = plan[1 + i];
+    const int64_t src = plan[1 + i];
     X[i * TW + col] = cok ? a[src * lda + gc] : 0.0;
   }
   for (int e = rl; e < ne; e += RL) {
-    int64_t src = plan[1 + np + 2 * e + 1];
+    const int64_t src = plan[1 + np + 2 * e + 1];
     E[e * TW + col] = cok ? a[src * lda + gc] : 0.0;
   }
   __syncthreads();
   if (cok)
     for (int e = rl; e < ne; e += RL) a[plan[1 + np + 2 * e] * lda + gc] = E[e * TW + col];
-  if (do_trsm) {
-    double* Lb = E;  // reuse: 32 x 32 diagonal block of L
-    for (int ib = 0; ib < np; ib += 32) {
-      const int nb = min(32, np - ib);
-      __syncthreads();
-      for (int idx = tid; idx < nb * nb; idx += 256) {
-        int r = idx / nb, i = idx - r * nb;
-        Lb[r * 32 + i] = L[(ib + r) * ldl + ib + i];
-      }
-      __syncthreads();
-      // diagonal block, one pivot row at a time
-      for (int i = 0; i < nb - 1; ++i) {
-        const double xi = X[(ib + i) * TW + col];
-        for (int r = i + 1 + rl; r < nb; r += RL)
-          X[(ib + r) * TW + col] = sub_mul_exact(X[(ib + r) * TW + col], Lb[r * 32 + i], xi);
-        __syncthreads();
-      }
-      // rows below: x_r -= sum_{i in block, ascending} L_ri x_i
-      for (int r = ib + nb + rl; r < np; r += RL) {
-        const double* Lr = L + (int64_t)r * ldl + ib;
-        double xr = X[r * TW + col];
-        for (int i = 0; i < nb; ++i) xr = sub_mul_exact(xr, __ldg(Lr + i), X[(ib + i) * TW + col]);
-        X[r * TW + col] = xr;
-      }
-    }
-    __syncthreads();
-  }
+  if (do_trsm) tile_trsm_smem<TW>(X, E, L, ldl, np);
+  else __syncthreads();
   if (cok)
     for (int i = rl; i < np; i += RL) a[(d + i) * lda + gc] = X[i * TW + col];
 }
 
 // Plain unit-lower solve X := unit_lower(L)^-1 X (no swaps), X = np rows x [0, ncols) columns.
-// Used inside the recursive panel, where the leaf already applied its interchanges across the
-// panel width, and for pflu_trsm.  Same op order as the fused kernel (_jit.py:109-113).
 template <int TW>
 __global__ void __launch_bounds__(256) trsm_kernel(const double* __restrict__ L, int64_t ldl,
                                                     double* __restrict__ Xg, int64_t ldx, int np,
@@ -422,30 +532,9 @@ __global__ void __launch_bounds__(256) trsm_kernel(const double* __restrict__ L,
   const int64_t gc = (int64_t)blockIdx.x * TW + col;
   const bool cok = gc < ncols;
   double* X = st_smem;
-  double* Lb = st_smem + np * TW;
+  double* Lst = st_smem + np * TW;
   for (int i = rl; i < np; i += RL) X[i * TW + col] = cok ? Xg[i * ldx + gc] : 0.0;
-  for (int ib = 0; ib < np; ib += 32) {
-    const int nb = min(32, np - ib);
-    __syncthreads();
-    for (int idx = tid; idx < nb * nb; idx += 256) {
-      int r = idx / nb, i = idx - r * nb;
-      Lb[r * 32 + i] = L[(ib + r) * ldl + ib + i];
-    }
-    __syncthreads();
-    for (int i = 0; i < nb - 1; ++i) {
-      const double xi = X[(ib + i) * TW + col];
-      for (int r = i + 1 + rl; r < nb; r += RL)
-        X[(ib + r) * TW + col] = sub_mul_exact(X[(ib + r) * TW + col], Lb[r * 32 + i], xi);
-      __syncthreads();
-    }
-    for (int r = ib + nb + rl; r < np; r += RL) {
-      const double* Lr = L + (int64_t)r * ldl + ib;
-      double xr = X[r * TW + col];
-      for (int i = 0; i < nb; ++i) xr = sub_mul_exact(xr, __ldg(Lr + i), X[(ib + i) * TW + col]);
-      X[r * TW + col] = xr;
-    }
-  }
-  __syncthreads();
+  tile_trsm_smem<TW>(X, Lst, L, ldl, np);
   if (cok)
     for (int i = rl; i < np; i += RL) Xg[i * ldx + gc] = X[i * TW + col];
 }

@@ -141,6 +141,20 @@ def test_laswp_random(cuda, seed, m, ncols, k1, k2):
     assert bitwise_equal(x.cpu().numpy(), want)
 
 
+def test_laswp_general_pivots(cuda):
+    """Pivots below the current row (allowed by the reference laswp, kernels.py:273-300)."""
+    import torch
+
+    rng = np.random.default_rng(17)
+    x0 = rng.standard_normal((300, 40))
+    piv0 = np.array([rng.integers(0, 300) for _ in range(120)], dtype=np.int64)
+    want = oracle.laswp(x0.copy(), piv0, 7, 120)
+    x = _t(x0, cuda)
+    piv = torch.from_numpy(piv0).to(cuda)
+    _lib().check(_lib().load().pflu_laswp(x.data_ptr(), 40, 0, 40, piv.data_ptr(), 7, 120, _stream()), "laswp")
+    assert bitwise_equal(x.cpu().numpy(), want)
+
+
 def test_laswp_roundtrip_and_identity(cuda):
     # reference test_kernels.py:335-396: identity is a no-op; applying inverse swaps restores
     import torch

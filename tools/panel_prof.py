@@ -1,0 +1,68 @@
+"""Per-phase clock breakdown of the persistent panel kernel (CTA 0), via pflu_debug_panel_profile."""
+import ctypes
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1804_07017_b200 import _lib  # noqa: E402
+
+NAMES = ["load", "A:argmax", "B:publish", "C:gather", "D:winner", "E:update", "sync1", "swaps+sync2", "U-trsm", "blk-update"]
+m = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+w = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+ctas = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+leaf = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+exact = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+L = _lib.load()
+L.pflu_debug_panel_profile.argtypes = [ctypes.c_void_p]
+dev = torch.device("cuda:0")
+prof = torch.zeros(16384 + 32 * 256, dtype=torch.int64, device=dev)
+x0 = torch.rand(m, w, dtype=torch.float64, device=dev) * 2 - 1
+x = x0.clone()
+piv = torch.zeros(w, dtype=torch.int64, device=dev)
+info = ctypes.c_int64(0)
+opt = _lib.options(exact=bool(exact), panel_ctas=ctas, leaf_width=leaf)
+st = torch.cuda.current_stream().cuda_stream
+run = lambda: _lib.check(L.pflu_panel(x.data_ptr(), w, m, 0, 0, w, piv.data_ptr(), ctypes.byref(info), st, ctypes.byref(opt)), "p")  # noqa
+for _ in range(2):
+    x.copy_(x0)
+    run()
+torch.cuda.synchronize()
+x.copy_(x0)
+L.pflu_debug_panel_profile(prof.data_ptr())
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+run()
+e1.record()
+torch.cuda.synchronize()
+L.pflu_debug_panel_profile(None)
+ms = e0.elapsed_time(e1)
+PP = prof.cpu()[:4096].view(256, 16)
+P = PP[:, :10]
+nz = int((P.sum(1) > 0).sum())
+P = P[:nz].double() / 1965.0
+print(f"panel m={m} w={w} ctas={ctas} W={leaf} exact={exact}: {ms:.3f} ms; {nz} CTAs; phases us (min/mean/max over CTAs):")
+for i, n in enumerate(NAMES):
+    col = P[:, i]
+    print(f"   {n:12s} {col.min():8.0f} {col.mean():8.0f} {col.max():8.0f}   argmax CTA {int(col.argmax())}")
+
+T = PP[:nz, 10:16].double()
+for jj in range(3):
+    pub = T[:, 2 * jj]
+    got = T[:, 2 * jj + 1]
+    t0 = pub.min()
+    print(f"   col {4 + jj}: publish spread {float(pub.max() - t0) / 1e3:.2f} us (last CTA {int(pub.argmax())}); "
+          f"gather done {float(got.min() - t0) / 1e3:.2f}..{float(got.max() - t0) / 1e3:.2f} us after first publish")
+
+G = prof.cpu()[4096:4096 + w].double() / 1965.0
+print("   per-column gather us (CTA 0):", " ".join(f"{x:.1f}" for x in G.tolist()[:64]))
+print(f"   gather us: mean {G.mean():.2f} median {G.median():.2f} max {G.max():.1f}")
+
+Wk = prof.cpu()[8192:8192 + 32 * 256].view(32, 256)[:min(nz, 32), :w].double() / 1965.0
+for col in range(33, 41):
+    v = Wk[:, col]
+    print(f"   col {col}: local work before publish: max {v.max():.1f} us on CTA {int(v.argmax())}, median {v.median():.1f}")
+
+Gq = prof.cpu()[16384:16384 + 32 * 256].view(32, 256)[:min(nz, 32), :w].double() / 1965.0
+for q in range(min(nz, 32)):
+    print(f"   CTA {q:2d} gather cols 32..47:", " ".join(f"{x:.1f}" for x in Gq[q, 32:48].tolist()))
