@@ -25,6 +25,7 @@
 #include "../../include/pflu.h"
 #include "pflu_kernels.cuh"
 #include "pflu_panel.cuh"
+#include "pflu_gemm.cuh"
 
 namespace pflu {
 
@@ -63,13 +64,10 @@ struct DevCtx {
   int sms = 0;
   size_t smem_optin = 0;
   cudaStream_t sP = nullptr, sU = nullptr;
-  double* slots = nullptr;
-  unsigned* bar = nullptr;
   int64_t* plan[2] = {nullptr, nullptr};
   unsigned long long* info = nullptr;
   unsigned long long* ll = nullptr;  // LL exchange words of the panel kernel
   unsigned* epoch = nullptr;
-  int leaf_occ[3] = {0, 0, 0};  // max active CTAs/SM for W = 8, 16, 32 at max smem (set lazily)
   std::vector<cudaEvent_t> ev;  // event pool (ordering only)
   std::vector<cudaEvent_t> tev; // timing event pool (tracing)
 };
@@ -77,6 +75,9 @@ struct DevCtx {
 static std::atomic<long long> g_launches{0};
 static unsigned long long* g_prof = nullptr;
 static int g_pf_cap = []() { const char* e = getenv("PFLU_PANEL_CAP"); return e ? atoi(e) : 32; }();
+static int g_gemm_variant = []() { const char* e = getenv("PFLU_GEMM_VARIANT"); return e ? atoi(e) : 0; }();
+static DevCtx* g_dc = nullptr;  // context of the current call (set by ctx_get)
+static int g_tur_grid = []() { const char* e = getenv("PFLU_TUR_GRID"); return e ? atoi(e) : 0; }();
 static int g_variant = []() { const char* e = getenv("PFLU_PANEL_VARIANT"); return e ? atoi(e) : 0; }();  // device buffer for panel-kernel phase clocks (tools only)
 
 // Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.
@@ -138,8 +139,6 @@ struct Tracer {
 static std::mutex g_mu;
 static DevCtx g_ctx[64];
 
-static constexpr int SLOT_MAX_CTAS = 1024;
-static constexpr int SLOT_MAX_W = 32;
 static constexpr int PF_MAX_CTAS = PF_THREADS;
 static constexpr size_t LL_WORDS = PF_LL_WORDS;
 
@@ -161,9 +160,6 @@ static int ctx_get(DevCtx** out) {
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&c.sP, cudaStreamNonBlocking, hi));
     CK(cudaStreamCreateWithPriority(&c.sU, cudaStreamNonBlocking, lo));
-    CK(cudaMalloc(&c.slots, sizeof(double) * 2 * (SLOT_MAX_CTAS + 1) * (SLOT_MAX_W + 2)));
-    CK(cudaMalloc(&c.bar, 64));
-    CK(cudaMemset(c.bar, 0, 64));
     CK(cudaMalloc(&c.plan[0], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
     CK(cudaMalloc(&c.plan[1], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
     CK(cudaMalloc(&c.info, 64));
@@ -185,22 +181,18 @@ static int ctx_get(DevCtx** out) {
     CK(allow((const void*)panel_kernel<8>));
     CK(allow((const void*)panel_kernel<16>));
     CK(allow((const void*)panel_kernel<32>));
-    CK(allow((const void*)leaf_getf2_kernel<8>));
-    CK(allow((const void*)leaf_getf2_kernel<16>));
-    CK(allow((const void*)leaf_getf2_kernel<32>));
     CK(allow((const void*)swap_trsm_kernel<8>));
     CK(allow((const void*)swap_trsm_kernel<16>));
     CK(allow((const void*)swap_trsm_kernel<32>));
     CK(allow((const void*)trsm_kernel<8>));
     CK(allow((const void*)trsm_kernel<16>));
     CK(allow((const void*)trsm_kernel<32>));
-    CK(allow((const void*)gemm_dmma_kernel<1>));
-    CK(allow((const void*)gemm_dmma_kernel<2>));
     CK(allow((const void*)gemm_exact_kernel<1>));
     CK(allow((const void*)gemm_exact_kernel<2>));
     c.ready = true;
   }
   *out = &c;
+  g_dc = &c;
   return PFLU_OK;
 }
 
@@ -218,26 +210,82 @@ static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t
 // ------------------------------------------------------------------------------------------
 // kernel launchers (all asynchronous on `st`)
 
+template <class C>
+static int launch_gemm_t(const GemmArgs& p0, bool v2, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(gemm_dmma_t<C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    CK(cudaFuncSetAttribute(gemm_dmma_t<C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  GemmArgs p = p0;
+  const int64_t tm = (p.M + C::BM - 1) / C::BM, tn = (p.N + C::BN - 1) / C::BN;
+  if (tm * tn > INT_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "gemm grid too large");
+  p.tiles_m = (int)tm;
+  p.tiles_n = (int)tn;
+  if (v2) gemm_dmma_t<C, 2><<<(unsigned)(tm * tn), C::THREADS, C::SMEM, st>>>(p);
+  else gemm_dmma_t<C, 1><<<(unsigned)(tm * tn), C::THREADS, C::SMEM, st>>>(p);
+  return PFLU_OK;
+}
+
+// persistent launch: at most `ctas` CTAs (0 = SMs x resident CTAs per SM)
+template <class C>
+static int launch_gemm_p(DevCtx& dc, const GemmArgs& p0, bool v2, int ctas, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(gemm_dmma_persistent<C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    CK(cudaFuncSetAttribute(gemm_dmma_persistent<C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  GemmArgs p = p0;
+  const int64_t tm = (p.M + C::BM - 1) / C::BM, tn = (p.N + C::BN - 1) / C::BN;
+  if (tm * tn > INT_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "gemm grid too large");
+  p.tiles_m = (int)tm;
+  p.tiles_n = (int)tn;
+  int grid = ctas > 0 ? ctas : dc.sms * C::MINB;
+  grid = (int)std::min<int64_t>(grid, tm * tn);
+  if (v2) gemm_dmma_persistent<C, 2><<<grid, C::THREADS, C::SMEM, st>>>(p);
+  else gemm_dmma_persistent<C, 1><<<grid, C::THREADS, C::SMEM, st>>>(p);
+  return PFLU_OK;
+}
+
 static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, const double* b, int64_t ldb,
-                       int64_t M, int64_t N, int64_t K, bool exact, cudaStream_t st) {
+                       int64_t M, int64_t N, int64_t K, bool exact, cudaStream_t st, int pgrid = 0) {
   if (M <= 0 || N <= 0 || K <= 0) return PFLU_OK;
   GemmArgs p;
   p.c = c; p.a = a; p.b = b;
   p.ldc = ldc; p.lda = lda; p.ldb = ldb;
   p.M = M; p.N = N; p.K = K;
-  int64_t tm = (M + GM_BM - 1) / GM_BM, tn = (N + GM_BN - 1) / GM_BN;
-  if (tm * tn > INT_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "gemm grid too large");
-  p.tiles_m = (int)tm;
-  p.tiles_n = (int)tn;
   const bool v2 = aligned16(c) && aligned16(a) && aligned16(b) && (ldc % 2 == 0) && (lda % 2 == 0) &&
                   (ldb % 2 == 0);
-  dim3 grid((unsigned)(tm * tn));
   if (exact) {
+    int64_t tm = (M + GM_BM - 1) / GM_BM, tn = (N + GM_BN - 1) / GM_BN;
+    if (tm * tn > INT_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "gemm grid too large");
+    p.tiles_m = (int)tm;
+    p.tiles_n = (int)tn;
+    dim3 grid((unsigned)(tm * tn));
     if (v2) gemm_exact_kernel<2><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
     else gemm_exact_kernel<1><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
   } else {
-    if (v2) gemm_dmma_kernel<2><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
-    else gemm_dmma_kernel<1><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
+    switch (g_gemm_variant) {
+      case 1: CKR(launch_gemm_t<GV1>(p, v2, st)); break;
+      case 2: CKR(launch_gemm_t<GV2>(p, v2, st)); break;
+      case 3: CKR(launch_gemm_t<GV3>(p, v2, st)); break;
+      case 4: CKR(launch_gemm_t<GV4>(p, v2, st)); break;
+      case 5: CKR(launch_gemm_t<GV5>(p, v2, st)); break;
+      case 6: CKR(launch_gemm_t<GV6>(p, v2, st)); break;
+      case 7: CKR(launch_gemm_t<GV7>(p, v2, st)); break;
+      case 10: CKR(launch_gemm_p<GV0>(*g_dc, p, v2, 0, st)); break;
+      case 13: CKR(launch_gemm_p<GV3>(*g_dc, p, v2, 0, st)); break;
+      case 17: CKR(launch_gemm_p<GV7>(*g_dc, p, v2, 0, st)); break;
+      case 20: CKR(launch_gemm_p<GV0>(*g_dc, p, v2, g_dc->sms, st)); break;
+      case 21: CKR(launch_gemm_p<GV3>(*g_dc, p, v2, g_dc->sms, st)); break;
+      case 0:
+        if (pgrid != 0) CKR(launch_gemm_p<GV0>(*g_dc, p, v2, pgrid > 0 ? pgrid : 0, st));
+        else CKR(launch_gemm_t<GV0>(p, v2, st));
+        break;
+      default: CKR(launch_gemm_t<GV0>(p, v2, st)); break;
+    }
   }
   CK(cudaGetLastError());
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -291,93 +339,6 @@ static int launch_swap(double* a, int64_t lda, int64_t d, int np, const int64_t*
   return PFLU_OK;
 }
 
-struct LeafCfg {
-  int W = 32;
-  int S = 1;
-  int64_t R = 1;
-  size_t smem = 0;
-};
-
-template <int W>
-static size_t leaf_smem_bytes(int64_t R) {
-  return (size_t)(R * (W + 1) + 2 * W) * 8;
-}
-
-static int leaf_occupancy(DevCtx& c, int W, size_t smem, int* out) {
-  int occ = 0;
-  if (W == 8) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, leaf_getf2_kernel<8>, LEAF_THREADS, smem));
-  else if (W == 16) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, leaf_getf2_kernel<16>, LEAF_THREADS, smem));
-  else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, leaf_getf2_kernel<32>, LEAF_THREADS, smem));
-  *out = occ;
-  return PFLU_OK;
-}
-
-// Choose leaf width and CTA count for a panel of `rows` rows.
-static int choose_leaf(DevCtx& c, int64_t rows, const pflu_options& opt, LeafCfg* cfg) {
-  const size_t smax = c.smem_optin - 1024;
-  int S_want;
-  if (opt.panel_ctas > 0) S_want = opt.panel_ctas;
-  else S_want = (int)std::min<int64_t>(c.sms, std::max<int64_t>(1, (rows + 191) / 192));
-  S_want = std::max(1, std::min(S_want, SLOT_MAX_CTAS));
-  const int Ws[3] = {32, 16, 8};
-  for (int wi = 0; wi < 3; ++wi) {
-    int W = Ws[wi];
-    if (opt.leaf_width > 0 && W != opt.leaf_width) continue;
-    for (int S = S_want; S <= SLOT_MAX_CTAS; S = S < 8 ? S + 1 : S + S / 8) {
-      int64_t R = (rows + S - 1) / S;
-      size_t smem = (size_t)(R * (W + 1) + 2 * W) * 8;
-      if (smem > smax) continue;
-      int occ = 0;
-      CKR(leaf_occupancy(c, W, smem, &occ));
-      if ((int64_t)occ * c.sms < S) break;  // cannot be co-resident with this much smem
-      cfg->W = W; cfg->S = S; cfg->R = R; cfg->smem = smem;
-      return PFLU_OK;
-    }
-  }
-  return set_err(PFLU_ERR_UNSUPPORTED, "panel of %lld rows does not fit the cooperative leaf", (long long)rows);
-}
-
-static int launch_leaf(DevCtx& c, const LeafCfg& cfg, double* a, int64_t lda, int64_t m, int64_t r0, int64_t col0,
-                       int64_t w, int64_t pc0, int64_t pc1, int64_t* piv, unsigned long long* info, cudaStream_t st) {
-  LeafArgs p;
-  p.a = a; p.lda = lda; p.m = m; p.r0 = r0; p.col0 = col0; p.wact = w; p.pc0 = pc0; p.pc1 = pc1;
-  p.piv = piv; p.info = info; p.slots = c.slots; p.bar = c.bar;
-  const int64_t rows = m - r0;
-  int S = cfg.S;
-  int64_t R = (rows + S - 1) / S;
-  // shrink S for short sub-panels (fewer barrier participants, same smem bound)
-  while (S > 1 && (int64_t)(S - 1) * R >= rows) --S;
-  p.R = R;
-  void* args[] = {&p};
-  const void* fn = cfg.W == 8 ? (const void*)leaf_getf2_kernel<8>
-                 : cfg.W == 16 ? (const void*)leaf_getf2_kernel<16>
-                               : (const void*)leaf_getf2_kernel<32>;
-  size_t smem = (size_t)(R * (cfg.W + 1) + 2 * cfg.W) * 8;
-  CK(cudaLaunchCooperativeKernel(fn, dim3(S), dim3(LEAF_THREADS), args, smem, st));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return PFLU_OK;
-}
-
-// Recursive panel (Gustavson/Toledo split): rows [r0, m), storage columns [c0, c0 + w); the panel's
-// swap range is [pc0, pc1).  Exactness: every element still receives its updates in ascending
-// pivot order with the reference's rounding when opt.exact.
-static int panel_rec(DevCtx& c, const LeafCfg& cfg, double* a, int64_t lda, int64_t m, int64_t r0, int64_t c0,
-                     int64_t w, int64_t pc0, int64_t pc1, int64_t* piv, unsigned long long* info, bool exact,
-                     cudaStream_t st) {
-  if (w <= 0 || r0 >= m) return PFLU_OK;
-  if (w <= cfg.W) return launch_leaf(c, cfg, a, lda, m, r0, c0, w, pc0, pc1, piv, info, st);
-  int64_t w1 = ((w / 2 + 7) / 8) * 8;
-  if (w1 >= w) w1 = w / 2;
-  CKR(panel_rec(c, cfg, a, lda, m, r0, c0, w1, pc0, pc1, piv, info, exact, st));
-  const int np = (int)std::min(w1, m - r0);
-  const double* L = a + r0 * lda + c0;
-  CKR(launch_trsm(L, lda, np, a + r0 * lda + c0 + w1, lda, w - w1, st));
-  if (r0 + w1 >= m) return PFLU_OK;  // short panel: no rows below the left half
-  CKR(launch_gemm(a + (r0 + w1) * lda + c0 + w1, lda, a + (r0 + w1) * lda + c0, lda, a + r0 * lda + c0 + w1, lda,
-                  m - r0 - w1, w - w1, w1, exact, st));
-  return panel_rec(c, cfg, a, lda, m, r0 + w1, c0 + w1, w - w1, pc0, pc1, piv, info, exact, st);
-}
-
 static int pf_occupancy(int W, size_t smem, int* occ) {
   if (W == 8) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, panel_kernel<8>, PF_THREADS, smem));
   else if (W == 16) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, panel_kernel<16>, PF_THREADS, smem));
@@ -416,7 +377,6 @@ static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0
       p.a = a; p.lda = lda; p.m = m; p.r0 = r0; p.col0 = c0; p.w = (int)w; p.R = R;
       p.piv = piv; p.info = info; p.ll = c.ll; p.epoch = c.epoch; p.exact = opt.exact;
       p.prof = g_prof;
-      p.variant = g_variant;
       void* args[] = {&p};
       const void* fn = W == 8 ? (const void*)panel_kernel<8> : W == 16 ? (const void*)panel_kernel<16>
                                                                        : (const void*)panel_kernel<32>;
@@ -456,8 +416,9 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     const int64_t below = s.col0 + s.bw;
     if (below < m) {
       if (label != PFLU_TRACE_TU_L) CKR(tr.begin(PFLU_TRACE_GEMM, k, st, &t_g));
+      const int pg = label == PFLU_TRACE_TU ? -1 : (label == PFLU_TRACE_TU_R ? g_tur_grid : 0);
       CKR(launch_gemm(a + below * lda + lo, lda, a + below * lda + s.col0, lda, a + s.col0 * lda + lo, lda,
-                      m - below, hi - lo, s.bw, exact, st));
+                      m - below, hi - lo, s.bw, exact, st, pg));
       CKR(tr.end(t_g, st));
     }
     return tr.end(t_tu, st);

@@ -5,14 +5,12 @@
 // operands are "K-contiguous" L21 rows and "N-contiguous" U12 rows.
 //
 // Kernels (reference functions they replace, pkg/src/panelforge/...):
-//   leaf_getf2_kernel   _jit.py:154-187 lu_unb_run  -- cooperative multi-CTA getf2 on a w<=32
-//                       column leaf; rows resident in shared memory, one grid barrier per column
 //   pivot_plan_kernel   _jit.py:141-151 laswp_run   -- composes b ascending swaps into a gather plan
 //   swap_trsm_kernel    _jit.py:141-151 + 104-113   -- laswp (gather/scatter by plan) fused with the
 //                       unit-lower triangular solve of the U12 block row
 //   trsm_kernel         _jit.py:104-113              -- in-panel unit-lower solve (no swaps)
-//   gemm_dmma_kernel    _jit.py:54-80 macro_run      -- C -= A*B on FP64 tensor cores (DMMA 8x8x4)
-//   gemm_exact_kernel   _jit.py:54-80 macro_run      -- same update, reference rounding (mul, then sub)
+//   gemm_exact_kernel   _jit.py:54-80 macro_run      -- C -= A*B in the reference rounding (mul, then sub)
+// The DMMA trailing-update GEMM lives in pflu_gemm.cuh, the panel kernel in pflu_panel.cuh.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -45,36 +43,6 @@ __device__ __forceinline__ double sub_mul_exact(double c, double a, double b) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Grid barrier for cooperative launches (sense/generation based, self-resetting).
-// bar[0] = arrival count, bar[1] = generation.  All CTAs of the grid must be co-resident
-// (guaranteed by cudaLaunchCooperativeKernel).
-
-__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.volatile.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p));
-  return v;
-}
-
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned gen = ld_volatile_u32(bar + 1);
-    __threadfence();
-    unsigned old = atomicAdd(bar, 1u);
-    if (old == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (ld_volatile_u32(bar + 1) == gen) {
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// ------------------------------------------------------------------------------------------
 // Pivot key: reproduces the sequential scan of _jit.py:163-170 (start with the diagonal, take a
 // row only if STRICTLY greater, so ties go to the smallest row and NaNs are never taken unless
 // the diagonal itself is NaN, in which case the diagonal is kept).
@@ -87,197 +55,6 @@ __device__ __forceinline__ double pivot_key(double x, bool is_diag) {
 // better(a, b): larger key wins; equal keys -> smaller row.
 __device__ __forceinline__ bool key_better(double ka, long long ra, double kb, long long rb) {
   return ka > kb || (ka == kb && ra < rb);
-}
-
-// ==========================================================================================
-// K1: leaf getf2 (cooperative).  Factors storage columns [col0, col0+wact) of rows [r0, m); the
-// diagonal of leaf column j is row r0 + j.  CTA q owns rows [r0 + q*R, r0 + (q+1)*R) and keeps their W leaf columns in shared memory.
-// Row interchanges are applied across the whole panel column range [pc0, pc1), like
-// lu_unb_run's full-width swap (_jit.py:175-179); columns outside the leaf are swapped in
-// global memory by the CTA that owns the pivot row.
-// Slots (global, double-buffered by column parity): per CTA (W + 2) doubles = candidate row,
-// key, row index; plus one diagonal-row entry.
-
-struct LeafArgs {
-  double* a;
-  int64_t lda, m;
-  int64_t r0;                   // diagonal row of the leaf's first column
-  int64_t col0;                 // storage column of the leaf's first column
-  int64_t wact;                 // leaf width (<= W)
-  int64_t pc0, pc1;             // panel storage-column range swapped across (contains the leaf)
-  int64_t R;                    // rows per CTA
-  int64_t* piv;                 // global 0-based pivot rows, entries [r0, r0 + wact)
-  unsigned long long* info;     // atomicMin of (first zero-pivot column + 1)
-  double* slots;                // 2 * (gridDim.x + 1) * (W + 2) doubles
-  unsigned* bar;                // grid barrier state (2 words, zero-initialised once)
-};
-
-constexpr int LEAF_THREADS = 256;
-
-template <int W>
-__global__ void __launch_bounds__(LEAF_THREADS, 1) leaf_getf2_kernel(LeafArgs p) {
-  extern __shared__ double leaf_smem[];
-  constexpr int LD = W + 1;  // odd stride: conflict-free column walks
-  const int tid = threadIdx.x;
-  const int q = blockIdx.x;
-  const int S = gridDim.x;
-  const int64_t rbeg = p.r0 + (int64_t)q * p.R;
-  const int64_t rend = min(p.m, rbeg + p.R);
-  const int nrows = (int)max((int64_t)0, rend - rbeg);
-  const int wact = (int)p.wact;
-  double* tile = leaf_smem;                    // [R][LD]
-  double* u = leaf_smem + p.R * LD;            // [W] pivot row
-  double* dg = u + W;                          // [W] old diagonal row
-  __shared__ double red_key[LEAF_THREADS / 32];
-  __shared__ long long red_row[LEAF_THREADS / 32];
-  __shared__ double s_key;
-  __shared__ long long s_row;
-  __shared__ int s_win;
-
-  // load own rows
-  for (int idx = tid; idx < nrows * wact; idx += LEAF_THREADS) {
-    int r = idx / wact, c = idx - r * wact;
-    tile[r * LD + c] = p.a[(rbeg + r) * p.lda + p.col0 + c];
-  }
-  __syncthreads();
-
-  const int64_t kmax = min((int64_t)wact, p.m - p.r0);
-  const int slot_stride = W + 2;
-  for (int j = 0; j < kmax; ++j) {
-    const int64_t c = p.r0 + j;  // diagonal row of leaf column j
-    const int par = j & 1;
-    double* slot_base = p.slots + (size_t)par * (S + 1) * slot_stride;
-    // ---- local argmax over own rows >= c
-    double bk = -3.0;
-    long long br = LLONG_MAX;
-    int64_t r_first = max((int64_t)0, c - rbeg);
-    for (int64_t r = r_first + tid; r < nrows; r += LEAF_THREADS) {
-      double k = pivot_key(tile[r * LD + j], rbeg + r == c);
-      if (key_better(k, rbeg + r, bk, br)) { bk = k; br = rbeg + r; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-      long long orr = __shfl_xor_sync(0xffffffffu, br, o);
-      if (key_better(ok, orr, bk, br)) { bk = ok; br = orr; }
-    }
-    if ((tid & 31) == 0) { red_key[tid >> 5] = bk; red_row[tid >> 5] = br; }
-    __syncthreads();
-    if (tid < 32) {
-      bk = tid < LEAF_THREADS / 32 ? red_key[tid] : -3.0;
-      br = tid < LEAF_THREADS / 32 ? red_row[tid] : LLONG_MAX;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-        long long orr = __shfl_xor_sync(0xffffffffu, br, o);
-        if (key_better(ok, orr, bk, br)) { bk = ok; br = orr; }
-      }
-      if (tid == 0) { s_key = bk; s_row = br; }
-    }
-    __syncthreads();
-    // ---- publish candidate row (+ key, row) and, if owned, the diagonal row
-    {
-      double* my = slot_base + (size_t)q * slot_stride;
-      const long long crow = s_row;
-      if (s_key > -2.0) {
-        for (int cc = tid; cc < wact; cc += LEAF_THREADS) my[cc] = tile[(crow - rbeg) * LD + cc];
-      }
-      if (tid == 0) { my[W] = s_key; my[W + 1] = (double)crow; }
-      if (c >= rbeg && c < rend) {
-        double* dslot = slot_base + (size_t)S * slot_stride;
-        for (int cc = tid; cc < wact; cc += LEAF_THREADS) dslot[cc] = tile[(c - rbeg) * LD + cc];
-      }
-    }
-    grid_barrier(p.bar, (unsigned)S);
-    // ---- global winner
-    {
-      bk = -3.0;
-      br = LLONG_MAX;
-      int wq = -1;
-      for (int t = tid; t < S; t += LEAF_THREADS) {
-        const double* sl = slot_base + (size_t)t * slot_stride;
-        double k = __ldcg(sl + W);
-        long long rr = (long long)__ldcg(sl + W + 1);
-        if (key_better(k, rr, bk, br)) { bk = k; br = rr; wq = t; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-        long long orr = __shfl_xor_sync(0xffffffffu, br, o);
-        int oq = __shfl_xor_sync(0xffffffffu, wq, o);
-        if (key_better(ok, orr, bk, br)) { bk = ok; br = orr; wq = oq; }
-      }
-      if ((tid & 31) == 0) { red_key[tid >> 5] = bk; red_row[tid >> 5] = br; }
-      __shared__ int red_q[LEAF_THREADS / 32];
-      if ((tid & 31) == 0) red_q[tid >> 5] = wq;
-      __syncthreads();
-      if (tid == 0) {
-        double k0 = red_key[0];
-        long long r0 = red_row[0];
-        int q0 = red_q[0];
-        for (int w = 1; w < LEAF_THREADS / 32; ++w)
-          if (key_better(red_key[w], red_row[w], k0, r0)) { k0 = red_key[w]; r0 = red_row[w]; q0 = red_q[w]; }
-        s_key = k0; s_row = r0; s_win = q0;
-      }
-      __syncthreads();
-    }
-    const double wkey = s_key;
-    const long long prow = s_row;
-    if (!(wkey > 0.0)) {
-      // exactly-zero pivot: info = c + 1, column left untouched (_jit.py:171-174)
-      if (q == 0 && tid == 0) {
-        p.piv[c] = c;
-        atomicMin(p.info, (unsigned long long)(c + 1));
-      }
-      __syncthreads();
-      continue;
-    }
-    {
-      const double* wsl = slot_base + (size_t)s_win * slot_stride;
-      for (int cc = tid; cc < wact; cc += LEAF_THREADS) u[cc] = __ldcg(wsl + cc);
-      if (prow != c && prow >= rbeg && prow < rend) {
-        const double* dslot = slot_base + (size_t)S * slot_stride;
-        for (int cc = tid; cc < wact; cc += LEAF_THREADS) dg[cc] = __ldcg(dslot + cc);
-      }
-      if (q == 0 && tid == 0) p.piv[c] = prow;
-    }
-    __syncthreads();
-    if (prow != c) {
-      if (c >= rbeg && c < rend)
-        for (int cc = tid; cc < wact; cc += LEAF_THREADS) tile[(c - rbeg) * LD + cc] = u[cc];
-      if (prow >= rbeg && prow < rend) {
-        for (int cc = tid; cc < wact; cc += LEAF_THREADS) tile[(prow - rbeg) * LD + cc] = dg[cc];
-        // full-panel-width swap of the columns outside the leaf (global memory)
-        double* r1 = p.a + c * p.lda;
-        double* r2 = p.a + prow * p.lda;
-        const int64_t nleft = p.col0 - p.pc0;
-        const int64_t nright = p.pc1 - (p.col0 + wact);
-        for (int64_t cc = tid; cc < nleft + nright; cc += LEAF_THREADS) {
-          int64_t col = cc < nleft ? p.pc0 + cc : p.col0 + wact + (cc - nleft);
-          double t1 = r1[col], t2 = r2[col];
-          r1[col] = t2;
-          r2[col] = t1;
-        }
-      }
-      __syncthreads();
-    }
-    // ---- scale by division (_jit.py:180-182) and rank-1 update, mul then sub (_jit.py:183-186)
-    {
-      const double pivot = u[j];
-      for (int64_t r = max((int64_t)0, c + 1 - rbeg) + tid; r < nrows; r += LEAF_THREADS) {
-        double* tr = tile + r * LD;
-        double l = __ddiv_rn(tr[j], pivot);
-        tr[j] = l;
-        for (int cc = j + 1; cc < wact; ++cc) tr[cc] = sub_mul_exact(tr[cc], l, u[cc]);
-      }
-    }
-    __syncthreads();
-  }
-  // write back own rows
-  for (int idx = tid; idx < nrows * wact; idx += LEAF_THREADS) {
-    int r = idx / wact, c = idx - r * wact;
-    p.a[(rbeg + r) * p.lda + p.col0 + c] = tile[r * LD + c];
-  }
 }
 
 // ==========================================================================================
@@ -334,7 +111,6 @@ __global__ void __launch_bounds__(256) pivot_plan_kernel(const int64_t* __restri
       if (flags[0] == 0) break;
       __syncthreads();
     }
-    int ne_local = 0;
     __shared__ int s_ne;
     if (tid == 0) s_ne = 0;
     __syncthreads();
@@ -358,7 +134,6 @@ __global__ void __launch_bounds__(256) pivot_plan_kernel(const int64_t* __restri
         plan[1 + np + 2 * e + 1] = g[i];
       }
     }
-    (void)ne_local;
     __syncthreads();
     if (tid == 0) plan[0] = s_ne;
     return;
@@ -616,94 +391,6 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
-}
-
-template <int VEC>
-__global__ void __launch_bounds__(GM_THREADS, 2) gemm_dmma_kernel(GemmArgs p) {
-  extern __shared__ __align__(128) double gm_smem[];
-  double* sA = gm_smem;                                 // [ST][BM*BK]
-  double* sB = gm_smem + GM_ST * GM_BM * GM_BK;         // [ST][BK*BN]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 1, wn = warp & 1;
-  int tm, tn;
-  tile_coords(blockIdx.x, p.tiles_m, p.tiles_n, tm, tn);
-  const int m0 = tm * GM_BM, n0 = tn * GM_BN;
-  const int KT = (int)((p.K + GM_BK - 1) / GM_BK);
-
-  // prologue: start the operand pipeline, then seed accumulators from C
-#pragma unroll
-  for (int s = 0; s < GM_ST - 1; ++s) {
-    if (s < KT) gemm_load_stage<VEC>(p, sA + s * GM_BM * GM_BK, sB + s * GM_BK * GM_BN, m0, n0, (int64_t)s * GM_BK, tid);
-    cp_async_commit();
-  }
-  double acc[8][4][2];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t row = m0 + wm * 64 + i * 8 + g;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t col = n0 + wn * 32 + j * 8 + 2 * t;
-      const double* cp = p.c + row * p.ldc + col;
-      if (VEC == 2 && row < p.M && col + 1 < p.N) {
-        double2 v = *reinterpret_cast<const double2*>(cp);
-        acc[i][j][0] = v.x;
-        acc[i][j][1] = v.y;
-      } else {
-        acc[i][j][0] = (row < p.M && col < p.N) ? cp[0] : 0.0;
-        acc[i][j][1] = (row < p.M && col + 1 < p.N) ? cp[1] : 0.0;
-      }
-    }
-  }
-
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<GM_ST - 2>();
-    __syncthreads();
-    {
-      const int nk = kt + GM_ST - 1;
-      const int s = nk % GM_ST;
-      if (nk < KT) gemm_load_stage<VEC>(p, sA + s * GM_BM * GM_BK, sB + s * GM_BK * GM_BN, m0, n0, (int64_t)nk * GM_BK, tid);
-      cp_async_commit();
-    }
-    const double* cA = sA + (kt % GM_ST) * GM_BM * GM_BK;
-    const double* cB = sB + (kt % GM_ST) * GM_BK * GM_BN;
-#pragma unroll
-    for (int kk = 0; kk < GM_BK; kk += 4) {
-      double af[8], bf[4];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int row = wm * 64 + i * 8 + g;
-        af[i] = cA[row * GM_BK + ((kk + t) ^ ((g & 3) << 2))];
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int col = wn * 32 + j * 8 + g;
-        bf[j] = -cB[(kk + t) * GM_BN + (col ^ (t << 2))];
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-  }
-  cp_async_wait<0>();
-
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t row = m0 + wm * 64 + i * 8 + g;
-    if (row >= p.M) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t col = n0 + wn * 32 + j * 8 + 2 * t;
-      double* cp = p.c + row * p.ldc + col;
-      if (VEC == 2 && col + 1 < p.N) {
-        *reinterpret_cast<double2*>(cp) = make_double2(acc[i][j][0], acc[i][j][1]);
-      } else {
-        if (col < p.N) cp[0] = acc[i][j][0];
-        if (col + 1 < p.N) cp[1] = acc[i][j][1];
-      }
-    }
-  }
 }
 
 // Same tiling and pipeline, SIMT arithmetic in the reference's rounding: per element p ascending,

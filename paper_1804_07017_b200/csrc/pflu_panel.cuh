@@ -42,7 +42,6 @@ struct PanelArgs {
   unsigned* epoch;         // flag base, advanced by every launch
   int exact;
   unsigned long long* prof;  // optional: per-phase clock64 totals of CTA 0 (tools/ only)
-  int variant;               // dev experiments: number of slot parities (2 or 4), poll backoff
 };
 
 #define PF_PROF_MARK(i)                                              \
@@ -372,7 +371,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     const int kb = kmax;  // pivots of this block
     const int nother = w - wb;
     // ---------------- 4. deferred swaps of this block on the panel's other columns
-    if (nother > 0 && kb > 0 && !(p.variant & 32)) {
+    if (nother > 0 && kb > 0) {
       if (tid == 0) {
         // slots: 0..kb-1 = rows cJ + i; extra slots for pivot rows >= cJ + kb (first occurrence)
         int ns = kb;
@@ -423,7 +422,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     // ---------------- 5. U_J = L_JJ^-1 A[J rows, right] and the block update of own rows
     const int right0 = jb + wb;
     const int nright = w - right0;
-    if (nright > 0 && kb > 0 && !(p.variant & 64)) {
+    if (nright > 0 && kb > 0) {
       for (int idx = tid; idx < W * W; idx += PF_THREADS) {
         const int r = idx / W, cc = idx - r * W;
         ljj[idx] = (r < kb && cc < kb) ? p.a[(cJ + r) * p.lda + p.col0 + jb + cc] : 0.0;
@@ -450,8 +449,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       const int64_t ub = max(rbeg, cJ + kb);
       const int nupd = (int)max((int64_t)0, rend - ub);
       const int toff = (int)(ub - rbeg);
-      if (p.variant & 16) {
-      } else if (!exact) {
+      if (!exact) {
         // DMMA: warp w handles 8-row groups w, w+8, ...; 64-column chunks; K = W (zero padded)
         const int ngroups = (nupd + 7) / 8;
         const int g = lane >> 2, t = lane & 3;
@@ -478,7 +476,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
                 dmma884(acc[nb][0], acc[nb][1], av, bv);
               }
             }
-            if (rok && !(p.variant & 128)) {
+            if (rok) {
 #pragma unroll
               for (int nb = 0; nb < 8; ++nb) {
                 const int col = c0 + nb * 8 + 2 * t;
@@ -486,7 +484,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
                 if (col + 1 < nright) crow[col + 1] = acc[nb][1];
               }
             }
-            if ((p.variant & 128) && acc[0][0] == 1.2345e-300) crow[0] = acc[1][1];
           }
         }
       } else {
