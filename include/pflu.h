@@ -85,9 +85,25 @@ int pflu_getrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b,
 /* Panel factorization (getf2 semantics, recursive + cooperative leaf): rows [d, m) of the
  * w columns starting at column `col`; the diagonal of panel column j is row d + j.  Row
  * interchanges are applied across the panel's w columns only.  Writes d_ipiv[d .. d+min(w,m-d))
- * (global 0-based rows).  *info: 0 or 1 + first zero-pivot ROW index d + j. */
+ * (global 0-based rows).  *info: 0 or 1 + first zero-pivot ROW index d + j.  With info == NULL the
+ * call is asynchronous on `stream` (see pflu_info_reset / pflu_info_read). */
 int pflu_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w,
                int64_t* d_ipiv, int64_t* info, void* stream, const pflu_options* opt);
+
+/* Asynchronous info handling for pflu_panel(..., info = NULL, ...): reset / read (blocking) the
+ * device-side "first zero pivot" word that asynchronous panel calls accumulate into. */
+int pflu_info_reset(void* stream);
+int pflu_info_read(int64_t* info, void* stream);
+
+/* Compose the ascending swaps d_ipiv[d .. d+nb) into a gather plan (device int64[1 + 3*nb], caller
+ * owned), for pflu_swap_trsm_plan.  Asynchronous on `stream`. */
+int pflu_pivot_plan(const int64_t* d_ipiv, int64_t d, int64_t nb, int64_t* d_plan, void* stream);
+
+/* laswp by a precomputed plan on columns [c0, c1) of rows >= d, then (if d_l != NULL) the nb top rows
+ * (d .. d+nb) of those columns := unit_lower(L)^-1 * rows, L = d_l (nb x nb, leading dimension ldl).
+ * Asynchronous; the multi-GPU driver's TU step for columns whose L11 lives in a broadcast buffer. */
+int pflu_swap_trsm_plan(double* d_a, int64_t lda, int64_t d, int64_t nb, const int64_t* d_plan, int64_t c0,
+                        int64_t c1, const double* d_l, int64_t ldl, void* stream);
 
 /* Row interchanges: for k = k1 .. k2-1 ascending, swap rows k and d_ipiv[k] on columns [c0, c1). */
 int pflu_laswp(double* d_a, int64_t lda, int64_t c0, int64_t c1, const int64_t* d_ipiv, int64_t k1,

@@ -23,7 +23,8 @@ TRACE_LABELS = {0: "PF", 1: "TU", 2: "TU_L", 3: "TU_R", 4: "GEMM"}
 EXPORTS = (
     "pflu_version", "pflu_launch_count", "pflu_last_error", "pflu_default_options", "pflu_device_count",
     "pflu_getrf", "pflu_getrf_device", "pflu_panel", "pflu_laswp", "pflu_swap_trsm",
-    "pflu_trsm", "pflu_gemm_update",
+    "pflu_trsm", "pflu_gemm_update", "pflu_info_reset", "pflu_info_read", "pflu_pivot_plan",
+    "pflu_swap_trsm_plan",
 )
 
 
@@ -82,6 +83,14 @@ def load():
         L.pflu_trsm.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _vp]
         L.pflu_gemm_update.restype = ctypes.c_int
         L.pflu_gemm_update.argtypes = [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp]
+        L.pflu_info_reset.restype = ctypes.c_int
+        L.pflu_info_reset.argtypes = [_vp]
+        L.pflu_info_read.restype = ctypes.c_int
+        L.pflu_info_read.argtypes = [_pi64, _vp]
+        L.pflu_pivot_plan.restype = ctypes.c_int
+        L.pflu_pivot_plan.argtypes = [_vp, _i64, _i64, _vp, _vp]
+        L.pflu_swap_trsm_plan.restype = ctypes.c_int
+        L.pflu_swap_trsm_plan.argtypes = [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp]
         _lib = L
         return L
 

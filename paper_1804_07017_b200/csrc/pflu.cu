@@ -608,9 +608,53 @@ int pflu_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int6
   DevCtx* c = nullptr;
   CKR(ctx_get(&c));
   cudaStream_t st = (cudaStream_t)stream;
+  if (!info) return panel_factor(*c, d_a, lda, m, d, col, w, d_ipiv, c->info, opt, st);  // asynchronous
   CK(cudaMemsetAsync(c->info, 0xff, 8, st));
   CKR(panel_factor(*c, d_a, lda, m, d, col, w, d_ipiv, c->info, opt, st));
   return finish_info(*c, st, info);
+}
+
+int pflu_info_reset(void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  CK(cudaMemsetAsync(c->info, 0xff, 8, (cudaStream_t)stream));
+  return PFLU_OK;
+}
+
+int pflu_info_read(int64_t* info, void* stream) {
+  if (!info) return -1;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  return finish_info(*c, (cudaStream_t)stream, info);
+}
+
+int pflu_pivot_plan(const int64_t* d_ipiv, int64_t d, int64_t nb, int64_t* d_plan, void* stream) {
+  if (!d_ipiv) return -1;
+  if (d < 0) return -2;
+  if (nb < 1 || nb > PLAN_MAX) return -3;
+  if (!d_plan) return -4;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  return launch_plan(d_ipiv, d, (int)nb, d_plan, (cudaStream_t)stream);
+}
+
+int pflu_swap_trsm_plan(double* d_a, int64_t lda, int64_t d, int64_t nb, const int64_t* d_plan, int64_t c0,
+                        int64_t c1, const double* d_l, int64_t ldl, void* stream) {
+  if (!d_a) return -1;
+  if (lda < 1) return -2;
+  if (d < 0) return -3;
+  if (nb < 1 || nb > PLAN_MAX) return -4;
+  if (!d_plan) return -5;
+  if (c0 < 0) return -6;
+  if (c1 < c0 || c1 > lda) return -7;
+  if (d_l && ldl < nb) return -9;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  return launch_swap(d_a, lda, d, (int)nb, d_plan, c0, c1, d_l, ldl, d_l != nullptr, (cudaStream_t)stream);
 }
 
 int pflu_laswp(double* d_a, int64_t lda, int64_t c0, int64_t c1, const int64_t* d_ipiv, int64_t k1, int64_t k2,

@@ -1,0 +1,397 @@
+"""Multi-GPU LU with partial pivoting: 1-D block-cyclic columns + per-step panel broadcast.
+
+SURVEY.md §8(e).  Column block j (width b) lives on rank j % P; every rank stores its blocks
+contiguously (row-major n x n_local).  Rows are not distributed, so the row interchanges of
+partial pivoting stay local to each rank.  Per step k (owner o = k % P):
+
+  owner o:   PF(k) on its local copy of block k            (pflu_panel, cooperative kernel)
+             pack rows [kb, n) of the factored panel         (contiguous (n - kb) x bw buffer)
+  all ranks: broadcast panel + pivots from o                 (torch.distributed -> NCCL on GPUs)
+             pivot plan; deferred left swaps on local blocks < k
+             TU on local blocks > k: laswp + L11^-1 (from the broadcast L11) + DMMA GEMM with L21
+
+Look-ahead (depth 1, dmf_la factor.py:455-515 across ranks): the owner of block k+1 first updates
+that block (TU_L) and factors / broadcasts it on a high-priority panel stream while every rank runs
+the rest of TU_R(k) on a low-priority update stream; events order TU_R(k+1) after the broadcast of
+panel k+1 and TU_L(k+1) after TU_R(k).
+
+The driver is written against a small kernel backend so that the SAME schedule runs
+  * on B200s through libpflu.so (CudaKernels: the product path), and
+  * on CPU tensors under gloo in tests/test_dist.py, where the test injects a backend built on the
+    CPU oracle (tests only; this module never imports the oracle).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+
+# ---------------------------------------------------------------------------------------------
+# block-cyclic bookkeeping
+
+def num_blocks(n: int, b: int) -> int:
+    return -(-n // b)
+
+
+def local_blocks(n: int, b: int, P: int, r: int) -> list[int]:
+    """Global block indices owned by rank r, in local storage order."""
+    return list(range(r, num_blocks(n, b), P))
+
+
+def local_cols(n: int, b: int, P: int, r: int) -> int:
+    return sum(min(b, n - j * b) for j in local_blocks(n, b, P, r))
+
+
+def local_col_of_block(j: int, b: int, P: int) -> int:
+    """Local storage column of global block j on its owner (all blocks before the last are full)."""
+    return (j // P) * b
+
+
+def local_cols_before(k: int, n: int, b: int, P: int, r: int) -> int:
+    """Number of local columns of rank r that belong to global blocks < k."""
+    return sum(min(b, n - j * b) for j in local_blocks(n, b, P, r) if j < k)
+
+
+def scatter_columns(a_full: torch.Tensor, b: int, P: int, r: int) -> torch.Tensor:
+    """Rank r's block-cyclic columns of a full n x n matrix, row-major contiguous."""
+    n = a_full.shape[1]
+    cols = [a_full[:, j * b: min(n, (j + 1) * b)] for j in local_blocks(n, b, P, r)]
+    return torch.cat(cols, dim=1).contiguous() if cols else a_full.new_empty((a_full.shape[0], 0))
+
+
+def gather_columns(local: list[torch.Tensor], n: int, b: int) -> torch.Tensor:
+    """Inverse of scatter_columns given every rank's local block (list indexed by rank)."""
+    P = len(local)
+    out = local[0].new_empty((local[0].shape[0], n))
+    for r in range(P):
+        c = 0
+        for j in local_blocks(n, b, P, r):
+            w = min(b, n - j * b)
+            out[:, j * b: j * b + w] = local[r][:, c: c + w]
+            c += w
+    return out
+
+
+def allgather_columns(a_loc: torch.Tensor, n: int, b: int, group=None) -> torch.Tensor:
+    """All-gather every rank's local columns into the full n x n matrix (padded to equal sizes,
+    since ranks own different numbers of columns)."""
+    P = dist.get_world_size(group)
+    wmax = max(local_cols(n, b, P, q) for q in range(P))
+    pad = a_loc.new_zeros((a_loc.shape[0], wmax))
+    pad[:, : a_loc.shape[1]] = a_loc
+    parts = [torch.empty_like(pad) for _ in range(P)]
+    dist.all_gather(parts, pad, group=group)
+    return gather_columns([parts[q][:, : local_cols(n, b, P, q)] for q in range(P)], n, b)
+
+
+# ---------------------------------------------------------------------------------------------
+# kernel backend of the product path: libpflu.so on torch CUDA tensors
+
+class CudaKernels:
+    """libpflu.so entry points on strided row-major torch CUDA views (pointer + leading dim)."""
+
+    is_cuda = True
+
+    def __init__(self, device: torch.device, exact: bool = False):
+        self.L = _lib.load()
+        self.device = device
+        self.opt = _lib.options(exact=exact)
+        self.exact = exact
+        lo, hi = torch.cuda.Stream.priority_range()
+        self.sP = torch.cuda.Stream(device=device, priority=hi)
+        self.sU = torch.cuda.Stream(device=device, priority=lo)
+
+    # streams / events
+    def stream(self, which: str):
+        return torch.cuda.stream(self.sP if which == "P" else self.sU)
+
+    def event(self):
+        return torch.cuda.Event()
+
+    def record(self, ev, which: str):
+        ev.record(self.sP if which == "P" else self.sU)
+
+    def wait(self, ev, which: str):
+        (self.sP if which == "P" else self.sU).wait_event(ev)
+
+    def begin(self):
+        cur = torch.cuda.current_stream(self.device)
+        self.sP.wait_stream(cur)
+        self.sU.wait_stream(cur)
+
+    def join(self):
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_stream(self.sP)
+        cur.wait_stream(self.sU)
+
+    def _st(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    # kernels (asynchronous on the current stream)
+    def info_reset(self):
+        _lib.check(self.L.pflu_info_reset(self._st()), "pflu_info_reset")
+
+    def info_read(self) -> int:
+        v = ctypes.c_int64(0)
+        _lib.check(self.L.pflu_info_read(ctypes.byref(v), self._st()), "pflu_info_read")
+        return int(v.value)
+
+    def panel(self, a, m: int, d: int, col: int, w: int, piv):
+        rc = self.L.pflu_panel(a.data_ptr(), a.stride(0), m, d, col, w, piv.data_ptr(), None, self._st(),
+                               ctypes.byref(self.opt))
+        _lib.check(rc, "pflu_panel")
+
+    def plan(self, piv, d: int, nb: int, plan):
+        _lib.check(self.L.pflu_pivot_plan(piv.data_ptr(), d, nb, plan.data_ptr(), self._st()), "pflu_pivot_plan")
+
+    def swap_trsm(self, a, d: int, nb: int, plan, c0: int, c1: int, l11=None):
+        if c1 <= c0:
+            return
+        lp = l11.data_ptr() if l11 is not None else None
+        ldl = l11.stride(0) if l11 is not None else nb
+        rc = self.L.pflu_swap_trsm_plan(a.data_ptr(), a.stride(0), d, nb, plan.data_ptr(), c0, c1, lp, ldl,
+                                        self._st())
+        _lib.check(rc, "pflu_swap_trsm_plan")
+
+    def gemm(self, c, a, b):
+        m, n = c.shape
+        k = a.shape[1]
+        if m == 0 or n == 0 or k == 0:
+            return
+        rc = self.L.pflu_gemm_update(c.data_ptr(), c.stride(0), a.data_ptr(), a.stride(0), b.data_ptr(),
+                                     b.stride(0), m, n, k, int(self.exact), self._st())
+        _lib.check(rc, "pflu_gemm_update")
+
+
+# ---------------------------------------------------------------------------------------------
+# the distributed driver
+
+def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, kernels=None, group=None,
+                       piv: torch.Tensor | None = None):
+    """Factor the block-cyclic distributed n x n matrix in place.
+
+    ``a_loc``: this rank's local columns (row-major, n rows, ``local_cols(n, b, P, rank)`` columns).
+    Returns ``(piv, info)``: the full 0-based pivot vector (identical on every rank) and the
+    1-based first zero-pivot column (0 if none), agreed over all ranks.
+    """
+    P = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    if kernels is None:
+        kernels = CudaKernels(a_loc.device)
+    dev = a_loc.device
+    if a_loc.shape[0] != n or a_loc.shape[1] != local_cols(n, b, P, r) or a_loc.stride(1) != 1:
+        raise ValueError("a_loc must be the row-major local block-cyclic columns (n x local_cols)")
+    nblk = num_blocks(n, b)
+    if piv is None:
+        piv = torch.zeros(n, dtype=torch.int64, device=dev)
+    pbuf = [torch.empty(n * b, dtype=torch.float64, device=dev) for _ in range(2)]
+    ppiv = [torch.empty(b, dtype=torch.int64, device=dev) for _ in range(2)]
+    plans = [torch.empty(1 + 3 * b, dtype=torch.int64, device=dev) for _ in range(2)]
+    ev_bc = [kernels.event() for _ in range(2)]
+    ev_tu = [kernels.event() for _ in range(2)]
+    kernels.begin()
+    with kernels.stream("P"):
+        kernels.info_reset()
+
+    def cols_before(k):
+        return local_cols_before(k, n, b, P, r)
+
+    def pf_pack_bcast(k):
+        """Owner: factor block k and pack it; everyone: broadcast + pivot plan (on the panel stream)."""
+        col0 = k * b
+        bw = min(b, n - col0)
+        rows = n - col0
+        o = k % P
+        buf = pbuf[k % 2][: rows * bw].view(rows, bw)
+        if r == o:
+            lc = local_col_of_block(k, b, P)
+            kernels.panel(a_loc, n, col0, lc, bw, piv)
+            buf.copy_(a_loc[col0:, lc: lc + bw])
+            ppiv[k % 2][:bw].copy_(piv[col0: col0 + bw])
+        if P > 1:
+            dist.broadcast(buf, src=o, group=group)
+            dist.broadcast(ppiv[k % 2][:bw], src=o, group=group)
+            if r != o:
+                piv[col0: col0 + bw].copy_(ppiv[k % 2][:bw])
+        kernels.plan(piv, col0, bw, plans[k % 2])
+        return buf
+
+    def update(k, buf, c0, c1):
+        """TU of step k on local columns [c0, c1): laswp + trsm (L11 from the broadcast) + GEMM."""
+        if c1 <= c0:
+            return
+        col0 = k * b
+        bw = min(b, n - col0)
+        kernels.swap_trsm(a_loc, col0, bw, plans[k % 2], c0, c1, buf[:bw, :bw])
+        if col0 + bw < n:
+            kernels.gemm(a_loc[col0 + bw:, c0:c1], buf[bw:, :], a_loc[col0: col0 + bw, c0:c1])
+
+    def left_swaps(k):
+        col0 = k * b
+        bw = min(b, n - col0)
+        kernels.swap_trsm(a_loc, col0, bw, plans[k % 2], 0, cols_before(k), None)
+
+    ncl = a_loc.shape[1]
+    if lookahead == 0:
+        for k in range(nblk):
+            with kernels.stream("P"):
+                buf = pf_pack_bcast(k)
+                left_swaps(k)
+                update(k, buf, cols_before(k + 1), ncl)
+    else:
+        bufs = {}
+        with kernels.stream("P"):
+            bufs[0] = pf_pack_bcast(0)
+            kernels.record(ev_bc[0], "P")
+        for k in range(nblk):
+            nxt = k + 1 < nblk
+            # columns of block k+1 on this rank (only its owner has them)
+            own_next = nxt and (k + 1) % P == r
+            lo_r = cols_before(k + 2) if own_next else cols_before(k + 1)
+            with kernels.stream("U"):
+                kernels.wait(ev_bc[k % 2], "U")
+                update(k, bufs[k], lo_r, ncl)
+                left_swaps(k)
+                kernels.record(ev_tu[k % 2], "U")
+            if nxt:
+                with kernels.stream("P"):
+                    if k > 0:
+                        kernels.wait(ev_tu[(k - 1) % 2], "P")
+                    if own_next:
+                        update(k, bufs[k], cols_before(k + 1), cols_before(k + 2))
+                    bufs[k + 1] = pf_pack_bcast(k + 1)
+                    kernels.record(ev_bc[(k + 1) % 2], "P")
+            bufs.pop(k - 1, None)
+    if kernels.is_cuda:
+        kernels.join()
+    with kernels.stream("P"):
+        info = kernels.info_read()
+    if P > 1:
+        t = torch.tensor([info if info > 0 else 2 ** 62], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        info = int(t.item())
+        info = 0 if info >= 2 ** 62 else info
+    return piv, info
+
+
+def lu_factor_dist(a, b: int = 256, lookahead: int = 1, exact: bool = False, return_info: bool = False):
+    """``lu_factor(..., n_gpus=P)``: every rank passes the same full matrix (numpy or torch); each
+    factors its block-cyclic columns on its own GPU and the factors are all-gathered back."""
+    import numpy as np
+
+    if not dist.is_initialized():
+        raise RuntimeError("n_gpus > 1 needs an initialised torch.distributed process group (one rank per GPU)")
+    P, r = dist.get_world_size(), dist.get_rank()
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", r % max(1, torch.cuda.device_count()))))
+    torch.cuda.set_device(dev)
+    full = torch.as_tensor(np.asarray(a, dtype=np.float64)) if not isinstance(a, torch.Tensor) else a
+    n = full.shape[1]
+    if full.shape[0] != n:
+        raise ValueError("the multi-GPU path factors square matrices")
+    a_loc = scatter_columns(full.to(dev), b, P, r)
+    piv, info = getrf_block_cyclic(a_loc, n, b, lookahead, CudaKernels(dev, exact=exact))
+    lu = allgather_columns(a_loc, n, b)
+    if not isinstance(a, torch.Tensor):
+        lu, piv = lu.cpu().numpy(), piv.cpu().numpy()
+    return (lu, piv, info) if return_info else (lu, piv)
+
+
+# ---------------------------------------------------------------------------------------------
+# bench.py --gpus N (torchrun, one rank per GPU)
+
+def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
+    import json
+    import time
+
+    import numpy as np
+
+    if not dist.is_initialized():
+        dist.init_process_group("nccl")
+    P, r = dist.get_world_size(), dist.get_rank()
+    local = int(os.environ.get("LOCAL_RANK", r))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    n, b, la = args.n, args.b, args.lookahead
+    full = np.random.default_rng(3).uniform(-1.0, 1.0, size=(n, n))
+    cols = [full[:, j * b: min(n, (j + 1) * b)] for j in local_blocks(n, b, P, r)]
+    host_loc = np.ascontiguousarray(np.concatenate(cols, axis=1))
+    del full, cols
+    a0 = torch.from_numpy(host_loc).to(dev)
+    a = torch.empty_like(a0)
+    piv = torch.zeros(n, dtype=torch.int64, device=dev)
+    kern = CudaKernels(dev)
+    L = _lib.load()
+
+    def step():
+        a.copy_(a0)
+        getrf_block_cyclic(a, n, b, la, kern, piv=piv)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local) if r == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    launches0 = L.pflu_launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    launches = L.pflu_launch_count() - launches0
+    clk = clocks.stop() if clocks else None
+    ms_step = float(ms.item()) / args.steps
+    value = lu_flops(n) / (ms_step * 1e-3) / 1e9
+    peak, peak_src = fp64_peak()
+    # end to end: full host matrix in, factors + pivots back on every rank (pinned host buffers)
+    e2e = None
+    if args.e2e_steps > 0:
+        from .api import lu_factor  # noqa: F401  (public API entry)
+
+        host = torch.from_numpy(np.random.default_rng(3).uniform(-1.0, 1.0, size=(n, n))).pin_memory()
+        ts = []
+        for it in range(args.e2e_steps + 1):
+            dist.barrier()
+            t0 = time.perf_counter()
+            lu, pv = lu_factor_dist(host, b=b, lookahead=la)
+            lu_h = lu.cpu()
+            torch.cuda.synchronize()
+            dist.barrier()
+            ts.append(time.perf_counter() - t0)
+            del lu, lu_h
+        tmax = torch.tensor([sum(ts[1:]) / len(ts[1:])], dtype=torch.float64, device=dev)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        e2e = {"value": lu_flops(n) / float(tmax.item()) / 1e9, "unit": unit, "h2d_bytes_per_step": n * n * 8,
+               "d2h_bytes_per_step": n * n * 8 + n * 8,
+               "api": "paper_1804_07017_b200.dist.lu_factor_dist(pinned host matrix) per rank"}
+    if r == 0:
+        line = {
+            "metric": metric, "value": value, "unit": unit, "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C4: LUpp n={n} U[-1,1) numpy seed 3, b={b}, look-ahead {la}", "n": n, "b": b,
+                       "lookahead": la, "parallelism": f"1-D block-cyclic columns over {P} GPUs, NCCL panel broadcast",
+                       "l2": "inputs larger than L2; local columns restored by a D2D copy inside each step",
+                       "fp64_peak_frac": value / 1e3 / (peak * P)},
+            "roofline": {"bound": "tensor", "achieved": None, "peak": peak * P, "unit": "TFLOP/s",
+                         "frac": value / 1e3 / (peak * P), "traffic": None, "peak_source": peak_src,
+                         "note": "aggregate over ranks; per-kernel roofline is reported by the N=1 line"},
+            "clocks": clk, "e2e": e2e, "gpu_launches": launches, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+

@@ -1,0 +1,96 @@
+"""Multi-process tests of the 1-D block-cyclic driver (paper_1804_07017_b200.dist), gloo on CPU.
+
+The product schedule runs unchanged; kernels come from the CPU oracle (tests/dist_oracle_backend.py),
+so the distributed factorization must be BITWISE equal to the single-process reference result
+(the per-element operation order does not depend on the column distribution).
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, b, lookahead, seed, out_dir, singular):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from dist_oracle_backend import OracleKernels
+    from paper_1804_07017_b200 import dist as pd
+
+    a = np.random.default_rng(seed).uniform(-1.0, 1.0, (n, n))
+    if singular:
+        a[:, 5] = 0.0
+    loc = pd.scatter_columns(torch.from_numpy(a), b, world, rank)
+    piv, info = pd.getrf_block_cyclic(loc, n, b, lookahead, OracleKernels())
+    lu = pd.allgather_columns(loc, n, b)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "lu.npy"), lu.numpy())
+        np.save(os.path.join(out_dir, "piv.npy"), piv.numpy())
+        np.save(os.path.join(out_dir, "info.npy"), np.array([info]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(tmp_path, world, n, b, lookahead, seed=0, singular=False):
+    mp.spawn(_worker, args=(world, _free_port(), n, b, lookahead, seed, str(tmp_path), singular), nprocs=world,
+             join=True)
+    return (np.load(tmp_path / "lu.npy"), np.load(tmp_path / "piv.npy"), int(np.load(tmp_path / "info.npy")[0]))
+
+
+@pytest.mark.parametrize("world,n,b,lookahead", [(2, 96, 16, 1), (2, 100, 16, 0), (3, 101, 8, 1), (2, 64, 64, 1),
+                                                 (3, 40, 16, 1)])
+def test_block_cyclic_matches_reference_bitwise(tmp_path, world, n, b, lookahead):
+    import oracle
+
+    a = np.random.default_rng(0).uniform(-1.0, 1.0, (n, n))
+    ref, rpiv, rinfo = oracle.getrf(a, b)
+    lu, piv, info = _run(tmp_path, world, n, b, lookahead)
+    assert info == rinfo == 0
+    assert np.array_equal(piv, rpiv)
+    assert lu.tobytes() == ref.tobytes()
+
+
+def test_block_cyclic_singular_info(tmp_path):
+    import oracle
+
+    a = np.random.default_rng(0).uniform(-1.0, 1.0, (48, 48))
+    a[:, 5] = 0.0
+    ref, rpiv, rinfo = oracle.getrf(a, 16)
+    lu, piv, info = _run(tmp_path, 2, 48, 16, 1, singular=True)
+    assert info == rinfo == 6
+    assert np.array_equal(piv, rpiv)
+    assert lu.tobytes() == ref.tobytes()
+
+
+def test_block_cyclic_bookkeeping():
+    from paper_1804_07017_b200 import dist as pd
+
+    n, b = 1000, 64
+    for P in (1, 2, 3, 8):
+        assert sum(pd.local_cols(n, b, P, r) for r in range(P)) == n
+        a = torch.arange(n * n, dtype=torch.float64).view(n, n)
+        parts = [pd.scatter_columns(a, b, P, r) for r in range(P)]
+        assert torch.equal(pd.gather_columns(parts, n, b), a)
+        for r in range(P):
+            for k in range(pd.num_blocks(n, b)):
+                if k % P == r:
+                    lc = pd.local_col_of_block(k, b, P)
+                    assert torch.equal(parts[r][:, lc: lc + min(b, n - k * b)], a[:, k * b: min(n, (k + 1) * b)])
+                    assert pd.local_cols_before(k, n, b, P, r) == lc

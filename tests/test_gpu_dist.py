@@ -1,0 +1,78 @@
+"""The block-cyclic driver with the product CUDA backend (GPU box, one GPU).
+
+World size 1 runs in-process (NCCL); world size 2 runs two processes on cuda:0 with gloo carrying
+the panel broadcasts (the ranks' kernels never wait on each other -- only the host collective
+synchronises them).  Exact mode must be bitwise equal to the oracle, DMMA mode must match pivots
+and backward error.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, backend, n, b, lookahead, exact, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+    from paper_1804_07017_b200 import dist as pd
+
+    dev = torch.device("cuda:0")
+    a = np.random.default_rng(4).uniform(-1.0, 1.0, (n, n))
+    loc = pd.scatter_columns(torch.from_numpy(a), b, world, rank).to(dev)
+    piv, info = pd.getrf_block_cyclic(loc, n, b, lookahead, pd.CudaKernels(dev, exact=exact))
+    lu = pd.allgather_columns(loc, n, b)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "lu.npy"), lu.cpu().numpy())
+        np.save(os.path.join(out_dir, "piv.npy"), piv.cpu().numpy())
+        np.save(os.path.join(out_dir, "info.npy"), np.array([info]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(tmp_path, world, backend, n, b, lookahead, exact):
+    mp.spawn(_worker, args=(world, _free_port(), backend, n, b, lookahead, exact, str(tmp_path)), nprocs=world,
+             join=True)
+    return np.load(tmp_path / "lu.npy"), np.load(tmp_path / "piv.npy"), int(np.load(tmp_path / "info.npy")[0])
+
+
+@pytest.mark.parametrize("world,backend", [(1, "nccl"), (2, "gloo")])
+@pytest.mark.parametrize("n,b,lookahead", [(700, 64, 1), (513, 128, 0), (2048, 256, 1)])
+def test_dist_cuda_exact_bitwise(cuda, tmp_path, world, backend, n, b, lookahead):
+    a = np.random.default_rng(4).uniform(-1.0, 1.0, (n, n))
+    ref, rpiv, _ = oracle.getrf(a, b)
+    lu, piv, info = _run(tmp_path, world, backend, n, b, lookahead, True)
+    assert info == 0
+    assert np.array_equal(piv, rpiv)
+    assert lu.tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("world,backend", [(1, "nccl"), (2, "gloo")])
+def test_dist_cuda_dmma(cuda, tmp_path, world, backend):
+    n, b = 1500, 128
+    a = np.random.default_rng(4).uniform(-1.0, 1.0, (n, n))
+    ref, rpiv, _ = oracle.getrf(a, b)
+    lu, piv, info = _run(tmp_path, world, backend, n, b, 1, False)
+    assert np.array_equal(piv, rpiv)
+    assert oracle.lu_residual(a, lu, piv) <= 10
+    assert oracle.max_rel_diff(lu, ref, a) <= 1e-8
