@@ -1,0 +1,68 @@
+"""The C-ABI boundary on CPU: the library loads, exports every symbol include/pflu.h declares, and
+validates arguments (LAPACK-style negative codes) before touching the device."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+def _header_symbols():
+    txt = open(os.path.join(ROOT, "include", "pflu.h")).read()
+    return sorted(set(re.findall(r"\b(pflu_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_1804_07017_b200 import _lib
+
+    L = _lib.load()
+    syms = _header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(L, s), f"{s} declared in pflu.h but not exported"
+    assert sorted(_lib.EXPORTS) == syms
+
+
+def test_header_is_plain_c():
+    txt = open(os.path.join(ROOT, "include", "pflu.h")).read()
+    assert 'extern "C"' in txt and "torch" not in txt.lower().replace("no torch types", "")
+    for s in _header_symbols():
+        assert s in txt
+
+
+def test_built_for_sm100a():
+    out = os.popen(f"cuobjdump --list-elf {ROOT}/paper_1804_07017_b200/libpflu.so 2>&1").read()
+    assert "sm_100a" in out
+
+
+def test_argument_validation_codes_without_gpu():
+    from paper_1804_07017_b200 import _lib
+
+    L = _lib.load()
+    a = np.zeros((4, 8))
+    piv = np.zeros(8, dtype=np.int64)
+    info = ctypes.c_int64(0)
+    # m < n -> -3 (n invalid), lda < n -> -4, b < 1 -> -5, lookahead 2 -> -6, null ipiv -> -7
+    assert L.pflu_getrf(a.ctypes.data, 4, 8, 8, 2, 1, piv.ctypes.data, ctypes.byref(info), None) == -3
+    b = np.zeros((8, 8))
+    assert L.pflu_getrf(b.ctypes.data, 8, 8, 4, 2, 1, piv.ctypes.data, ctypes.byref(info), None) == -4
+    assert L.pflu_getrf(b.ctypes.data, 8, 8, 8, 0, 1, piv.ctypes.data, ctypes.byref(info), None) == -5
+    assert L.pflu_getrf(b.ctypes.data, 8, 8, 8, 2, 2, piv.ctypes.data, ctypes.byref(info), None) == -6
+    assert L.pflu_getrf(b.ctypes.data, 8, 8, 8, 2, 1, None, ctypes.byref(info), None) == -7
+    assert L.pflu_getrf(None, 8, 8, 8, 2, 1, piv.ctypes.data, ctypes.byref(info), None) == -1
+    assert L.pflu_gemm_update(None, 1, None, 1, None, 1, 1, 1, 1, 0, None) == -1
+    assert L.pflu_laswp(b.ctypes.data, 8, 5, 3, piv.ctypes.data, 0, 1, None) == -4
+
+
+def test_no_device_fails_loudly():
+    """Without a B200 the product path raises -- there is no CPU fallback."""
+    import torch
+    from paper_1804_07017_b200 import lu_factor
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    with pytest.raises(RuntimeError):
+        lu_factor(np.eye(8), b=4)

@@ -1,0 +1,93 @@
+"""Pin the CPU oracle to vectors produced by the reference itself (tests/golden/, made by
+tests/golden/make_golden.py from the unmodified panelforge package).  CPU only."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN, bitwise_equal
+
+CONFIGS = json.load(open(os.path.join(GOLDEN, "configs.json")))
+PIVOTS = np.load(os.path.join(GOLDEN, "configs_pivots.npz"))
+SMALL = ["swap2", "diag4", "zero3", "grid16", "grid32", "grid80", "grid97", "u300", "n200", "tall57x32",
+         "sing48", "la6b", "la4b7", "n257b64", "tie4"]
+
+
+@pytest.mark.parametrize("tag", SMALL)
+def test_oracle_blocked_matches_reference(golden_small, tag):
+    a0 = golden_small[f"{tag}__a"]
+    b, info, _ = golden_small[f"{tag}__meta"]
+    lu, piv, inf = oracle.getrf(a0, int(b))
+    assert inf == info
+    assert np.array_equal(piv, golden_small[f"{tag}__piv"])
+    assert bitwise_equal(lu, golden_small[f"{tag}__f"])
+
+
+@pytest.mark.parametrize("tag", ["u300", "grid97", "tall57x32", "sing48", "tie4"])
+def test_oracle_unblocked_equals_blocked(golden_small, tag):
+    """Op-order invariance: unblocked right-looking LU == blocked reference."""
+    a0 = golden_small[f"{tag}__a"]
+    lu, piv, info = oracle.lu_unb(a0.copy())
+    assert bitwise_equal(lu, golden_small[f"{tag}__f"])
+    assert np.array_equal(piv, golden_small[f"{tag}__piv"])
+
+
+def test_oracle_kernels_match_reference(golden_small):
+    x = oracle.laswp(golden_small["laswp__a"].copy(), golden_small["laswp__piv1"] - 1, 0,
+                     len(golden_small["laswp__piv1"]))
+    assert bitwise_equal(x, golden_small["laswp__out"])
+    y = oracle.trsm_llnu(golden_small["trsm__l"], golden_small["trsm__x"].copy())
+    assert bitwise_equal(y, golden_small["trsm__out"])
+    c = oracle.gemm_sub(golden_small["gemm__c"].copy(), golden_small["gemm__a"], golden_small["gemm__b"])
+    assert bitwise_equal(c, golden_small["gemm__out"])
+
+
+def test_hand_cases():
+    # reference test_factor.py:24-45: [[0,1],[1,0]] -> pivots (1-based) [2, 2], factors = I
+    lu, piv, info = oracle.getrf(np.array([[0.0, 1.0], [1.0, 0.0]]), 16)
+    assert (piv + 1).tolist() == [2, 2] and np.array_equal(lu, np.eye(2)) and info == 0
+    d = np.diag([5.0, 4.0, 3.0, 2.0])
+    lu, piv, info = oracle.getrf(d, 2)
+    assert piv.tolist() == [0, 1, 2, 3] and np.array_equal(lu, d)
+
+
+def test_ties_break_to_smallest_row():
+    a = np.array([[1.0, 2.0], [-1.0, 3.0], [1.0, 5.0]])
+    lu, piv, info = oracle.lu_unb(a.copy())
+    assert piv[0] == 0            # |1| == |-1| == |1|: strict '>' keeps the first (smallest row)
+
+
+def test_c1_full_sha_matches_reference():
+    a = np.random.default_rng(0).uniform(-1.0, 1.0, size=(2048, 2048))
+    lu, piv, info = oracle.getrf(a, 128)
+    assert hashlib.sha256(lu.tobytes()).hexdigest() == CONFIGS["c1"]["sha256_factors"]
+    assert np.array_equal(piv, PIVOTS["c1"])
+
+
+def test_prefix_oracle_rows_are_final():
+    """lu_prefix(s) reproduces rows [0, s) and piv[:s] of the full factorization (used at C4/C5)."""
+    a = np.random.default_rng(0).uniform(-1.0, 1.0, size=(2048, 2048))
+    pre, ppiv, _ = oracle.lu_prefix(a, 256)
+    assert hashlib.sha256(np.ascontiguousarray(pre[:256]).tobytes()).hexdigest() == CONFIGS["c1"]["sha256_rows_0_256"]
+    assert np.array_equal(ppiv, PIVOTS["c1"][:256])
+
+
+def test_residual_definition():
+    a = np.random.default_rng(19).random((200, 200))
+    lu, piv, _ = oracle.getrf(a, 16)
+    r = oracle.lu_residual(a, lu, piv)
+    assert 0 < r <= 50                                         # reference test_factor.py:391-398
+    # row blocking changes the BLAS rounding of L @ U at the u-level the residual measures
+    assert oracle.lu_residual(a, lu, piv, block=37) == pytest.approx(r, rel=0.2)
+    assert np.max(np.abs(np.tril(lu, -1))) <= 1.0 + 4 * oracle.UNIT_ROUNDOFF
+
+
+def test_golden_configs_present():
+    for name in ("c1", "c2", "c2s", "c3"):
+        assert name in CONFIGS and name in PIVOTS.files
+    assert CONFIGS["c2"]["first_pivots"][:4] == [4465, 1370, 4721, 3630]    # SURVEY §8(d) anchor
+    assert CONFIGS["c3"]["first_pivots"][:4] == [4176, 8860, 16281, 7873]
+    assert np.array_equal(PIVOTS["c2s"], np.arange(8192))
