@@ -242,7 +242,7 @@ def run_single(args) -> None:
                     g_cnt += 1
     peak, peak_src = fp64_peak()
     achieved = g_flops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else None
-    traffic, traffic_src = load_traffic()
+    traffic, traffic_src = load_traffic()  # DRAM bytes of ONE launch at the step-0 shape (ncu --set full)
     pf_ms = sum((ev.end - ev.start) * 1e3 for ev in traces[-1] if ev.label == "PF")
     gemm_share = (g_ms / args.steps) / ms_step if ms_step else None
 
@@ -274,10 +274,11 @@ def run_single(args) -> None:
                    "n": n, "b": b, "lookahead": la, "parallelism": "single GPU",
                    "l2": "inputs (8.6 GB) larger than L2; pristine matrix restored by a D2D copy inside each step",
                    "fp64_peak_frac": value / 1e3 / peak},
-        "roofline": {"bound": "tensor", "kernel": "gemm_dmma_kernel (trailing update A22 -= L21*U12)",
+        "roofline": {"bound": "tensor", "kernel": "gemm_dmma_t<128x64x16, 4 stages> (trailing update A22 -= L21*U12)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": peak_src, "traffic_source": traffic_src,
+                     "traffic_shape": "one launch at the step-0 shape 32512x32512x256 (algorithmic C r+w 16.9 GB)",
                      "launches_timed": g_cnt, "gemm_share_of_step": gemm_share,
                      "algorithmic": "2*(n-(k+1)b)*(n-(k+2)b)*b flop per TU_R launch of step k"},
         "panel_ms_per_step": pf_ms,
