@@ -27,7 +27,8 @@ namespace pflu {
 constexpr int PF_THREADS = 256;
 constexpr int PF_UCH = 64;  // right-columns chunk of the block update
 constexpr size_t PF_MBOX_OFFSET = 2 * 257 * 80 + 512;  // words; after slots + sync words
-constexpr size_t PF_LL_WORDS = PF_MBOX_OFFSET + 2 * 256 * 256 * 4;
+constexpr size_t PF_SBOX_OFFSET = PF_MBOX_OFFSET + 2 * 256 * 256 * 4;  // grid-sync mailboxes
+constexpr size_t PF_LL_WORDS = PF_SBOX_OFFSET + 256 * 256 * 2;
 
 struct PanelArgs {
   double* a;
@@ -93,20 +94,28 @@ __device__ __forceinline__ bool ll_try2(const unsigned long long* p, unsigned fl
 }
 __device__ __forceinline__ double ll_get2_d(const unsigned long long* p, unsigned flag) {
   unsigned a, b;
-  while (!ll_try2(p, flag, a, b)) {
-  }
+  // one-shot reads of data that is normally already visible; on a miss back off instead of
+  // spinning, since many SMs spinning on a line delay the writer's store
+  while (!ll_try2(p, flag, a, b)) __nanosleep(128);
   return __longlong_as_double(((long long)b << 32) | a);
 }
 
-// grid-wide sync through LL flags (S <= PF_THREADS); fences give release/acquire on data
-__device__ __forceinline__ void ll_grid_sync(unsigned long long* sync_words, int S, int q, unsigned flag) {
+// Grid-wide sync through per-reader mailboxes: CTA q stores its arrival flag into every reader's
+// line (sbox[reader][writer], 16 bytes apart) and polls only its own S entries, so no L2 line is
+// spun on by more than one SM (many SMs polling one line delay the writer's store by microseconds).
+// Fences give release/acquire semantics for the data written before the sync.
+__device__ __forceinline__ void ll_grid_sync(unsigned long long* sbox, int S, int q, unsigned flag) {
   __syncthreads();
   if (S > 1) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
       __threadfence();
-      ll_put(sync_words + q, 0u, flag);
+      for (int t = threadIdx.x; t < S; t += 32) ll_put2(sbox + ((size_t)t * 256 + q) * 2, 0u, 0u, flag);
     }
-    if ((int)threadIdx.x < S) ll_get(sync_words + threadIdx.x, flag);
+    if ((int)threadIdx.x < S) {
+      unsigned a, b;
+      while (!ll_try2(sbox + ((size_t)q * 256 + threadIdx.x) * 2, flag, a, b)) {
+      }
+    }
     __threadfence();
   }
   __syncthreads();
@@ -118,7 +127,7 @@ struct PanelSmem {
   static size_t bytes(int64_t R, int w) {
     // tile R x LD, U buffer W x (w - W) (>= W x 8), L_JJ W x W, u / dg W each, plan 4W ints
     const int64_t nright = w > W ? w - W : 8;
-    return (size_t)(R * LD + (int64_t)W * nright + W * W + 2 * W) * 8 + 4 * W * 8 + 256;
+    return (size_t)(R * LD + (int64_t)W * nright + W * W + 4 * W) * 8 + 4 * W * 8 + 256;
   }
 };
 
@@ -137,32 +146,27 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   double* tile = pf_smem;                                 // [R][LD]
   double* ubuf = tile + p.R * LD;                         // [W][nright_max]  U_J (solved)
   double* ljj = ubuf + (int64_t)W * nright_max;           // [W][W]
-  double* u = ljj + W * W;                                // [W]
-  double* dg = u + W;                                     // [W]
-  long long* plan_row = reinterpret_cast<long long*>(dg + W);  // [2W] slot -> row
-  int* plan_src = reinterpret_cast<int*>(plan_row + 2 * W);    // [2W] slot -> source slot
+  double* u = ljj + W * W;                                // [2][W] pivot row (double-buffered)
+  double* dg = u + 2 * W;                                 // [2][W] old diagonal row
+  long long* plan_row = reinterpret_cast<long long*>(dg + 2 * W);  // [2W] slot -> destination row
+  long long* plan_src_row = plan_row + 2 * W;                       // [2W] slot -> source row
   __shared__ double red_key[PF_THREADS / 32];
   __shared__ long long red_row[PF_THREADS / 32];
   __shared__ int red_q[PF_THREADS / 32];
   __shared__ double red2_key[PF_THREADS / 32];
   __shared__ long long red2_row[PF_THREADS / 32];
-  __shared__ double s_key;
-  __shared__ long long s_row;
-  __shared__ int s_win;
   __shared__ int s_nslots;
   __shared__ long long blk_piv[32];  // pivots of the current block (every CTA knows them)
 
   const unsigned epoch = *(volatile unsigned*)p.epoch;
   // LL layout: [2 parities][S + 1 records][16 + 2W words], then S sync words
   const int rec = 16 + 2 * W;  // [key line: key, row (16 words = 128 B)][data: 2W words]; 128-B aligned
-  const int npar = 2;
-  unsigned long long* sync_words = p.ll + (size_t)npar * (S + 1) * rec;
+  unsigned long long* sync_words = p.ll + PF_SBOX_OFFSET;  // [reader 256][writer 256][2 words]
   unsigned long long* mbox = p.ll + PF_MBOX_OFFSET;  // [2][reader 256][writer 256][4 words]
   const bool exact = p.exact != 0;
   const bool prof_on = p.prof != nullptr && tid == 0;
   long long prof_t = clock64();
   long long prof_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  long long last_gather_done = clock64();
 
   int pend_kb = 0, pend_nright = 0, pend_right0 = 0;  // U rows awaiting write-back
   int64_t pend_cJ = 0;
@@ -186,18 +190,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     __syncthreads();
     PF_PROF_MARK(0);
     // ---------------- 2. leaf: columns of the block
+    // Per column: gather the pivot keys -> read the winner row -> (pass 1) swap-in, scale, update
+    // column j+1 while tracking its pivot candidate -> publish the candidate (its row finished by
+    // warp 0; the next diagonal row by warp 1) -> (pass 2) remaining columns, overlapping the
+    // exchange.  Every row is owned by one thread, so the swap needs no barrier.
     const int kmax = (int)min((int64_t)wb, p.m - cJ);
-    for (int j = 0; j < kmax; ++j) {
-      const int64_t c = cJ + j;
-      const unsigned flag = epoch + (unsigned)(jb + j);
-      unsigned long long* slots = p.ll + (size_t)(j & (npar - 1)) * (S + 1) * rec;
-      // A: local candidate over own rows >= c
-      double bk = -3.0;
-      long long br = LLONG_MAX;
-      for (int64_t r = max((int64_t)0, c - rbeg) + tid; r < nrows; r += PF_THREADS) {
-        const double k = pivot_key(tile[r * LD + j], rbeg + r == c);
-        if (key_better(k, rbeg + r, bk, br)) { bk = k; br = rbeg + r; }
-      }
+    auto cta_best = [&](double& bk, long long& br) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
@@ -206,156 +204,204 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       }
       if (lane == 0) { red_key[warp] = bk; red_row[warp] = br; }
       __syncthreads();
-      PF_PROF_MARK(1);
-      if (warp == 0) {
-        bk = lane < PF_THREADS / 32 ? red_key[lane] : -3.0;
-        br = lane < PF_THREADS / 32 ? red_row[lane] : LLONG_MAX;
+      bk = red_key[0];
+      br = red_row[0];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-          const long long orr = __shfl_xor_sync(0xffffffffu, br, o);
-          if (key_better(ok, orr, bk, br)) { bk = ok; br = orr; }
-        }
-        if (S > 1) {
-          // B: publish candidate (key, row, row data) -- data before key is irrelevant: every
-          // word carries its own flag
-          unsigned long long* my = slots + (size_t)q * rec;
-          if (bk > -2.0) {
-            const double* trow = tile + (br - rbeg) * LD;
-            for (int cc = lane; cc < wb; cc += 32) ll_put2_d(my + 16 + 2 * cc, trow[cc], flag);
-          }
-          // keys are pushed into every reader's mailbox, so each polled line has a single reader SM
-          // (many SMs spinning on one line delay the writer's store by microseconds)
-          {
-            const long long kb_ = __double_as_longlong(bk);
-            const unsigned rowoff = (unsigned)(bk > -2.0 ? br - p.r0 : 0);
-            unsigned long long* mb = mbox + (size_t)(j & 1) * 256 * 256 * 4 + (size_t)q * 4;
-            for (int t = lane; t < S; t += 32) {
-              unsigned long long* e = mb + (size_t)t * 256 * 4;
-              ll_put2(e, (unsigned)kb_, (unsigned)(kb_ >> 32), flag);
-              ll_put2(e + 2, rowoff, 0u, flag);
-            }
-          }
-        }
-        if (lane == 0) { s_key = bk; s_row = br; s_win = q; }
-      } else if (warp == 1 && S > 1 && c >= rbeg && c < rend) {
-        unsigned long long* dslot = slots + (size_t)S * rec;
-        const double* trow = tile + (c - rbeg) * LD;
-        for (int cc = lane; cc < wb; cc += 32) ll_put2_d(dslot + 16 + 2 * cc, trow[cc], flag);
+      for (int w2 = 1; w2 < PF_THREADS / 32; ++w2)
+        if (key_better(red_key[w2], red_row[w2], bk, br)) { bk = red_key[w2]; br = red_row[w2]; }
+    };
+    // publish candidate (key, row, data of tile row br) for column jn; warp 0 only
+    auto publish_cand = [&](int jn, double bk, long long br) {
+      const unsigned fl = epoch + (unsigned)(jb + jn);
+      unsigned long long* sl = p.ll + (size_t)(jn & 1) * (S + 1) * rec;
+      unsigned long long* my = sl + (size_t)q * rec;
+      if (bk > -2.0) {
+        const double* trow = tile + (br - rbeg) * LD;
+        for (int cc = lane; cc < wb; cc += 32) ll_put2_d(my + 16 + 2 * cc, trow[cc], fl);
       }
-      if (S == 1) __syncthreads();  // S > 1: the gather below needs no barrier (own record is polled too)
-      const long long gc0 = clock64();
-      if (prof_on && q < 32) p.prof[8192 + q * 256 + jb + j] = gc0 - last_gather_done;
-      PF_PROF_MARK(2);
-      if (prof_on && jb == 0 && j >= 4 && j < 7) {
-        unsigned long long gt;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.prof[q * 16 + 10 + 2 * (j - 4)] = gt;
+      const long long kb_ = __double_as_longlong(bk);
+      const unsigned rowoff = (unsigned)(bk > -2.0 ? br - p.r0 : 0);
+      unsigned long long* mb = mbox + (size_t)(jn & 1) * 256 * 256 * 4 + (size_t)q * 4;
+      for (int t = lane; t < S; t += 32) {
+        unsigned long long* e = mb + (size_t)t * 256 * 4;
+        ll_put2(e, (unsigned)kb_, (unsigned)(kb_ >> 32), fl);
+        ll_put2(e + 2, rowoff, 0u, fl);
       }
-      // C: gather all candidates
+    };
+    auto publish_diag = [&](int jn, long long row) {  // the owner of the next diagonal row, one warp
+      const unsigned fl = epoch + (unsigned)(jb + jn);
+      unsigned long long* dsl = p.ll + (size_t)(jn & 1) * (S + 1) * rec + (size_t)S * rec;
+      const double* trow = tile + (row - rbeg) * LD;
+      for (int cc = lane; cc < wb; cc += 32) ll_put2_d(dsl + 16 + 2 * cc, trow[cc], fl);
+    };
+    double ck = -3.0;
+    long long cr = LLONG_MAX;
+    if (kmax > 0) {  // candidate for the block's first column (the tile is current)
+      for (int64_t r = max((int64_t)0, cJ - rbeg) + tid; r < nrows; r += PF_THREADS) {
+        const double k = pivot_key(tile[r * LD], rbeg + r == cJ);
+        if (key_better(k, rbeg + r, ck, cr)) { ck = k; cr = rbeg + r; }
+      }
+      cta_best(ck, cr);
       if (S > 1) {
-        bk = -3.0;
-        br = LLONG_MAX;
-        int wq = -1;
+        if (warp == 0) publish_cand(0, ck, cr);
+        else if (warp == 1 && cJ >= rbeg && cJ < rend) publish_diag(0, cJ);
+      }
+    }
+    for (int j = 0; j < kmax; ++j) {
+      const int64_t c = cJ + j;
+      const unsigned flag = epoch + (unsigned)(jb + j);
+      unsigned long long* slots = p.ll + (size_t)(j & 1) * (S + 1) * rec;
+      double* ucur = u + (j & 1) * W;
+      double* dcur = dg + (j & 1) * W;
+      const bool nxt = j + 1 < kmax;
+      const long long last_gather_start = clock64();
+      // C: the winner of column j
+      double wkey;
+      long long prow;
+      int wq;
+      if (S > 1) {
+        double bk = -3.0;
+        long long br = LLONG_MAX;
+        int bq = -1;
         if (tid < S) {
           const unsigned long long* sl = mbox + (size_t)(j & 1) * 256 * 256 * 4 + (size_t)q * 256 * 4 + (size_t)tid * 4;
           unsigned k0, k1, r0_, r1_;
           bool ok0 = false, ok1 = false;
+          int spins = 0;
           while (!(ok0 && ok1)) {  // both 16-byte loads in flight together
             if (!ok0) ok0 = ll_try2(sl, flag, k0, k1);
             if (!ok1) ok1 = ll_try2(sl + 2, flag, r0_, r1_);
+            if (!(ok0 && ok1) && ++spins > 4) __nanosleep(64);
           }
           const double k = __longlong_as_double(((long long)k1 << 32) | k0);
-          const long long rr = (long long)r0_ + p.r0;
-          if (k > -2.0) { bk = k; br = rr; wq = tid; }
+          if (k > -2.0) { bk = k; br = (long long)r0_ + p.r0; bq = tid; }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
           const long long orr = __shfl_xor_sync(0xffffffffu, br, o);
-          const int oq = __shfl_xor_sync(0xffffffffu, wq, o);
-          if (key_better(ok, orr, bk, br)) { bk = ok; br = orr; wq = oq; }
+          const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+          if (key_better(ok, orr, bk, br)) { bk = ok; br = orr; bq = oq; }
         }
-        if (lane == 0) { red2_key[warp] = bk; red2_row[warp] = br; red_q[warp] = wq; }
+        if (lane == 0) { red2_key[warp] = bk; red2_row[warp] = br; red_q[warp] = bq; }
         __syncthreads();
-        if (warp == 0) {
-          bk = lane < PF_THREADS / 32 ? red2_key[lane] : -3.0;
-          br = lane < PF_THREADS / 32 ? red2_row[lane] : LLONG_MAX;
-          wq = lane < PF_THREADS / 32 ? red_q[lane] : -1;
+        wkey = red2_key[0];
+        prow = red2_row[0];
+        wq = red_q[0];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-            const long long orr = __shfl_xor_sync(0xffffffffu, br, o);
-            const int oq = __shfl_xor_sync(0xffffffffu, wq, o);
-            if (key_better(ok, orr, bk, br)) { bk = ok; br = orr; wq = oq; }
-          }
-          if (lane == 0) { s_key = bk; s_row = br; s_win = wq; }
-        }
+        for (int w2 = 1; w2 < PF_THREADS / 32; ++w2)
+          if (key_better(red2_key[w2], red2_row[w2], wkey, prow)) { wkey = red2_key[w2]; prow = red2_row[w2]; wq = red_q[w2]; }
+      } else {
+        wkey = ck;
+        prow = cr;
+        wq = q;
         __syncthreads();
       }
+      if (prof_on && q == 0) p.prof[4096 + jb + j] = clock64() - last_gather_start;
       PF_PROF_MARK(3);
-      if (prof_on && q == 0) p.prof[4096 + jb + j] = clock64() - gc0;
-      if (prof_on && q < 32) p.prof[16384 + q * 256 + jb + j] = clock64() - gc0;
-      last_gather_done = clock64();
-      if (prof_on && jb == 0 && j >= 4 && j < 7) {
-        unsigned long long gt;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.prof[q * 16 + 11 + 2 * (j - 4)] = gt;
+      if (tid == 0) blk_piv[j] = (wkey > 0.0) ? prow : c;
+      if (q == 0 && tid == 0) {
+        p.piv[c] = (wkey > 0.0) ? prow : c;
+        if (!(wkey > 0.0)) atomicMin(p.info, (unsigned long long)(c + 1));
       }
-      const double wkey = s_key;
-      const long long prow = s_row;
       if (!(wkey > 0.0)) {
-        // exactly-zero pivot: info = c + 1, column left untouched (_jit.py:171-174)
-        if (tid == 0) blk_piv[j] = c;
-        if (q == 0 && tid == 0) {
-          p.piv[c] = c;
-          atomicMin(p.info, (unsigned long long)(c + 1));
-        }
-        continue;  // s_* are rewritten only after the next __syncthreads
-      }
-      // D: winner row (and the old diagonal row for the owner of the pivot row)
-      if (S > 1) {
-        if (warp == 0) {
-          const unsigned long long* wsl = slots + (size_t)s_win * rec;
-          for (int cc = lane; cc < wb; cc += 32) u[cc] = ll_get2_d(wsl + 16 + 2 * cc, flag);
-        } else if (warp == 1 && prow != c && prow >= rbeg && prow < rend) {
-          if (c >= rbeg && c < rend) {
-            for (int cc = lane; cc < wb; cc += 32) dg[cc] = tile[(c - rbeg) * LD + cc];
-          } else {
-            const unsigned long long* dsl = slots + (size_t)S * rec;
-            for (int cc = lane; cc < wb; cc += 32) dg[cc] = ll_get2_d(dsl + 16 + 2 * cc, flag);
+        // exactly-zero pivot: column left untouched (_jit.py:171-174); next candidate from the tile
+        ck = -3.0;
+        cr = LLONG_MAX;
+        if (nxt) {
+          for (int64_t r = max((int64_t)0, c + 1 - rbeg) + tid; r < nrows; r += PF_THREADS) {
+            const double k = pivot_key(tile[r * LD + j + 1], rbeg + r == c + 1);
+            if (key_better(k, rbeg + r, ck, cr)) { ck = k; cr = rbeg + r; }
+          }
+          cta_best(ck, cr);
+          if (S > 1) {
+            if (warp == 0) publish_cand(j + 1, ck, cr);
+            else if (warp == 1 && c + 1 >= rbeg && c + 1 < rend) publish_diag(j + 1, c + 1);
           }
         }
-      } else {
-        if (warp == 0)
-          for (int cc = lane; cc < wb; cc += 32) u[cc] = tile[(prow - rbeg) * LD + cc];
-        else if (warp == 1 && prow != c)
-          for (int cc = lane; cc < wb; cc += 32) dg[cc] = tile[(c - rbeg) * LD + cc];
+        continue;
       }
-      if (tid == 0) blk_piv[j] = prow;
-      if (q == 0 && tid == 0) p.piv[c] = prow;
+      // D: winner row -> ucur; old diagonal row -> dcur (only the owner of the pivot row needs it)
+      const bool own_c = c >= rbeg && c < rend;
+      const bool own_p = prow >= rbeg && prow < rend;
+      if (warp == 0) {
+        if (S > 1 && !own_p) {
+          const unsigned long long* wsl = slots + (size_t)wq * rec;
+          for (int cc = lane; cc < wb; cc += 32) ucur[cc] = ll_get2_d(wsl + 16 + 2 * cc, flag);
+        } else {
+          for (int cc = lane; cc < wb; cc += 32) ucur[cc] = tile[(prow - rbeg) * LD + cc];
+        }
+      } else if (warp == 1 && prow != c && own_p) {
+        if (own_c) {
+          for (int cc = lane; cc < wb; cc += 32) dcur[cc] = tile[(c - rbeg) * LD + cc];
+        } else {
+          const unsigned long long* dsl = slots + (size_t)S * rec;
+          for (int cc = lane; cc < wb; cc += 32) dcur[cc] = ll_get2_d(dsl + 16 + 2 * cc, flag);
+        }
+      }
       __syncthreads();
       PF_PROF_MARK(4);
-      // E: swap inside the block, scale by division, rank-1 update (mul then sub)
-      if (prow != c) {
-        if (c >= rbeg && c < rend)
-          for (int cc = tid; cc < wb; cc += PF_THREADS) tile[(c - rbeg) * LD + cc] = u[cc];
-        if (prow >= rbeg && prow < rend)
-          for (int cc = tid; cc < wb; cc += PF_THREADS) tile[(prow - rbeg) * LD + cc] = dg[cc];
-        __syncthreads();
-      }
-      {
-        const double pivot = u[j];
-        for (int64_t r = max((int64_t)0, c + 1 - rbeg) + tid; r < nrows; r += PF_THREADS) {
-          double* tr = tile + r * LD;
-          const double l = __ddiv_rn(tr[j], pivot);
-          tr[j] = l;
-          for (int cc = j + 1; cc < wb; ++cc) tr[cc] = sub_mul_exact(tr[cc], l, u[cc]);
+      if (own_c && prow != c)
+        for (int cc = tid; cc < wb; cc += PF_THREADS) tile[(c - rbeg) * LD + cc] = ucur[cc];
+      // pass 1: swap-in, scale by division (_jit.py:180-182), column j+1, next candidate
+      const double pivot = ucur[j];
+      const double uj1 = (j + 1 < wb) ? ucur[j + 1] : 0.0;
+      ck = -3.0;
+      cr = LLONG_MAX;
+      for (int64_t r = max((int64_t)0, c + 1 - rbeg) + tid; r < nrows; r += PF_THREADS) {
+        double* tr = tile + r * LD;
+        if (rbeg + r == prow)
+          for (int cc = 0; cc < wb; ++cc) tr[cc] = dcur[cc];
+        const double l = __ddiv_rn(tr[j], pivot);
+        tr[j] = l;
+        if (j + 1 < wb) {
+          const double x = sub_mul_exact(tr[j + 1], l, uj1);
+          tr[j + 1] = x;
+          if (nxt) {
+            const double k = pivot_key(x, rbeg + r == c + 1);
+            if (key_better(k, rbeg + r, ck, cr)) { ck = k; cr = rbeg + r; }
+          }
         }
       }
-      __syncthreads();
+      if (nxt) cta_best(ck, cr);
+      PF_PROF_MARK(1);
+      // publish the next column's candidate and diagonal rows (S > 1): their remaining columns are
+      // finished here by warps 0 / 1 and skipped by pass 2
+      const bool special = S > 1 && nxt;
+      const bool cand_own = special && ck > -2.0;                 // cr is one of this CTA's rows
+      const bool diag_own = special && c + 1 >= rbeg && c + 1 < rend;
+      if (special) {
+        auto finish_row = [&](long long row) {
+          double* tr = tile + (row - rbeg) * LD;
+          const double l = tr[j];
+          for (int cc = j + 2 + lane; cc < wb; cc += 32) tr[cc] = sub_mul_exact(tr[cc], l, ucur[cc]);
+          __syncwarp();
+        };
+        if (warp == 0 && cand_own) {
+          finish_row(cr);
+          publish_cand(j + 1, ck, cr);
+          if (diag_own && cr == c + 1) publish_diag(j + 1, c + 1);
+        } else if (warp == 0) {
+          publish_cand(j + 1, ck, cr);
+        } else if (warp == 1 && diag_own && !(cand_own && cr == c + 1)) {
+          finish_row(c + 1);
+          publish_diag(j + 1, c + 1);
+        }
+      }
+      PF_PROF_MARK(2);
+      // pass 2: remaining columns (mul then sub, _jit.py:183-186)
+      if (j + 2 < wb) {
+        for (int64_t r = max((int64_t)0, c + 1 - rbeg) + tid; r < nrows; r += PF_THREADS) {
+          const long long gr = rbeg + r;
+          if ((cand_own && gr == cr) || (diag_own && gr == c + 1)) continue;
+          double* tr = tile + r * LD;
+          const double l = tr[j];
+          for (int cc = j + 2; cc < wb; ++cc) tr[cc] = sub_mul_exact(tr[cc], l, ucur[cc]);
+        }
+      }
       PF_PROF_MARK(5);
     }
+    __syncthreads();
     // ---------------- 3. write back own rows >= cJ of the block
     {
       const int r_first = (int)max((int64_t)0, cJ - rbeg);
@@ -372,25 +418,39 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     const int nother = w - wb;
     // ---------------- 4. deferred swaps of this block on the panel's other columns
     if (nother > 0 && kb > 0) {
-      if (tid == 0) {
-        // slots: 0..kb-1 = rows cJ + i; extra slots for pivot rows >= cJ + kb (first occurrence)
-        int ns = kb;
-        for (int i = 0; i < kb; ++i) plan_row[i] = cJ + i;
-        for (int i = 0; i < kb; ++i) plan_src[i] = i;
-        for (int i = 0; i < kb; ++i) {
-          const long long r = blk_piv[i];
-          int s;
-          if (r < cJ + kb) {
-            s = (int)(r - cJ);
-          } else {
-            s = -1;
-            for (int e = kb; e < ns; ++e)
-              if (plan_row[e] == r) { s = e; break; }
-            if (s < 0) { s = ns++; plan_row[s] = r; plan_src[s] = s; }
-          }
-          if (s != i) { const int t = plan_src[i]; plan_src[i] = plan_src[s]; plan_src[s] = t; }
+      if (warp == 0) {
+        // block swap plan by one warp (kb <= 32, piv[i] >= cJ + i): g(i) = data in row cJ+i before
+        // swap i, resolved by pointer jumping over pt(i) = last earlier swap targeting row cJ+i;
+        // top row i then receives g(i) (own pivot) / g(ps(i)) / original row piv[i]; an extra row
+        // receives g(last swap into it).  plan_row[s] = destination, plan_src[s] -> source row.
+        const long long ri = lane < kb ? blk_piv[lane] : -1;
+        int pt = -1, ps = -1, nx = -1;
+        for (int i2 = 0; i2 < kb; ++i2) {
+          const long long v = __shfl_sync(0xffffffffu, ri, i2);
+          if (i2 < lane && v == cJ + lane) pt = i2;
+          if (i2 < lane && v == ri) ps = i2;
+          if (i2 > lane && v == ri && nx < 0) nx = i2;
         }
-        s_nslots = ns;
+        long long gi = pt < 0 ? cJ + lane : -1;
+        for (int round = 0; round < 6; ++round) {
+          const long long gp = __shfl_sync(0xffffffffu, gi, pt < 0 ? lane : pt);
+          const int pp = __shfl_sync(0xffffffffu, pt, pt < 0 ? lane : pt);
+          if (gi < 0) {
+            if (gp >= 0) gi = gp;
+            else pt = pp;
+          }
+        }
+        const long long g_ps = __shfl_sync(0xffffffffu, gi, ps < 0 ? lane : ps);
+        long long src = ri == cJ + lane ? gi : (ps >= 0 ? g_ps : ri);
+        if (lane < kb) { plan_row[lane] = cJ + lane; plan_src_row[lane] = src; }
+        const bool extra = lane < kb && ri >= cJ + kb && nx < 0;
+        const unsigned em = __ballot_sync(0xffffffffu, extra);
+        if (extra) {
+          const int e = kb + __popc(em & ((1u << lane) - 1));
+          plan_row[e] = ri;
+          plan_src_row[e] = gi;
+        }
+        if (lane == 0) s_nslots = kb + __popc(em);
       }
       __syncthreads();
       const int ns = s_nslots;
@@ -405,7 +465,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           const int s = idx / nb_, ci = cb + idx - (idx / nb_) * nb_;
           const int oc = q + ci * S;
           const int pc = oc < jb ? oc : oc + wb;
-          gbuf[idx] = p.a[plan_row[plan_src[s]] * p.lda + p.col0 + pc];
+          gbuf[idx] = p.a[plan_src_row[s] * p.lda + p.col0 + pc];
         }
         __syncthreads();
         for (int idx = tid; idx < ns * nb_; idx += PF_THREADS) {
@@ -450,39 +510,54 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       const int nupd = (int)max((int64_t)0, rend - ub);
       const int toff = (int)(ub - rbeg);
       if (!exact) {
-        // DMMA: warp w handles 8-row groups w, w+8, ...; 64-column chunks; K = W (zero padded)
+        // DMMA: a warp tile is 4 row groups (32 rows) x 64 columns, so 64 C values per thread are in
+        // flight before the first MMA; K = W (zero padded)
+        constexpr int GR = 4;
         const int ngroups = (nupd + 7) / 8;
+        const int ntr = (ngroups + GR - 1) / GR;      // 32-row tiles
+        const int nch = (nright + PF_UCH - 1) / PF_UCH;
         const int g = lane >> 2, t = lane & 3;
-        for (int c0 = 0; c0 < nright; c0 += PF_UCH) {
-          for (int gi = warp; gi < ngroups; gi += PF_THREADS / 32) {
-            const int rl = gi * 8 + g;  // local update row
+        for (int wt = warp; wt < ntr * nch; wt += PF_THREADS / 32) {
+          const int tr_ = wt / nch, c0 = (wt - tr_ * nch) * PF_UCH;
+          double acc[GR][8][2];
+#pragma unroll
+          for (int gg = 0; gg < GR; ++gg) {
+            const int rl = (tr_ * GR + gg) * 8 + g;
             const bool rok = rl < nupd;
-            double* crow = p.a + (ub + rl) * p.lda + p.col0 + right0;
-            double acc[8][2];
+            const double* crow = p.a + (ub + rl) * p.lda + p.col0 + right0;
 #pragma unroll
             for (int nb = 0; nb < 8; ++nb) {
               const int col = c0 + nb * 8 + 2 * t;
-              acc[nb][0] = (rok && col < nright) ? crow[col] : 0.0;
-              acc[nb][1] = (rok && col + 1 < nright) ? crow[col + 1] : 0.0;
+              acc[gg][nb][0] = (rok && col < nright) ? crow[col] : 0.0;
+              acc[gg][nb][1] = (rok && col + 1 < nright) ? crow[col + 1] : 0.0;
             }
-            const double* arow = tile + (int64_t)(toff + rl) * LD;
+          }
 #pragma unroll
-            for (int k4 = 0; k4 < W; k4 += 4) {
-              const double av = rok ? arow[k4 + t] : 0.0;
+          for (int k4 = 0; k4 < W; k4 += 4) {
+            double bv[8];
 #pragma unroll
-              for (int nb = 0; nb < 8; ++nb) {
-                const int col = c0 + nb * 8 + g;
-                const double bv = (col < nright) ? -ubuf[(k4 + t) * nright + col] : 0.0;
-                dmma884(acc[nb][0], acc[nb][1], av, bv);
-              }
+            for (int nb = 0; nb < 8; ++nb) {
+              const int col = c0 + nb * 8 + g;
+              bv[nb] = (col < nright) ? -ubuf[(k4 + t) * nright + col] : 0.0;
             }
-            if (rok) {
 #pragma unroll
-              for (int nb = 0; nb < 8; ++nb) {
-                const int col = c0 + nb * 8 + 2 * t;
-                if (col < nright) crow[col] = acc[nb][0];
-                if (col + 1 < nright) crow[col + 1] = acc[nb][1];
-              }
+            for (int gg = 0; gg < GR; ++gg) {
+              const int rl = (tr_ * GR + gg) * 8 + g;
+              const double av = rl < nupd ? tile[(int64_t)(toff + rl) * LD + k4 + t] : 0.0;
+#pragma unroll
+              for (int nb = 0; nb < 8; ++nb) dmma884(acc[gg][nb][0], acc[gg][nb][1], av, bv[nb]);
+            }
+          }
+#pragma unroll
+          for (int gg = 0; gg < GR; ++gg) {
+            const int rl = (tr_ * GR + gg) * 8 + g;
+            if (rl >= nupd) continue;
+            double* crow = p.a + (ub + rl) * p.lda + p.col0 + right0;
+#pragma unroll
+            for (int nb = 0; nb < 8; ++nb) {
+              const int col = c0 + nb * 8 + 2 * t;
+              if (col < nright) crow[col] = acc[gg][nb][0];
+              if (col + 1 < nright) crow[col + 1] = acc[gg][nb][1];
             }
           }
         }

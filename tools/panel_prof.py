@@ -7,7 +7,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_1804_07017_b200 import _lib  # noqa: E402
 
-NAMES = ["load", "A:argmax", "B:publish", "C:gather", "D:winner", "E:update", "sync1", "swaps+sync2", "U-trsm", "blk-update"]
+NAMES = ["load", "pass1+reduce", "publish", "gather", "winner", "pass2", "wb+swaps", "sync", "U-trsm", "blk-update"]
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 w = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 ctas = int(sys.argv[3]) if len(sys.argv) > 3 else 0
@@ -58,11 +58,3 @@ G = prof.cpu()[4096:4096 + w].double() / 1965.0
 print("   per-column gather us (CTA 0):", " ".join(f"{x:.1f}" for x in G.tolist()[:64]))
 print(f"   gather us: mean {G.mean():.2f} median {G.median():.2f} max {G.max():.1f}")
 
-Wk = prof.cpu()[8192:8192 + 32 * 256].view(32, 256)[:min(nz, 32), :w].double() / 1965.0
-for col in range(33, 41):
-    v = Wk[:, col]
-    print(f"   col {col}: local work before publish: max {v.max():.1f} us on CTA {int(v.argmax())}, median {v.median():.1f}")
-
-Gq = prof.cpu()[16384:16384 + 32 * 256].view(32, 256)[:min(nz, 32), :w].double() / 1965.0
-for q in range(min(nz, 32)):
-    print(f"   CTA {q:2d} gather cols 32..47:", " ".join(f"{x:.1f}" for x in Gq[q, 32:48].tolist()))
