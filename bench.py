@@ -301,6 +301,7 @@ def main():
     ap.add_argument("--lookahead", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="force the block-cyclic multi-GPU path (testing at N=1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -308,7 +309,7 @@ def main():
         run_reference(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or args.dist:
         from paper_1804_07017_b200.dist import bench_dist
 
         bench_dist(args, lu_flops, METRIC, UNIT, ClockSampler, fp64_peak)

@@ -144,3 +144,24 @@ def test_c3_block_sweep(cuda, b):
     lu_x, piv_x, _ = run(a0, b, 1, exact=True)
     assert sha(lu_x) == CONFIGS["c3"]["sha256_factors"]
     assert oracle.max_rel_diff(lu, lu_x, a0) <= 1e-8
+
+
+@pytest.mark.slow
+def test_c4_prefix_and_residual(cuda):
+    """C4 (n = 32768, b = 256, look-ahead 1): too large for a full host oracle run, so the first 256
+    elimination steps are pinned by the oracle's prefix mode (rows [0, 256) and piv[:256] are final
+    after 256 steps; the prefix mode itself is pinned against the reference's C1 prefix sha in
+    test_oracle.py), the rest by the backward error of the full factorization."""
+    import oracle as orc
+
+    a0 = config_matrix("c4")
+    orc.set_threads(os.cpu_count() or 1)
+    pre, ppiv, _ = orc.lu_prefix(a0, 256)
+    lu, piv, info = run(a0, 256, 1, exact=False)
+    assert info == 0
+    assert np.array_equal(piv[:256], ppiv)
+    assert np.max(np.abs(lu[:256] - pre[:256])) / np.max(np.abs(a0)) <= 1e-10
+    assert gpu_residual(a0, lu, piv) <= 10
+    # pivots are a permutation sequence (every piv[k] >= k) and multipliers are bounded
+    assert np.all(piv >= np.arange(len(piv)))
+    assert np.max(np.abs(np.tril(lu, -1))) <= 1.0 + 4 * orc.UNIT_ROUNDOFF
