@@ -77,6 +77,7 @@ static unsigned long long* g_prof = nullptr;
 static int g_pf_cap = []() { const char* e = getenv("PFLU_PANEL_CAP"); return e ? atoi(e) : 32; }();
 static int g_gemm_variant = []() { const char* e = getenv("PFLU_GEMM_VARIANT"); return e ? atoi(e) : 0; }();
 static DevCtx* g_dc = nullptr;  // context of the current call (set by ctx_get)
+static int g_resync = []() { const char* e = getenv("PFLU_PANEL_RESYNC"); return e ? atoi(e) : 4; }();
 static int g_tur_grid = []() { const char* e = getenv("PFLU_TUR_GRID"); return e ? atoi(e) : 0; }();
 static int g_variant = []() { const char* e = getenv("PFLU_PANEL_VARIANT"); return e ? atoi(e) : 0; }();  // device buffer for panel-kernel phase clocks (tools only)
 
@@ -377,6 +378,7 @@ static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0
       p.a = a; p.lda = lda; p.m = m; p.r0 = r0; p.col0 = c0; p.w = (int)w; p.R = R;
       p.piv = piv; p.info = info; p.ll = c.ll; p.epoch = c.epoch; p.exact = opt.exact;
       p.prof = g_prof;
+      p.resync = g_resync;
       void* args[] = {&p};
       const void* fn = W == 8 ? (const void*)panel_kernel<8> : W == 16 ? (const void*)panel_kernel<16>
                                                                        : (const void*)panel_kernel<32>;

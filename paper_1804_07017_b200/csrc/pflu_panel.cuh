@@ -43,6 +43,7 @@ struct PanelArgs {
   unsigned* epoch;         // flag base, advanced by every launch
   int exact;
   unsigned long long* prof;  // optional: per-phase clock64 totals of CTA 0 (tools/ only)
+  int resync;                // re-align all CTAs every `resync` columns (0 = never)
 };
 
 #define PF_PROF_MARK(i)                                              \
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   unsigned long long* sync_words = p.ll + PF_SBOX_OFFSET;  // [reader 256][writer 256][2 words]
   unsigned long long* mbox = p.ll + PF_MBOX_OFFSET;  // [2][reader 256][writer 256][4 words]
   const bool exact = p.exact != 0;
+  const int g_resync = p.resync;
   const bool prof_on = p.prof != nullptr && tid == 0;
   long long prof_t = clock64();
   long long prof_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -400,6 +402,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         }
       }
       PF_PROF_MARK(5);
+      // periodic re-alignment: once CTAs drift apart by a column, early arrivals spin on lines the
+      // late ones still have to write and the skew sustains itself (measured ~5 us per column)
+      if (g_resync > 0 && nxt && ((j + 1) % g_resync) == 0)
+        ll_grid_sync(sync_words, S, q, epoch + (unsigned)w + 4u * (unsigned)((w + W - 1) / W) + 16u + (unsigned)(jb + j));
     }
     __syncthreads();
     // ---------------- 3. write back own rows >= cJ of the block
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   if (prof_on)
     for (int i = 0; i < 10; ++i) p.prof[q * 16 + i] += prof_acc[i];
   // advance the flag base for the next launch (all CTAs read it at their start)
-  if (q == 0 && tid == 0) atomicAdd(p.epoch, (unsigned)(w + 3 * ((w + W - 1) / W) + 16));
+  if (q == 0 && tid == 0) atomicAdd(p.epoch, (unsigned)(2 * w + 4 * ((w + W - 1) / W) + 32));
 }
 
 }  // namespace pflu
