@@ -90,6 +90,11 @@ int pflu_getrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b,
 int pflu_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w,
                int64_t* d_ipiv, int64_t* info, void* stream, const pflu_options* opt);
 
+/* Strided 2-D copy (bytes; host or device pointers, unified addressing): `height` rows of `width`
+ * bytes.  Moves a rank's block-cyclic columns between a host matrix and its device buffer. */
+int pflu_copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
+                void* stream);
+
 /* Asynchronous info handling for pflu_panel(..., info = NULL, ...): reset / read (blocking) the
  * device-side "first zero pivot" word that asynchronous panel calls accumulate into. */
 int pflu_info_reset(void* stream);

@@ -616,6 +616,20 @@ int pflu_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int6
   return finish_info(*c, st, info);
 }
 
+int pflu_copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
+                void* stream) {
+  if (!dst) return -1;
+  if (dpitch < width) return -2;
+  if (!src) return -3;
+  if (spitch < width) return -4;
+  if (width < 0) return -5;
+  if (height < 0) return -6;
+  if (width == 0 || height == 0) return PFLU_OK;
+  CK(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height, cudaMemcpyDefault,
+                       (cudaStream_t)stream));
+  return PFLU_OK;
+}
+
 int pflu_info_reset(void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   DevCtx* c = nullptr;

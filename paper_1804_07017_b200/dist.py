@@ -279,9 +279,36 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
     return piv, info
 
 
-def lu_factor_dist(a, b: int = 256, lookahead: int = 1, exact: bool = False, return_info: bool = False):
-    """``lu_factor(..., n_gpus=P)``: every rank passes the same full matrix (numpy or torch); each
-    factors its block-cyclic columns on its own GPU and the factors are all-gathered back."""
+def copy_local_columns(dst, src, n: int, b: int, P: int, r: int, to_device: bool, stream=None):
+    """Strided copies of rank r's block-cyclic column blocks between a full row-major n x n matrix
+    (host, ideally pinned) and the rank's local device buffer (pflu_copy2d per block)."""
+    L = _lib.load()
+    st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    nloc = local_cols(n, b, P, r)
+    full = src if to_device else dst
+    loc = dst if to_device else src
+    c = 0
+    for j in local_blocks(n, b, P, r):
+        w = min(b, n - j * b)
+        fptr = full.data_ptr() + j * b * 8
+        lptr = loc.data_ptr() + c * 8
+        if to_device:
+            rc = L.pflu_copy2d(lptr, nloc * 8, fptr, n * 8, w * 8, n, st)
+        else:
+            rc = L.pflu_copy2d(fptr, n * 8, lptr, nloc * 8, w * 8, n, st)
+        _lib.check(rc, "pflu_copy2d")
+        c += w
+
+
+def lu_factor_dist(a, b: int = 256, lookahead: int = 1, exact: bool = False, return_info: bool = False,
+                   gather: str = "all"):
+    r"""``lu_factor(..., n_gpus=P)``: every rank passes the same full n x n matrix (host numpy / torch,
+    or a CUDA tensor); each rank copies only its block-cyclic columns to its GPU and factors them.
+
+    gather="all"   -> every rank gets the full packed L\U (all-gather over NCCL);
+    gather="local" -> each rank writes ITS columns of L\U back into ``a`` in place (the distributed
+                      result, ScaLAPACK style) -- the cheap path used by bench.py's e2e leg.
+    Returns (lu, piv) (+ info): piv is the full 0-based pivot vector on every rank."""
     import numpy as np
 
     if not dist.is_initialized():
@@ -289,15 +316,24 @@ def lu_factor_dist(a, b: int = 256, lookahead: int = 1, exact: bool = False, ret
     P, r = dist.get_world_size(), dist.get_rank()
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", r % max(1, torch.cuda.device_count()))))
     torch.cuda.set_device(dev)
-    full = torch.as_tensor(np.asarray(a, dtype=np.float64)) if not isinstance(a, torch.Tensor) else a
+    full = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+    if full.dim() != 2 or full.shape[0] != full.shape[1] or full.dtype != torch.float64 or full.stride(1) != 1:
+        raise ValueError("the multi-GPU path factors square row-major float64 matrices")
     n = full.shape[1]
-    if full.shape[0] != n:
-        raise ValueError("the multi-GPU path factors square matrices")
-    a_loc = scatter_columns(full.to(dev), b, P, r)
+    a_loc = torch.empty((n, local_cols(n, b, P, r)), dtype=torch.float64, device=dev)
+    copy_local_columns(a_loc, full, n, b, P, r, to_device=True)
     piv, info = getrf_block_cyclic(a_loc, n, b, lookahead, CudaKernels(dev, exact=exact))
-    lu = allgather_columns(a_loc, n, b)
+    if gather == "local":
+        copy_local_columns(full, a_loc, n, b, P, r, to_device=False)
+        torch.cuda.synchronize()
+        lu = full
+    else:
+        lu = allgather_columns(a_loc, n, b)
+        if not full.is_cuda:
+            lu = lu.cpu()
     if not isinstance(a, torch.Tensor):
-        lu, piv = lu.cpu().numpy(), piv.cpu().numpy()
+        lu = lu.numpy() if gather == "all" else a
+        piv = piv.cpu().numpy()
     return (lu, piv, info) if return_info else (lu, piv)
 
 
@@ -355,27 +391,28 @@ def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
     ms_step = float(ms.item()) / args.steps
     value = lu_flops(n) / (ms_step * 1e-3) / 1e9
     peak, peak_src = fp64_peak()
-    # end to end: full host matrix in, factors + pivots back on every rank (pinned host buffers)
+    # end to end through the public API: full pinned host matrix in, each rank's L\U columns and
+    # the pivots back to the host (gather="local": the distributed result)
     e2e = None
     if args.e2e_steps > 0:
-        from .api import lu_factor  # noqa: F401  (public API entry)
-
-        host = torch.from_numpy(np.random.default_rng(3).uniform(-1.0, 1.0, size=(n, n))).pin_memory()
+        pristine = torch.from_numpy(np.random.default_rng(3).uniform(-1.0, 1.0, size=(n, n)))
+        host = torch.empty((n, n), dtype=torch.float64).pin_memory()
         ts = []
         for it in range(args.e2e_steps + 1):
+            host.copy_(pristine)
             dist.barrier()
             t0 = time.perf_counter()
-            lu, pv = lu_factor_dist(host, b=b, lookahead=la)
-            lu_h = lu.cpu()
-            torch.cuda.synchronize()
+            lu, pv = lu_factor_dist(host, b=b, lookahead=la, gather="local")
+            pv = pv.cpu()
             dist.barrier()
             ts.append(time.perf_counter() - t0)
-            del lu, lu_h
         tmax = torch.tensor([sum(ts[1:]) / len(ts[1:])], dtype=torch.float64, device=dev)
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        e2e = {"value": lu_flops(n) / float(tmax.item()) / 1e9, "unit": unit, "h2d_bytes_per_step": n * n * 8,
-               "d2h_bytes_per_step": n * n * 8 + n * 8,
-               "api": "paper_1804_07017_b200.dist.lu_factor_dist(pinned host matrix) per rank"}
+        nloc = local_cols(n, b, P, r)
+        e2e = {"value": lu_flops(n) / float(tmax.item()) / 1e9, "unit": unit, "h2d_bytes_per_step": n * nloc * 8,
+               "d2h_bytes_per_step": n * nloc * 8 + n * 8,
+               "api": "paper_1804_07017_b200.dist.lu_factor_dist(pinned host matrix, gather='local') per rank"}
+        del host, pristine
     if r == 0:
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": P, "steps": args.steps, "warmup": args.warmup,

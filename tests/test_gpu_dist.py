@@ -76,3 +76,41 @@ def test_dist_cuda_dmma(cuda, tmp_path, world, backend):
     assert np.array_equal(piv, rpiv)
     assert oracle.lu_residual(a, lu, piv) <= 10
     assert oracle.max_rel_diff(lu, ref, a) <= 1e-8
+
+
+def _worker_api(rank, world, port, backend, n, b, gather, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["LOCAL_RANK"] = "0"
+    torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+    from paper_1804_07017_b200 import dist as pd
+
+    a = np.random.default_rng(8).uniform(-1.0, 1.0, (n, n))
+    host = torch.from_numpy(a.copy()).pin_memory()
+    lu, piv, info = pd.lu_factor_dist(host, b=b, lookahead=1, exact=True, return_info=True, gather=gather)
+    out = lu.numpy() if isinstance(lu, torch.Tensor) else np.asarray(lu)
+    np.save(os.path.join(out_dir, f"lu{rank}.npy"), out)
+    np.save(os.path.join(out_dir, f"piv{rank}.npy"), piv.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("gather", ["all", "local"])
+def test_lu_factor_dist_api(cuda, tmp_path, gather):
+    from paper_1804_07017_b200 import dist as pd
+
+    n, b, world = 700, 64, 2
+    a = np.random.default_rng(8).uniform(-1.0, 1.0, (n, n))
+    ref, rpiv, _ = oracle.getrf(a, b)
+    mp.spawn(_worker_api, args=(world, _free_port(), "gloo", n, b, gather, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        lu = np.load(tmp_path / f"lu{r}.npy")
+        assert np.array_equal(np.load(tmp_path / f"piv{r}.npy"), rpiv)
+        if gather == "all":
+            assert lu.tobytes() == ref.tobytes()
+        else:   # the rank's own block-cyclic columns hold the factors
+            for j in pd.local_blocks(n, b, world, r):
+                sl = slice(j * b, min(n, (j + 1) * b))
+                assert lu[:, sl].tobytes() == np.ascontiguousarray(ref[:, sl]).tobytes()

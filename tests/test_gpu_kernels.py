@@ -214,3 +214,15 @@ def test_panel_zero_column_info(cuda):
     assert info.value == 2 == winfo
     assert bitwise_equal(x.cpu().numpy(), want)
     assert np.all(x.cpu().numpy()[2:, 1] == 0.0)
+
+
+def test_cli_sweep_with_check(cuda, capsys):
+    """python -m paper_1804_07017_b200.cli --check on the reference's own instances."""
+    from paper_1804_07017_b200 import cli
+
+    assert cli.main(["--kind", "lu", "--strategy", "all", "--n-min", "300", "--n-max", "600", "--n-step", "300",
+                     "--b", "64", "--reps", "1", "--check"]) == 0
+    recs = cli.parse_csv(capsys.readouterr().out)
+    assert len(recs) == 6 and {r.strategy for r in recs} == {"MTB", "LA", "LA_MB"}
+    for r in recs:
+        assert r.gflops > 0 and 0 < r.residual <= 50      # reference test_factor.py:391-398 bound
