@@ -59,6 +59,7 @@ typedef struct pflu_trace_event {
   int32_t k;
   float start_ms; /* CUDA-event time relative to the start of the factorization */
   float end_ms;
+  double flop;    /* algorithmic flops of the traced work (GEMM records; 0 otherwise) */
 } pflu_trace_event;
 
 int pflu_version(void);

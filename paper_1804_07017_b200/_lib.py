@@ -35,7 +35,7 @@ class Options(ctypes.Structure):
 
 class TraceEvent(ctypes.Structure):
     _fields_ = [("label", ctypes.c_int32), ("k", ctypes.c_int32),
-                ("start_ms", ctypes.c_float), ("end_ms", ctypes.c_float)]
+                ("start_ms", ctypes.c_float), ("end_ms", ctypes.c_float), ("flop", ctypes.c_double)]
 
 
 _lib = None

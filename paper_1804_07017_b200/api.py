@@ -116,6 +116,7 @@ class TraceEvent:
     start: float
     end: float
     worker: int | None
+    flop: float = 0.0   # algorithmic flops of the traced work (GEMM records)
 
 
 def flops(kind: Kind, n: int) -> int:
@@ -170,7 +171,7 @@ def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int
     tbuf, tcap, tlen = None, 0, ctypes.c_int(0)
     if trace is not None:
         steps = -(-n // max(1, min(b, n)))
-        tcap = 6 * steps + 16
+        tcap = 24 * steps + 32
         tbuf = (_lib.TraceEvent * tcap)()
     with torch.cuda.device(a.device):
         rc = L.pflu_getrf_device(a.data_ptr(), m, n, a.stride(0), int(b), int(lookahead), piv.data_ptr(),
@@ -181,7 +182,7 @@ def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int
             e = tbuf[i]
             lab = _lib.TRACE_LABELS.get(e.label, str(e.label))
             j = e.k + 1 if lab == "TU_L" else None
-            trace.append(TraceEvent(lab, int(e.k), j, e.start_ms * 1e-3, e.end_ms * 1e-3, None))
+            trace.append(TraceEvent(lab, int(e.k), j, e.start_ms * 1e-3, e.end_ms * 1e-3, None, float(e.flop)))
     return piv, int(info.value)
 
 

@@ -64,6 +64,10 @@ struct DevCtx {
   int sms = 0;
   size_t smem_optin = 0;
   cudaStream_t sP = nullptr, sU = nullptr;
+  cudaStream_t sL = nullptr;                 // deferred left swaps
+  std::vector<cudaStream_t> sC;              // trailing-update column-chunk streams
+  int64_t* plans = nullptr;                  // per-step pivot plans
+  size_t plans_cap = 0;                      // in int64 words
   int64_t* plan[2] = {nullptr, nullptr};
   unsigned long long* info = nullptr;
   unsigned long long* ll = nullptr;  // LL exchange words of the panel kernel
@@ -78,6 +82,7 @@ static int g_pf_cap = []() { const char* e = getenv("PFLU_PANEL_CAP"); return e 
 static int g_gemm_variant = []() { const char* e = getenv("PFLU_GEMM_VARIANT"); return e ? atoi(e) : 0; }();
 static DevCtx* g_dc = nullptr;  // context of the current call (set by ctx_get)
 static int g_resync = []() { const char* e = getenv("PFLU_PANEL_RESYNC"); return e ? atoi(e) : 4; }();
+static int g_chunks = []() { const char* e = getenv("PFLU_CHUNKS"); return e ? atoi(e) : 1; }();
 static int g_tur_grid = []() { const char* e = getenv("PFLU_TUR_GRID"); return e ? atoi(e) : 0; }();
 static int g_variant = []() { const char* e = getenv("PFLU_PANEL_VARIANT"); return e ? atoi(e) : 0; }();  // device buffer for panel-kernel phase clocks (tools only)
 
@@ -87,7 +92,7 @@ struct Tracer {
   bool on = false;
   size_t used = 0;
   cudaEvent_t t0 = nullptr;
-  struct Rec { int label, k; cudaEvent_t e0, e1; };
+  struct Rec { int label, k; cudaEvent_t e0, e1; double flop; };
   std::vector<Rec> recs;
   int ev(cudaEvent_t* out) {
     if (used == c->tev.size()) {
@@ -104,10 +109,10 @@ struct Tracer {
     CK(cudaEventRecord(t0, st));
     return PFLU_OK;
   }
-  int begin(int label, int k, cudaStream_t st, int* idx) {
+  int begin(int label, int k, cudaStream_t st, int* idx, double flop = 0.0) {
     *idx = -1;
     if (!on) return PFLU_OK;
-    Rec r{label, k, nullptr, nullptr};
+    Rec r{label, k, nullptr, nullptr, flop};
     CKR(ev(&r.e0));
     CKR(ev(&r.e1));
     CK(cudaEventRecord(r.e0, st));
@@ -128,7 +133,7 @@ struct Tracer {
         float a = 0.f, b = 0.f;
         CK(cudaEventElapsedTime(&a, t0, r.e0));
         CK(cudaEventElapsedTime(&b, t0, r.e1));
-        out[n].label = r.label; out[n].k = r.k; out[n].start_ms = a; out[n].end_ms = b;
+        out[n].label = r.label; out[n].k = r.k; out[n].start_ms = a; out[n].end_ms = b; out[n].flop = r.flop;
         ++n;
       }
     }
@@ -141,6 +146,7 @@ static std::mutex g_mu;
 static DevCtx g_ctx[64];
 
 static constexpr int PF_MAX_CTAS = PF_THREADS;
+static constexpr int MAX_CHUNKS = 8;
 static constexpr size_t LL_WORDS = PF_LL_WORDS;
 
 static int ctx_get(DevCtx** out) {
@@ -161,6 +167,9 @@ static int ctx_get(DevCtx** out) {
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&c.sP, cudaStreamNonBlocking, hi));
     CK(cudaStreamCreateWithPriority(&c.sU, cudaStreamNonBlocking, lo));
+    CK(cudaStreamCreateWithPriority(&c.sL, cudaStreamNonBlocking, lo));
+    c.sC.resize(MAX_CHUNKS);
+    for (auto& s : c.sC) CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, lo));
     CK(cudaMalloc(&c.plan[0], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
     CK(cudaMalloc(&c.plan[1], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
     CK(cudaMalloc(&c.info, 64));
@@ -407,6 +416,14 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   const bool exact = opt.exact != 0;
   CK(cudaMemsetAsync(info, 0xff, sizeof(unsigned long long), user));
   CKR(tr.start(user));
+  // per-step pivot plans (no reuse hazards between concurrently running steps)
+  const size_t plan_words = 1 + 3 * (size_t)std::max<int64_t>(1, std::min(b, n));
+  if (c.plans_cap < plan_words * count) {
+    if (c.plans) CK(cudaFree(c.plans));
+    c.plans_cap = plan_words * count;
+    CK(cudaMalloc(&c.plans, sizeof(int64_t) * c.plans_cap));
+  }
+  auto plan_of = [&](int k) { return c.plans + plan_words * k; };
   auto update_cols = [&](int k, int64_t lo, int64_t hi, cudaStream_t st, int label) -> int {
     // TU of step k on storage columns [lo, hi): laswp + trsm (fused), then the DMMA update
     if (hi <= lo) return PFLU_OK;
@@ -414,10 +431,11 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     const int np = (int)std::min(s.bw, m - s.col0);
     int t_tu = -1, t_g = -1;
     CKR(tr.begin(label, k, st, &t_tu));
-    CKR(launch_swap(a, lda, s.col0, np, c.plan[k & 1], lo, hi, a + s.col0 * lda + s.col0, lda, true, st));
+    CKR(launch_swap(a, lda, s.col0, np, plan_of(k), lo, hi, a + s.col0 * lda + s.col0, lda, true, st));
     const int64_t below = s.col0 + s.bw;
     if (below < m) {
-      if (label != PFLU_TRACE_TU_L) CKR(tr.begin(PFLU_TRACE_GEMM, k, st, &t_g));
+      if (label != PFLU_TRACE_TU_L)
+        CKR(tr.begin(PFLU_TRACE_GEMM, k, st, &t_g, 2.0 * (double)(m - below) * (double)(hi - lo) * (double)s.bw));
       const int pg = label == PFLU_TRACE_TU ? -1 : (label == PFLU_TRACE_TU_R ? g_tur_grid : 0);
       CKR(launch_gemm(a + below * lda + lo, lda, a + below * lda + s.col0, lda, a + s.col0 * lda + lo, lda,
                       m - below, hi - lo, s.bw, exact, st, pg));
@@ -429,7 +447,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     const Step s = grid[k];
     if (s.col0 == 0) return PFLU_OK;
     const int np = (int)std::min(s.bw, m - s.col0);
-    return launch_swap(a, lda, s.col0, np, c.plan[k & 1], 0, s.col0, nullptr, lda, false, st);
+    return launch_swap(a, lda, s.col0, np, plan_of(k), 0, s.col0, nullptr, lda, false, st);
   };
   auto pf = [&](int k, cudaStream_t st) -> int {
     const Step s = grid[k];
@@ -437,7 +455,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     CKR(tr.begin(PFLU_TRACE_PF, k, st, &t_pf));
     CKR(panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, opt, st));
     const int np = (int)std::min(s.bw, m - s.col0);
-    CKR(launch_plan(piv, s.col0, np, c.plan[k & 1], st));
+    CKR(launch_plan(piv, s.col0, np, plan_of(k), st));
     return tr.end(t_pf, st);
   };
 
@@ -450,35 +468,71 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     }
     return PFLU_OK;
   }
-  // lookahead 1 (dmf_la, factor.py:481-512)
-  CKR(ctx_events(c, 2 * (size_t)count + 4));
+  // lookahead 1 (dmf_la, factor.py:481-512) as a column-chunk dataflow.  The trailing columns are
+  // split into NCH fixed, block-aligned chunks, each with its own stream that runs its part of every
+  // step (laswp + trsm, then the GEMM) and depends only on the panel of that step -- a chunk never
+  // waits for another chunk, so one chunk's swap/solve overlaps the others' GEMMs.
+  //   sP (highest priority): TU_L(k) on block k+1 (after the chunk holding it finished step k-1),
+  //                          PF(k+1), plan(k+1)
+  //   sC[c]:                 TU_R(k) restricted to chunk c (after PF(k))
+  //   sL:                    left swaps(k) on blocks < k (after every reader of L21(k-1) finished)
+  const int nch = std::max(1, std::min({g_chunks, MAX_CHUNKS, count}));
+  std::vector<int> chunk_blk(nch + 1);
+  for (int ch = 0; ch <= nch; ++ch) chunk_blk[ch] = (int)((int64_t)count * ch / nch);
+  auto chunk_of_block = [&](int blk) {
+    int ch = 0;
+    while (ch + 1 < nch && chunk_blk[ch + 1] <= blk) ++ch;
+    return ch;
+  };
+  const size_t nev = 2 + (size_t)count * (nch + 2);
+  CKR(ctx_events(c, nev));
   cudaEvent_t ev_start = c.ev[0];
+  auto ev_pf = [&](int k) { return c.ev[2 + (size_t)k * (nch + 2)]; };
+  auto ev_tul = [&](int k) { return c.ev[3 + (size_t)k * (nch + 2)]; };
+  auto ev_ck = [&](int ch, int k) { return c.ev[4 + (size_t)k * (nch + 2) + ch]; };
   CK(cudaEventRecord(ev_start, user));
   CK(cudaStreamWaitEvent(c.sP, ev_start, 0));
-  CK(cudaStreamWaitEvent(c.sU, ev_start, 0));
-  auto ev_pf = [&](int k) { return c.ev[2 + 2 * k]; };
-  auto ev_tu = [&](int k) { return c.ev[3 + 2 * k]; };
+  CK(cudaStreamWaitEvent(c.sL, ev_start, 0));
+  for (int ch = 0; ch < nch; ++ch) CK(cudaStreamWaitEvent(c.sC[ch], ev_start, 0));
   CKR(pf(0, c.sP));
   CK(cudaEventRecord(ev_pf(0), c.sP));
   for (int k = 0; k < count; ++k) {
-    // branch_b: TU_R(k) on columns beyond panel k+1, then the deferred left swaps of step k
-    CK(cudaStreamWaitEvent(c.sU, ev_pf(k), 0));
     const int64_t lo_r = (k + 1 < count) ? grid[k + 1].col0 + grid[k + 1].bw : n;
-    CKR(update_cols(k, lo_r, n, c.sU, PFLU_TRACE_TU_R));
-    CKR(left_swaps(k, c.sU));
-    CK(cudaEventRecord(ev_tu(k), c.sU));
-    // branch_a: TU_L(k) on panel k+1's columns, then PF(k+1)
+    for (int ch = 0; ch < nch; ++ch) {
+      cudaStream_t st = c.sC[ch];
+      const int64_t c_lo = std::max<int64_t>(lo_r, (int64_t)chunk_blk[ch] * b);
+      const int64_t c_hi = std::min<int64_t>(n, (int64_t)chunk_blk[ch + 1] * b);
+      if (c_hi > c_lo) {
+        CK(cudaStreamWaitEvent(st, ev_pf(k), 0));
+        CKR(update_cols(k, c_lo, c_hi, st, PFLU_TRACE_TU_R));
+      }
+      CK(cudaEventRecord(ev_ck(ch, k), st));
+    }
+    if (k > 0) {
+      // left swaps(k) rewrite rows of L21(k-1): wait for every GEMM(k-1) (chunks + TU_L)
+      CK(cudaStreamWaitEvent(c.sL, ev_pf(k), 0));
+      for (int ch = 0; ch < nch; ++ch) CK(cudaStreamWaitEvent(c.sL, ev_ck(ch, k - 1), 0));
+      CK(cudaStreamWaitEvent(c.sL, ev_tul(k - 1), 0));
+      CKR(left_swaps(k, c.sL));
+    }
     if (k + 1 < count) {
-      if (k > 0) CK(cudaStreamWaitEvent(c.sP, ev_tu(k - 1), 0));
+      if (k > 0) CK(cudaStreamWaitEvent(c.sP, ev_ck(chunk_of_block(k + 1), k - 1), 0));
       CKR(update_cols(k, grid[k + 1].col0, grid[k + 1].col0 + grid[k + 1].bw, c.sP, PFLU_TRACE_TU_L));
+      CK(cudaEventRecord(ev_tul(k), c.sP));
       CKR(pf(k + 1, c.sP));
       CK(cudaEventRecord(ev_pf(k + 1), c.sP));
+    } else {
+      CK(cudaEventRecord(ev_tul(k), c.sP));
     }
   }
   CK(cudaEventRecord(c.ev[1], c.sP));
   CK(cudaStreamWaitEvent(user, c.ev[1], 0));
-  CK(cudaEventRecord(ev_tu(count - 1), c.sU));
-  CK(cudaStreamWaitEvent(user, ev_tu(count - 1), 0));
+  for (int ch = 0; ch < nch; ++ch) {
+    CK(cudaEventRecord(ev_ck(ch, count - 1), c.sC[ch]));
+    CK(cudaStreamWaitEvent(user, ev_ck(ch, count - 1), 0));
+  }
+  CK(cudaEventRecord(ev_tul(count - 1), c.sL));
+  CK(cudaStreamWaitEvent(user, ev_tul(count - 1), 0));
   return PFLU_OK;
 }
 

@@ -24,14 +24,18 @@ for it in range(2):
     torch.cuda.synchronize()
 tot = e0.elapsed_time(e1)
 by = {}
-for ev in tr:
-    by.setdefault((ev.label, ev.k), ev)
+for ev in tr:  # chunked TU_R: several records per (label, k) -> span from first start to last end
+    if (ev.label, ev.k) in by:
+        o = by[(ev.label, ev.k)]
+        by[(ev.label, ev.k)] = type(ev)(ev.label, ev.k, ev.j, min(o.start, ev.start), max(o.end, ev.end), None, o.flop + ev.flop)
+    else:
+        by[(ev.label, ev.k)] = ev
 steps = max(ev.k for ev in tr) + 1
 lab_r = "TU_R" if la else "TU"
-gemm_ms = sum((ev.end - ev.start) * 1e3 for ev in tr if ev.label == "GEMM")
+gemm_ms = sum((by[k].end - by[k].start) * 1e3 for k in by if k[0] == "GEMM")
 pf_ms = sum((ev.end - ev.start) * 1e3 for ev in tr if ev.label == "PF")
 tul_ms = sum((ev.end - ev.start) * 1e3 for ev in tr if ev.label == "TU_L")
-tur_ms = sum((ev.end - ev.start) * 1e3 for ev in tr if ev.label == lab_r)
+tur_ms = sum((by[k].end - by[k].start) * 1e3 for k in by if k[0] == lab_r)
 gaps = 0.0
 rows = []
 for k in range(steps):
