@@ -239,12 +239,12 @@ static int launch_gemm_t(const GemmArgs& p0, bool v2, cudaStream_t st) {
 }
 
 // persistent launch: at most `ctas` CTAs (0 = SMs x resident CTAs per SM)
-template <class C>
+template <class C, bool PREF = false>
 static int launch_gemm_p(DevCtx& dc, const GemmArgs& p0, bool v2, int ctas, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(gemm_dmma_persistent<C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    CK(cudaFuncSetAttribute(gemm_dmma_persistent<C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    CK(cudaFuncSetAttribute(gemm_dmma_persistent<C, 1, PREF>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    CK(cudaFuncSetAttribute(gemm_dmma_persistent<C, 2, PREF>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
   GemmArgs p = p0;
@@ -254,8 +254,8 @@ static int launch_gemm_p(DevCtx& dc, const GemmArgs& p0, bool v2, int ctas, cuda
   p.tiles_n = (int)tn;
   int grid = ctas > 0 ? ctas : dc.sms * C::MINB;
   grid = (int)std::min<int64_t>(grid, tm * tn);
-  if (v2) gemm_dmma_persistent<C, 2><<<grid, C::THREADS, C::SMEM, st>>>(p);
-  else gemm_dmma_persistent<C, 1><<<grid, C::THREADS, C::SMEM, st>>>(p);
+  if (v2) gemm_dmma_persistent<C, 2, PREF><<<grid, C::THREADS, C::SMEM, st>>>(p);
+  else gemm_dmma_persistent<C, 1, PREF><<<grid, C::THREADS, C::SMEM, st>>>(p);
   return PFLU_OK;
 }
 
@@ -286,6 +286,7 @@ static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, con
       case 6: CKR(launch_gemm_t<GV6>(p, v2, st)); break;
       case 7: CKR(launch_gemm_t<GV7>(p, v2, st)); break;
       case 10: CKR(launch_gemm_p<GV0>(*g_dc, p, v2, 0, st)); break;
+      case 11: CKR((launch_gemm_p<GV0, true>(*g_dc, p, v2, 0, st))); break;
       case 13: CKR(launch_gemm_p<GV3>(*g_dc, p, v2, 0, st)); break;
       case 17: CKR(launch_gemm_p<GV7>(*g_dc, p, v2, 0, st)); break;
       case 20: CKR(launch_gemm_p<GV0>(*g_dc, p, v2, g_dc->sms, st)); break;

@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_t(GemmArgs p) {
 // Persistent form: gridDim.x CTAs stride over the tiles; the operand pipeline runs continuously
 // across tile boundaries (the first stages of tile t+1 are issued while tile t computes its last
 // stages), which removes CTA launch gaps and hides the per-tile pipeline fill.
-template <class C, int VEC>
+template <class C, int VEC, bool PREF = false>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_persistent(GemmArgs p) {
   extern __shared__ __align__(128) double gm_smem[];
   double* sA = gm_smem;
@@ -278,6 +278,24 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_persistent(Gemm
       cp_async_wait<C::ST - 2>();
       __syncthreads();
       issue();
+      if (PREF && kt == KT / 2) {
+        // pull the next tile's C block into L2 so its accumulator load does not wait on HBM
+        const int nt = tile + gridDim.x;
+        if (nt < ntiles) {
+          int ntm, ntn;
+          tile_coords(nt, p.tiles_m, p.tiles_n, ntm, ntn);
+          const int nm0 = ntm * C::BM, nn0 = ntn * C::BN;
+          for (int r = tid; r < C::BM; r += C::THREADS) {
+            const int64_t row = nm0 + r;
+            if (row < p.M) {
+              const double* rp = p.c + row * p.ldc + nn0;
+#pragma unroll
+              for (int cl = 0; cl < C::BN * 8; cl += 128)
+                if (nn0 + cl / 8 < p.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + cl / 8));
+            }
+          }
+        }
+      }
       const double* cA = sA + (cstage % C::ST) * C::BM * C::BK;
       const double* cB = sB + (cstage % C::ST) * C::BK * C::BN;
 #pragma unroll

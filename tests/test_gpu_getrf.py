@@ -201,3 +201,27 @@ def test_c5_prefix_and_residual_single_gpu(cuda):
     amax = float(d_a0.abs().max())
     assert float((d_lu[:512].cpu() - torch.from_numpy(top)).abs().max()) / amax <= 1e-10
     assert lu_residual_gpu(d_a0, d_lu, piv, block=8192) <= 10
+
+
+@pytest.mark.parametrize("lookahead", [0, 1])
+def test_nan_inf_pivot_rules(cuda, lookahead):
+    """Special values follow the reference's strict '>' scan (_jit.py:163-170): a NaN candidate is never
+    taken unless it is on the diagonal, +-inf wins, ties go to the smallest row."""
+    import warnings
+
+    rng = np.random.default_rng(31)
+    a = rng.uniform(-1.0, 1.0, (300, 300))
+    a[17, 3] = np.nan          # below the diagonal of column 3: must not be chosen
+    a[5, 5] = np.nan           # a NaN diagonal candidate
+    a[200, 40] = np.inf        # must win column 40 (if still finite there)
+    a[100, 60] = -np.inf
+    a[150, 80] = a[151, 80] = 7.0   # exact tie: smaller row wins
+    ref, rpiv, rinfo = oracle.getrf(a, 64)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        for exact in (True, False):
+            lu, piv, info = run(a, 64, lookahead, exact=exact)
+            assert np.array_equal(piv, rpiv), exact
+            assert info == rinfo
+            if exact:
+                assert np.array_equal(lu, ref, equal_nan=True)
