@@ -81,6 +81,11 @@ static unsigned long long* g_prof = nullptr;
 static int g_pf_cap = []() { const char* e = getenv("PFLU_PANEL_CAP"); return e ? atoi(e) : 32; }();
 static int g_gemm_variant = []() { const char* e = getenv("PFLU_GEMM_VARIANT"); return e ? atoi(e) : 0; }();
 static DevCtx* g_dc = nullptr;  // context of the current call (set by ctx_get)
+static int g_leaf = []() { const char* e = getenv("PFLU_LEAF"); return e ? atoi(e) : 0; }();
+// cluster panel: max CTAs per cluster (0 = LL kernel only), min rows per CTA, max panel rows
+static int g_cluster = []() { const char* e = getenv("PFLU_CLUSTER"); return e ? atoi(e) : 16; }();
+static int g_cl_minrows = []() { const char* e = getenv("PFLU_CL_MINROWS"); return e ? std::max(1, atoi(e)) : 128; }();
+static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
 static int g_resync = []() { const char* e = getenv("PFLU_PANEL_RESYNC"); return e ? atoi(e) : 4; }();
 static int g_chunks = []() { const char* e = getenv("PFLU_CHUNKS"); return e ? atoi(e) : 1; }();
 static int g_tur_grid = []() { const char* e = getenv("PFLU_TUR_GRID"); return e ? atoi(e) : 0; }();
@@ -146,6 +151,13 @@ static std::mutex g_mu;
 static DevCtx g_ctx[64];
 
 static constexpr int PF_MAX_CTAS = PF_THREADS;
+
+static const void* pf_fn(int W, bool cl) {
+  if (cl) return W == 8 ? (const void*)panel_kernel<8, true> : W == 16 ? (const void*)panel_kernel<16, true>
+                                                                       : (const void*)panel_kernel<32, true>;
+  return W == 8 ? (const void*)panel_kernel<8, false> : W == 16 ? (const void*)panel_kernel<16, false>
+                                                                : (const void*)panel_kernel<32, false>;
+}
 static constexpr int MAX_CHUNKS = 8;
 static constexpr size_t LL_WORDS = PF_LL_WORDS;
 
@@ -188,9 +200,11 @@ static int ctx_get(DevCtx** out) {
       return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(c.smem_optin - fa.sharedSizeBytes));
     };
-    CK(allow((const void*)panel_kernel<8>));
-    CK(allow((const void*)panel_kernel<16>));
-    CK(allow((const void*)panel_kernel<32>));
+    for (int W : {8, 16, 32})
+      for (bool cl : {false, true}) {
+        CK(allow(pf_fn(W, cl)));
+        if (cl) CK(cudaFuncSetAttribute(pf_fn(W, cl), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      }
     CK(allow((const void*)swap_trsm_kernel<8>));
     CK(allow((const void*)swap_trsm_kernel<16>));
     CK(allow((const void*)swap_trsm_kernel<32>));
@@ -351,16 +365,48 @@ static int launch_swap(double* a, int64_t lda, int64_t d, int np, const int64_t*
 }
 
 static int pf_occupancy(int W, size_t smem, int* occ) {
-  if (W == 8) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, panel_kernel<8>, PF_THREADS, smem));
-  else if (W == 16) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, panel_kernel<16>, PF_THREADS, smem));
-  else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, panel_kernel<32>, PF_THREADS, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, pf_fn(W, false), PF_THREADS, smem));
   return PFLU_OK;
 }
 
-static size_t pf_smem_bytes(int W, int64_t R, int w) {
-  if (W == 8) return PanelSmem<8>::bytes(R, w);
-  if (W == 16) return PanelSmem<16>::bytes(R, w);
-  return PanelSmem<32>::bytes(R, w);
+static size_t pf_smem_bytes(int W, int64_t R, int w, bool cl = false) {
+  if (W == 8) return PanelSmem<8>::bytes(R, w, cl);
+  if (W == 16) return PanelSmem<16>::bytes(R, w, cl);
+  return PanelSmem<32>::bytes(R, w, cl);
+}
+
+// can a cluster of S panel CTAs (W, full shared memory) be resident?  cached per (W, S)
+static int pf_cluster_ok(DevCtx& c, int W, int S, bool* ok) {
+  static int cache[3][PF_CL_MAX + 1];
+  static bool init = false;
+  if (!init) {
+    for (auto& r : cache)
+      for (int& v : r) v = -1;
+    init = true;
+  }
+  const int wi = W == 8 ? 0 : W == 16 ? 1 : 2;
+  if (cache[wi][S] < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = S;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(S);
+    cfg.blockDim = dim3(PF_THREADS);
+    cfg.dynamicSmemBytes = c.smem_optin - 2048;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&n, pf_fn(W, true), &cfg);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    cache[wi][S] = n;
+  }
+  *ok = cache[wi][S] > 0;
+  return PFLU_OK;
 }
 
 // Persistent panel factorization: rows [r0, m) of storage columns [c0, c0 + w).
@@ -369,8 +415,46 @@ static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0
   const int64_t rows = m - r0;
   if (rows <= 0 || w <= 0) return PFLU_OK;
   const size_t smax = c.smem_optin - 2048;
-  int Wpref = opt.leaf_width > 0 ? opt.leaf_width : (w > 16 ? 32 : (w > 8 ? 16 : 8));
+  int Wpref = opt.leaf_width > 0 ? opt.leaf_width : g_leaf > 0 ? g_leaf : (w > 16 ? 32 : (w > 8 ? 16 : 8));
   const int Ws[3] = {32, 16, 8};
+  PanelArgs p;
+  p.a = a; p.lda = lda; p.m = m; p.r0 = r0; p.col0 = c0; p.w = (int)w;
+  p.piv = piv; p.info = info; p.ll = c.ll; p.epoch = c.epoch; p.exact = opt.exact;
+  p.prof = g_prof;
+  p.resync = g_resync;
+  // one thread-block cluster (DSMEM exchange) when the rows fit its CTAs' shared memory
+  if (g_cluster > 0 && rows <= g_cl_rows) {
+    const int Smax = std::max(1, std::min(g_cluster, PF_CL_MAX));
+    for (int wi = 0; wi < 3; ++wi) {
+      const int W = Ws[wi];
+      if (W > Wpref) continue;
+      const int S0 = (int)std::min<int64_t>(Smax, std::max<int64_t>(1, (rows + g_cl_minrows - 1) / g_cl_minrows));
+      const int64_t R = (rows + S0 - 1) / S0;
+      const int S = (int)((rows + R - 1) / R);
+      const size_t smem = pf_smem_bytes(W, R, (int)w, true);
+      if (smem > smax) continue;
+      bool ok = false;
+      CKR(pf_cluster_ok(c, W, S, &ok));
+      if (!ok) continue;
+      p.R = R;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = S;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(S);
+      cfg.blockDim = dim3(PF_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      void* args[] = {&p};
+      CK(cudaLaunchKernelExC(&cfg, pf_fn(W, true), args));
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return PFLU_OK;
+    }
+  }
   for (int wi = 0; wi < 3; ++wi) {
     const int W = Ws[wi];
     if (W > Wpref) continue;
@@ -384,15 +468,9 @@ static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0
       CKR(pf_occupancy(W, smem, &occ));
       if ((int64_t)occ * c.sms < S) break;
       int S_eff = (int)((rows + R - 1) / R);
-      PanelArgs p;
-      p.a = a; p.lda = lda; p.m = m; p.r0 = r0; p.col0 = c0; p.w = (int)w; p.R = R;
-      p.piv = piv; p.info = info; p.ll = c.ll; p.epoch = c.epoch; p.exact = opt.exact;
-      p.prof = g_prof;
-      p.resync = g_resync;
+      p.R = R;
       void* args[] = {&p};
-      const void* fn = W == 8 ? (const void*)panel_kernel<8> : W == 16 ? (const void*)panel_kernel<16>
-                                                                       : (const void*)panel_kernel<32>;
-      CK(cudaLaunchCooperativeKernel(fn, dim3(S_eff), dim3(PF_THREADS), args, smem, st));
+      CK(cudaLaunchCooperativeKernel(pf_fn(W, false), dim3(S_eff), dim3(PF_THREADS), args, smem, st));
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return PFLU_OK;
     }

@@ -57,6 +57,33 @@ __device__ __forceinline__ bool key_better(double ka, long long ra, double kb, l
   return ka > kb || (ka == kb && ra < rb);
 }
 
+// Order-preserving map of a (non-NaN) double onto uint64.
+__device__ __forceinline__ unsigned long long key_ord(double k) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(k);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+// Warp arg-max under key_better (largest key, equal keys -> smallest row) with redux.sync: every
+// lane receives the winner; returns the winning lane (for extra payload).  Rows are >= 0.
+__device__ __forceinline__ int warp_best(double& k, long long& r) {
+  const unsigned full = 0xffffffffu;
+  const unsigned long long u = key_ord(k);
+  const unsigned hi = (unsigned)(u >> 32), lo = (unsigned)u;
+  const unsigned mhi = __reduce_max_sync(full, hi);
+  const unsigned mlo = __reduce_max_sync(full, hi == mhi ? lo : 0u);
+  const unsigned eq = __ballot_sync(full, hi == mhi && lo == mlo);
+  int src = __ffs(eq) - 1;
+  if (eq & (eq - 1)) {  // bitwise-equal best keys in several lanes: the smallest row
+    const unsigned long long rr = ((eq >> (threadIdx.x & 31)) & 1u) ? (unsigned long long)r : ~0ull;
+    const unsigned rhi = (unsigned)(rr >> 32), rlo = (unsigned)rr;
+    const unsigned nhi = __reduce_min_sync(full, rhi);
+    const unsigned nlo = __reduce_min_sync(full, rhi == nhi ? rlo : ~0u);
+    src = __ffs(__ballot_sync(full, rhi == nhi && rlo == nlo)) - 1;
+  }
+  k = __shfl_sync(full, k, src);
+  r = __shfl_sync(full, r, src);
+  return src;
+}
+
 // ==========================================================================================
 // Pivot plan: composes the ascending LAPACK swaps piv[d..d+np) (global 0-based rows, piv[i] >= i)
 // into a gather.  Output layout (int64): [0] = E (extra rows), [1 .. np] = source row of top row

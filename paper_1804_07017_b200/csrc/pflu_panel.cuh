@@ -46,6 +46,21 @@ struct PanelArgs {
   int resync;                // re-align all CTAs every `resync` columns (0 = never)
 };
 
+// key polling: spin this many misses before backing off with __nanosleep (whose granularity is
+// coarse, ~1 us: a sleep on the critical path costs a column's worth of time)
+constexpr int PF_POLL_SPINS = 64;
+
+__device__ __forceinline__ unsigned long long pf_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// timeline (tools/panel_prof.py): prof[8192 + ((q * 64) + col) * 4 + event], globaltimer ns
+#define PF_TL(ev, col)                                                                          \
+  do {                                                                                          \
+    if (p.prof != nullptr && (col) < 64) p.prof[8192 + ((size_t)q * 64 + (col)) * 4 + (ev)] = pf_gtime(); \
+  } while (0)
+
 #define PF_PROF_MARK(i)                                              \
   do {                                                              \
     if (prof_on) {                                                  \
@@ -93,11 +108,19 @@ __device__ __forceinline__ bool ll_try2(const unsigned long long* p, unsigned fl
   b = (unsigned)v1;
   return (unsigned)(v0 >> 32) == flag && (unsigned)(v1 >> 32) == flag;
 }
-__device__ __forceinline__ double ll_get2_d(const unsigned long long* p, unsigned flag) {
+// sync words carry a per-launch monotonic counter: "reached" = flag at or past the wanted one, so a
+// fast writer that already moved on to the next sync cannot strand a slow reader
+__device__ __forceinline__ bool ll_reached2(const unsigned long long* p, unsigned flag) {
+  unsigned long long v0, v1;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(v0), "=l"(v1) : "l"(p) : "memory");
+  return (int)((unsigned)(v0 >> 32) - flag) >= 0 && (int)((unsigned)(v1 >> 32) - flag) >= 0;
+}
+__device__ __forceinline__ double ll_get2_d(const unsigned long long* p, unsigned flag, int spins = 1 << 30) {
   unsigned a, b;
-  // one-shot reads of data that is normally already visible; on a miss back off instead of
-  // spinning, since many SMs spinning on a line delay the writer's store
-  while (!ll_try2(p, flag, a, b)) __nanosleep(128);
+  // one-shot reads of data that is normally already visible; after `spins` misses back off (the
+  // sleep granularity is coarse: ~1 us)
+  for (int s = 0; !ll_try2(p, flag, a, b); ++s)
+    if (s >= spins) __nanosleep(128);
   return __longlong_as_double(((long long)b << 32) | a);
 }
 
@@ -113,8 +136,7 @@ __device__ __forceinline__ void ll_grid_sync(unsigned long long* sbox, int S, in
       for (int t = threadIdx.x; t < S; t += 32) ll_put2(sbox + ((size_t)t * 256 + q) * 2, 0u, 0u, flag);
     }
     if ((int)threadIdx.x < S) {
-      unsigned a, b;
-      while (!ll_try2(sbox + ((size_t)q * 256 + threadIdx.x) * 2, flag, a, b)) {
+      while (!ll_reached2(sbox + ((size_t)q * 256 + threadIdx.x) * 2, flag)) {
       }
     }
     __threadfence();
@@ -122,17 +144,65 @@ __device__ __forceinline__ void ll_grid_sync(unsigned long long* sbox, int S, in
   __syncthreads();
 }
 
+// Re-alignment of all CTAs without memory ordering (no data is published through it): LL flags only.
+__device__ __forceinline__ void ll_grid_align(unsigned long long* sbox, int S, int q, unsigned flag) {
+  if (S > 1) {
+    if (threadIdx.x < 32) {
+      for (int t = threadIdx.x; t < S; t += 32) ll_put2(sbox + ((size_t)t * 256 + q) * 2, 0u, 0u, flag);
+      for (int t = threadIdx.x; t < S; t += 32) {
+        while (!ll_reached2(sbox + ((size_t)q * 256 + t) * 2, flag)) {
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- cluster (DSMEM) exchange primitives
+constexpr int PF_CL_MAX = 16;  // CTAs per cluster (16 = non-portable size)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t cl_map(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// 16-byte store into a peer CTA's shared memory that completes `bytes` on the peer's mbarrier
+__device__ __forceinline__ void cl_put16(uint32_t raddr, unsigned long long x, unsigned long long y, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];\n"
+               ::"r"(raddr), "l"(x), "l"(y), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void cl_expect(uint32_t bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cl_wait(uint32_t bar, unsigned parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+                 "selp.u32 %0, 1, 0, p;\n}\n" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  }
+}
+// all threads of all CTAs of the cluster; release/acquire at cluster scope (global data included)
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 template <int W>
 struct PanelSmem {
   static constexpr int LD = W + 1;
-  static size_t bytes(int64_t R, int w) {
+  static size_t bytes(int64_t R, int w, bool cl = false) {
     // tile R x LD, U buffer W x (w - W) (>= W x 8), L_JJ W x W, u / dg W each, plan 4W ints
+    // (+ cluster mode: keys [2][PF_CL_MAX][2], published rows [2][W] x 2, 2 mbarriers, alignment)
     const int64_t nright = w > W ? w - W : 8;
-    return (size_t)(R * LD + (int64_t)W * nright + W * W + 4 * W) * 8 + 4 * W * 8 + 256;
+    return (size_t)(R * LD + (int64_t)W * nright + W * W + 4 * W) * 8 + 4 * W * 8 + 256 +
+           (cl ? (size_t)(4 * PF_CL_MAX + 4 * W + 2 + 2) * 8 : 0);
   }
 };
 
-template <int W>
+// CL = false: S co-resident CTAs exchange through LL words in global memory (any S <= 256).
+// CL = true:  the S <= 16 CTAs form one thread-block cluster; candidates and the diagonal row are
+//             pushed into every peer's shared memory with st.async completing on the peer's mbarrier
+//             (no polling, no L2 round trip), and grid syncs are cluster barriers.
+template <int W, bool CL>
 __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   extern __shared__ __align__(16) double pf_smem[];
   constexpr int LD = W + 1;
@@ -151,15 +221,29 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   double* dg = u + 2 * W;                                 // [2][W] old diagonal row
   long long* plan_row = reinterpret_cast<long long*>(dg + 2 * W);  // [2W] slot -> destination row
   long long* plan_src_row = plan_row + 2 * W;                       // [2W] slot -> source row
+  // CL: keys pushed by the peers (16-byte aligned for st.async), own published candidate / diagonal
+  // rows (pulled by the peers with DSMEM loads), mbarriers; all double-buffered by exchange parity
+  double* xkey = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(plan_src_row + 2 * W) + 15) & ~(uintptr_t)15);
+  double* pubrow = xkey + 2 * PF_CL_MAX * 2;  // [2][W]
+  double* pubdiag = pubrow + 2 * W;           // [2][W]
+  unsigned long long* xbar = reinterpret_cast<unsigned long long*>(pubdiag + 2 * W);  // [2]
+  unsigned xs = 0;  // CL: exchanges so far (uniform over the cluster): buffer xs & 1, phase (xs >> 1) & 1
+  if constexpr (CL) {
+    if (tid == 0) {
+      for (int i = 0; i < 2; ++i)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(xbar + i)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    cl_sync();  // peers may push into this CTA's barriers only once they are initialised
+  }
   __shared__ double red_key[PF_THREADS / 32];
   __shared__ long long red_row[PF_THREADS / 32];
-  __shared__ int red_q[PF_THREADS / 32];
-  __shared__ double red2_key[PF_THREADS / 32];
-  __shared__ long long red2_row[PF_THREADS / 32];
   __shared__ int s_nslots;
   __shared__ long long blk_piv[32];  // pivots of the current block (every CTA knows them)
+  __shared__ double s_wkey;          // winner of the next column (written by warp 0)
+  __shared__ long long s_wrow;
 
-  const unsigned epoch = *(volatile unsigned*)p.epoch;
+  const unsigned epoch = CL ? 0u : *(volatile unsigned*)p.epoch;
   // LL layout: [2 parities][S + 1 records][16 + 2W words], then S sync words
   const int rec = 16 + 2 * W;  // [key line: key, row (16 words = 128 B)][data: 2W words]; 128-B aligned
   unsigned long long* sync_words = p.ll + PF_SBOX_OFFSET;  // [reader 256][writer 256][2 words]
@@ -170,6 +254,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   long long prof_t = clock64();
   long long prof_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 
+  // grid-sync flags: epoch + w + (running count of syncs in this launch); the sync sequence is the same
+  // on every CTA, and the epoch advance below exceeds w + the sync count
+  unsigned nsync = 0;
+  auto sync_flag = [&]() { return epoch + (unsigned)w + (++nsync); };
   int pend_kb = 0, pend_nright = 0, pend_right0 = 0;  // U rows awaiting write-back
   int64_t pend_cJ = 0;
   for (int jb = 0; jb < w; jb += W) {
@@ -198,22 +286,30 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     // exchange.  Every row is owned by one thread, so the swap needs no barrier.
     const int kmax = (int)min((int64_t)wb, p.m - cJ);
     auto cta_best = [&](double& bk, long long& br) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-        const long long orr = __shfl_xor_sync(0xffffffffu, br, o);
-        if (key_better(ok, orr, bk, br)) { bk = ok; br = orr; }
-      }
+      warp_best(bk, br);
       if (lane == 0) { red_key[warp] = bk; red_row[warp] = br; }
       __syncthreads();
-      bk = red_key[0];
-      br = red_row[0];
-#pragma unroll
-      for (int w2 = 1; w2 < PF_THREADS / 32; ++w2)
-        if (key_better(red_key[w2], red_row[w2], bk, br)) { bk = red_key[w2]; br = red_row[w2]; }
+      constexpr int NW = PF_THREADS / 32;
+      bk = lane < NW ? red_key[lane] : -3.0;
+      br = lane < NW ? red_row[lane] : LLONG_MAX;
+      warp_best(bk, br);
     };
     // publish candidate (key, row, data of tile row br) for column jn; warp 0 only
     auto publish_cand = [&](int jn, double bk, long long br) {
+      if constexpr (CL) {
+        // the finished candidate row goes to the publish buffer, then one (key, row) st.async per
+        // peer; its complete_tx has release semantics at cluster scope, so a peer that saw the key
+        // can pull the row
+        double* pr = pubrow + (xs & 1) * W;
+        if (bk > -2.0)
+          for (int cc = lane; cc < wb; cc += 32) pr[cc] = tile[(br - rbeg) * LD + cc];
+        __syncwarp();
+        if (lane < S)
+          cl_put16(cl_map(smem_addr(xkey + ((xs & 1) * PF_CL_MAX + q) * 2), lane),
+                   (unsigned long long)__double_as_longlong(bk), (unsigned long long)br,
+                   cl_map(smem_addr(xbar + (xs & 1)), lane));
+        return;
+      }
       const unsigned fl = epoch + (unsigned)(jb + jn);
       unsigned long long* sl = p.ll + (size_t)(jn & 1) * (S + 1) * rec;
       unsigned long long* my = sl + (size_t)q * rec;
@@ -231,10 +327,96 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       }
     };
     auto publish_diag = [&](int jn, long long row) {  // the owner of the next diagonal row, one warp
+      if constexpr (CL) {  // warp 0, before it pushes its key: the diagonal row to the publish buffer
+        double* pd = pubdiag + (xs & 1) * W;
+        for (int cc = lane; cc < wb; cc += 32) pd[cc] = tile[(row - rbeg) * LD + cc];
+        return;
+      }
       const unsigned fl = epoch + (unsigned)(jb + jn);
       unsigned long long* dsl = p.ll + (size_t)(jn & 1) * (S + 1) * rec + (size_t)S * rec;
       const double* trow = tile + (row - rbeg) * LD;
       for (int cc = lane; cc < wb; cc += 32) ll_put2_d(dsl + 16 + 2 * cc, trow[cc], fl);
+    };
+    // Warp 0 gathers the winner of column jn: the S keys from this CTA's mailbox, then the winner's
+    // row (LL slot, or the tile when this CTA owns it -- finished by warp 0 itself) into u[jn & 1] and,
+    // when this CTA owns the winner but not the diagonal row, the old diagonal row into dg[jn & 1]
+    // (when it owns both, warp 1 staged that row).  (lk, lr) is this CTA's own candidate.
+    auto gather = [&](int jn, double lk, long long lr) {
+      const unsigned flag = epoch + (unsigned)(jb + jn);
+      const int64_t cn = cJ + jn;
+      double bk = -3.0;
+      long long br = LLONG_MAX;
+      int bq = -1;
+      if (CL && S > 1) {
+        const uint32_t bar = smem_addr(xbar + (xs & 1));
+        if (lane == 0) cl_expect(bar, (unsigned)S * 16u);
+        cl_wait(bar, (xs >> 1) & 1u);
+        if (lane < S) {
+          const double* kk = xkey + ((xs & 1) * PF_CL_MAX + lane) * 2;
+          const double k = kk[0];
+          const long long rr = __double_as_longlong(kk[1]);
+          if (k > -2.0) { bk = k; br = rr; }
+        }
+        bq = warp_best(bk, br);
+      } else if (S > 1) {
+        const unsigned long long* mb = mbox + (size_t)(jn & 1) * 256 * 256 * 4 + (size_t)q * 256 * 4;
+        for (int t = lane; t < S; t += 32) {
+          const unsigned long long* e = mb + (size_t)t * 4;
+          unsigned k0, k1, r0_, r1_;
+          bool ok0 = false, ok1 = false;
+          int spins = 0;
+          while (!(ok0 && ok1)) {  // both 16-byte loads in flight together
+            if (!ok0) ok0 = ll_try2(e, flag, k0, k1);
+            if (!ok1) ok1 = ll_try2(e + 2, flag, r0_, r1_);
+            if (!(ok0 && ok1) && ++spins > PF_POLL_SPINS) __nanosleep(32);
+          }
+          const double k = __longlong_as_double(((long long)k1 << 32) | k0);
+          const long long rr = (long long)r0_ + p.r0;
+          if (k > -2.0 && key_better(k, rr, bk, br)) { bk = k; br = rr; bq = t; }
+        }
+        bq = __shfl_sync(0xffffffffu, bq, warp_best(bk, br));
+      } else {
+        bk = lk; br = lr; bq = q;
+      }
+      if (bk > 0.0) {
+        double* un = u + (jn & 1) * W;
+        double* dn = dg + (jn & 1) * W;
+        const bool own_p = br >= rbeg && br < rend;
+        const bool own_cn = cn >= rbeg && cn < rend;
+        const unsigned long long* sl = p.ll + (size_t)(jn & 1) * (S + 1) * rec;
+        if (CL && S > 1) {
+          // pull the winner row (and, for the winner's owner, the old diagonal row) from the owners'
+          // publish buffers; both loads in flight together
+          const bool need_d = own_p && br != cn && !own_cn;
+          const uint32_t ra = cl_map(smem_addr(pubrow + (xs & 1) * W), bq);
+          const uint32_t rd = cl_map(smem_addr(pubdiag + (xs & 1) * W), (int)((cn - p.r0) / p.R));
+          if (lane < wb) {
+            double x, y = 0.0;
+            asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(x) : "r"(ra + 8 * lane) : "memory");
+            if (need_d) asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(y) : "r"(rd + 8 * lane) : "memory");
+            un[lane] = x;
+            if (need_d) dn[lane] = y;
+          }
+        } else if (!own_p) {
+          const unsigned long long* wsl = sl + (size_t)bq * rec;
+          for (int cc = lane; cc < wb; cc += 32) un[cc] = ll_get2_d(wsl + 16 + 2 * cc, flag, PF_POLL_SPINS);
+        } else {
+          for (int cc = lane; cc < wb; cc += 32) un[cc] = tile[(br - rbeg) * LD + cc];
+        }
+        if (!CL && S > 1 && own_p && br != cn && !own_cn) {
+          const unsigned long long* dsl = sl + (size_t)S * rec;
+          for (int cc = lane; cc < wb; cc += 32) dn[cc] = ll_get2_d(dsl + 16 + 2 * cc, flag, PF_POLL_SPINS);
+        }
+      }
+      if (lane == 0) { s_wkey = bk; s_wrow = br; }
+      if (tid == 0) PF_TL(1, jb + jn);
+    };
+    // warp 1: the owner of the next diagonal row publishes it and stages it as dg[jn & 1]
+    auto stage_diag = [&](int jn, long long row) {
+      if (S > 1) publish_diag(jn, row);
+      const double* trow = tile + (row - rbeg) * LD;
+      double* dn = dg + (jn & 1) * W;
+      for (int cc = lane; cc < wb; cc += 32) dn[cc] = trow[cc];
     };
     double ck = -3.0;
     long long cr = LLONG_MAX;
@@ -244,62 +426,29 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         if (key_better(k, rbeg + r, ck, cr)) { ck = k; cr = rbeg + r; }
       }
       cta_best(ck, cr);
-      if (S > 1) {
-        if (warp == 0) publish_cand(0, ck, cr);
-        else if (warp == 1 && cJ >= rbeg && cJ < rend) publish_diag(0, cJ);
+      if (warp == 0) {
+        if (CL && cJ >= rbeg && cJ < rend) stage_diag(0, cJ);
+        if (S > 1) publish_cand(0, ck, cr);
+        gather(0, ck, cr);
+      } else if (!CL && warp == 1 && cJ >= rbeg && cJ < rend) {
+        stage_diag(0, cJ);
       }
+      __syncthreads();
+      ++xs;
     }
+    // Per column j (its winner, row and the old diagonal row are in shared memory):
+    //   pass 1 (all warps): swap-in, scale by division, update column j+1, its pivot candidate
+    //   warp 0: finish the candidate row, publish it, gather the winner of column j+1
+    //   warp 1: finish the next diagonal row, publish and stage it
+    //   warps 1..7: pass 2 (the remaining columns), overlapping the exchange
     for (int j = 0; j < kmax; ++j) {
       const int64_t c = cJ + j;
-      const unsigned flag = epoch + (unsigned)(jb + j);
-      unsigned long long* slots = p.ll + (size_t)(j & 1) * (S + 1) * rec;
+      const double wkey = s_wkey;
+      const long long prow = s_wrow;
       double* ucur = u + (j & 1) * W;
       double* dcur = dg + (j & 1) * W;
       const bool nxt = j + 1 < kmax;
-      const long long last_gather_start = clock64();
-      // C: the winner of column j
-      double wkey;
-      long long prow;
-      int wq;
-      if (S > 1) {
-        double bk = -3.0;
-        long long br = LLONG_MAX;
-        int bq = -1;
-        if (tid < S) {
-          const unsigned long long* sl = mbox + (size_t)(j & 1) * 256 * 256 * 4 + (size_t)q * 256 * 4 + (size_t)tid * 4;
-          unsigned k0, k1, r0_, r1_;
-          bool ok0 = false, ok1 = false;
-          int spins = 0;
-          while (!(ok0 && ok1)) {  // both 16-byte loads in flight together
-            if (!ok0) ok0 = ll_try2(sl, flag, k0, k1);
-            if (!ok1) ok1 = ll_try2(sl + 2, flag, r0_, r1_);
-            if (!(ok0 && ok1) && ++spins > 4) __nanosleep(64);
-          }
-          const double k = __longlong_as_double(((long long)k1 << 32) | k0);
-          if (k > -2.0) { bk = k; br = (long long)r0_ + p.r0; bq = tid; }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-          const long long orr = __shfl_xor_sync(0xffffffffu, br, o);
-          const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
-          if (key_better(ok, orr, bk, br)) { bk = ok; br = orr; bq = oq; }
-        }
-        if (lane == 0) { red2_key[warp] = bk; red2_row[warp] = br; red_q[warp] = bq; }
-        __syncthreads();
-        wkey = red2_key[0];
-        prow = red2_row[0];
-        wq = red_q[0];
-#pragma unroll
-        for (int w2 = 1; w2 < PF_THREADS / 32; ++w2)
-          if (key_better(red2_key[w2], red2_row[w2], wkey, prow)) { wkey = red2_key[w2]; prow = red2_row[w2]; wq = red_q[w2]; }
-      } else {
-        wkey = ck;
-        prow = cr;
-        wq = q;
-        __syncthreads();
-      }
-      if (prof_on && q == 0) p.prof[4096 + jb + j] = clock64() - last_gather_start;
+      if (tid == 0) PF_TL(0, jb + j);
       PF_PROF_MARK(3);
       if (tid == 0) blk_piv[j] = (wkey > 0.0) ? prow : c;
       if (q == 0 && tid == 0) {
@@ -316,33 +465,19 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
             if (key_better(k, rbeg + r, ck, cr)) { ck = k; cr = rbeg + r; }
           }
           cta_best(ck, cr);
-          if (S > 1) {
-            if (warp == 0) publish_cand(j + 1, ck, cr);
-            else if (warp == 1 && c + 1 >= rbeg && c + 1 < rend) publish_diag(j + 1, c + 1);
+          if (warp == 0) {
+            if (CL && c + 1 >= rbeg && c + 1 < rend) stage_diag(j + 1, c + 1);
+            if (S > 1) publish_cand(j + 1, ck, cr);
+            gather(j + 1, ck, cr);
+          } else if (!CL && warp == 1 && c + 1 >= rbeg && c + 1 < rend) {
+            stage_diag(j + 1, c + 1);
           }
+          __syncthreads();
+          ++xs;
         }
         continue;
       }
-      // D: winner row -> ucur; old diagonal row -> dcur (only the owner of the pivot row needs it)
       const bool own_c = c >= rbeg && c < rend;
-      const bool own_p = prow >= rbeg && prow < rend;
-      if (warp == 0) {
-        if (S > 1 && !own_p) {
-          const unsigned long long* wsl = slots + (size_t)wq * rec;
-          for (int cc = lane; cc < wb; cc += 32) ucur[cc] = ll_get2_d(wsl + 16 + 2 * cc, flag);
-        } else {
-          for (int cc = lane; cc < wb; cc += 32) ucur[cc] = tile[(prow - rbeg) * LD + cc];
-        }
-      } else if (warp == 1 && prow != c && own_p) {
-        if (own_c) {
-          for (int cc = lane; cc < wb; cc += 32) dcur[cc] = tile[(c - rbeg) * LD + cc];
-        } else {
-          const unsigned long long* dsl = slots + (size_t)S * rec;
-          for (int cc = lane; cc < wb; cc += 32) dcur[cc] = ll_get2_d(dsl + 16 + 2 * cc, flag);
-        }
-      }
-      __syncthreads();
-      PF_PROF_MARK(4);
       if (own_c && prow != c)
         for (int cc = tid; cc < wb; cc += PF_THREADS) tile[(c - rbeg) * LD + cc] = ucur[cc];
       // pass 1: swap-in, scale by division (_jit.py:180-182), column j+1, next candidate
@@ -350,10 +485,18 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       const double uj1 = (j + 1 < wb) ? ucur[j + 1] : 0.0;
       ck = -3.0;
       cr = LLONG_MAX;
-      for (int64_t r = max((int64_t)0, c + 1 - rbeg) + tid; r < nrows; r += PF_THREADS) {
+      const int64_t p1 = max((int64_t)0, c + 1 - rbeg);  // first row of pass 1
+      if (prow != c && prow >= rbeg + p1 && prow < rend) {
+        // swap-in of the old diagonal row, by the lanes of the warp whose thread owns row prow
+        const int owner = (int)((prow - rbeg - p1) % PF_THREADS);
+        if (warp == owner / 32) {
+          double* tp = tile + (prow - rbeg) * LD;
+          for (int cc = lane; cc < wb; cc += 32) tp[cc] = dcur[cc];
+          __syncwarp();
+        }
+      }
+      for (int64_t r = p1 + tid; r < nrows; r += PF_THREADS) {
         double* tr = tile + r * LD;
-        if (rbeg + r == prow)
-          for (int cc = 0; cc < wb; ++cc) tr[cc] = dcur[cc];
         const double l = __ddiv_rn(tr[j], pivot);
         tr[j] = l;
         if (j + 1 < wb) {
@@ -367,33 +510,40 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       }
       if (nxt) cta_best(ck, cr);
       PF_PROF_MARK(1);
-      // publish the next column's candidate and diagonal rows (S > 1): their remaining columns are
-      // finished here by warps 0 / 1 and skipped by pass 2
-      const bool special = S > 1 && nxt;
-      const bool cand_own = special && ck > -2.0;                 // cr is one of this CTA's rows
-      const bool diag_own = special && c + 1 >= rbeg && c + 1 < rend;
-      if (special) {
-        auto finish_row = [&](long long row) {
-          double* tr = tile + (row - rbeg) * LD;
-          const double l = tr[j];
-          for (int cc = j + 2 + lane; cc < wb; cc += 32) tr[cc] = sub_mul_exact(tr[cc], l, ucur[cc]);
-          __syncwarp();
-        };
-        if (warp == 0 && cand_own) {
-          finish_row(cr);
-          publish_cand(j + 1, ck, cr);
-          if (diag_own && cr == c + 1) publish_diag(j + 1, c + 1);
-        } else if (warp == 0) {
-          publish_cand(j + 1, ck, cr);
-        } else if (warp == 1 && diag_own && !(cand_own && cr == c + 1)) {
+      // the next column's candidate and diagonal rows are finished here by warps 0 / 1 and skipped
+      // by pass 2
+      const bool cand_own = nxt && ck > -2.0;  // cr is one of this CTA's rows
+      const bool diag_own = nxt && c + 1 >= rbeg && c + 1 < rend;
+      auto finish_row = [&](long long row) {
+        double* tr = tile + (row - rbeg) * LD;
+        const double l = tr[j];
+        for (int cc = j + 2 + lane; cc < wb; cc += 32) tr[cc] = sub_mul_exact(tr[cc], l, ucur[cc]);
+        __syncwarp();
+      };
+      if (nxt) {
+        if (warp == 0) {
+          if (cand_own) finish_row(cr);
+          if (CL && diag_own) {  // cluster: warp 0 also finishes and publishes the diagonal row
+            if (!(cand_own && cr == c + 1)) finish_row(c + 1);
+            stage_diag(j + 1, c + 1);
+          }
+          if (S > 1) {
+            publish_cand(j + 1, ck, cr);
+            if (!CL && diag_own && cand_own && cr == c + 1) publish_diag(j + 1, c + 1);
+          }
+          if (lane == 0) PF_TL(2, jb + j + 1);
+          PF_PROF_MARK(2);
+          gather(j + 1, ck, cr);
+          PF_PROF_MARK(4);
+        } else if (!CL && warp == 1 && diag_own && !(cand_own && cr == c + 1)) {
           finish_row(c + 1);
-          publish_diag(j + 1, c + 1);
+          stage_diag(j + 1, c + 1);
         }
       }
-      PF_PROF_MARK(2);
-      // pass 2: remaining columns (mul then sub, _jit.py:183-186)
-      if (j + 2 < wb) {
-        for (int64_t r = max((int64_t)0, c + 1 - rbeg) + tid; r < nrows; r += PF_THREADS) {
+      // pass 2 (warps 1..7): remaining columns (mul then sub, _jit.py:183-186)
+      if (j + 2 < wb && warp > 0) {
+        constexpr int NT2 = PF_THREADS - 32;
+        for (int64_t r = max((int64_t)0, c + 1 - rbeg) + (tid - 32); r < nrows; r += NT2) {
           const long long gr = rbeg + r;
           if ((cand_own && gr == cr) || (diag_own && gr == c + 1)) continue;
           double* tr = tile + r * LD;
@@ -401,11 +551,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           for (int cc = j + 2; cc < wb; ++cc) tr[cc] = sub_mul_exact(tr[cc], l, ucur[cc]);
         }
       }
+      __syncthreads();
       PF_PROF_MARK(5);
+      if (tid == 0) PF_TL(3, jb + j);
       // periodic re-alignment: once CTAs drift apart by a column, early arrivals spin on lines the
-      // late ones still have to write and the skew sustains itself (measured ~5 us per column)
-      if (g_resync > 0 && nxt && ((j + 1) % g_resync) == 0)
-        ll_grid_sync(sync_words, S, q, epoch + (unsigned)w + 4u * (unsigned)((w + W - 1) / W) + 16u + (unsigned)(jb + j));
+      // late ones still have to write and the skew sustains itself
+      if (nxt) ++xs;
+      if (!CL && g_resync > 0 && nxt && ((j + 1) % g_resync) == 0)
+        ll_grid_align(sync_words, S, q, sync_flag());
     }
     __syncthreads();
     // ---------------- 3. write back own rows >= cJ of the block
@@ -416,7 +569,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         if (cc < wb) p.a[(rbeg + r) * p.lda + p.col0 + jb + cc] = tile[r * LD + cc];
       }
     }
-    const unsigned sflag = epoch + (unsigned)w + 2u * (unsigned)(jb / W);
     __syncthreads();  // blk_piv complete; no grid sync needed: the swaps below touch only columns
                       // outside this block, which no CTA reads or writes during the leaf
     PF_PROF_MARK(6);
@@ -483,7 +635,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         __syncthreads();
       }
     }
-    ll_grid_sync(sync_words, S, q, sflag + 1u);
+    if constexpr (CL) cl_sync();
+    else ll_grid_sync(sync_words, S, q, sync_flag());
     PF_PROF_MARK(7);
     // ---------------- 5. U_J = L_JJ^-1 A[J rows, right] and the block update of own rows
     const int right0 = jb + wb;
@@ -580,12 +733,16 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     }
     // re-align the CTAs before the next leaf: they leave the update at different times, and a
     // skewed start makes early CTAs spin on lines that late CTAs still have to write
-    if (jb + W < w) ll_grid_sync(sync_words, S, q, epoch + (unsigned)w + 2u * (unsigned)((w + W - 1) / W) + 8u + (unsigned)(jb / W));
+    if (jb + W < w) {
+      if constexpr (CL) cl_sync();
+      else ll_grid_sync(sync_words, S, q, sync_flag());
+    }
     __syncthreads();
     PF_PROF_MARK(9);
   }
   if (pend_kb > 0) {  // only reachable if the last block had a right part (it never does)
-    ll_grid_sync(sync_words, S, q, epoch + (unsigned)w + 2u * (unsigned)((w + W - 1) / W) + 4u);
+    if constexpr (CL) cl_sync();
+    else ll_grid_sync(sync_words, S, q, sync_flag());
     for (int idx = tid; idx < pend_kb * pend_nright; idx += PF_THREADS) {
       const int i = idx / pend_nright, col = idx - i * pend_nright;
       const int64_t r = pend_cJ + i;
@@ -595,7 +752,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   if (prof_on)
     for (int i = 0; i < 10; ++i) p.prof[q * 16 + i] += prof_acc[i];
   // advance the flag base for the next launch (all CTAs read it at their start)
-  if (q == 0 && tid == 0) atomicAdd(p.epoch, (unsigned)(2 * w + 4 * ((w + W - 1) / W) + 32));
+  if constexpr (CL) {
+    cl_sync();  // no CTA may exit while peers can still push into its shared memory
+  } else {
+    if (q == 0 && tid == 0) atomicAdd(p.epoch, (unsigned)(2 * w + 4 * ((w + W - 1) / W) + 32));
+  }
 }
 
 }  // namespace pflu

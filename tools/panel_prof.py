@@ -13,10 +13,13 @@ w = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 ctas = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 leaf = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 exact = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+import os
+if os.environ.get("PFLU_LIB_PATH"):
+    _lib.LIB_PATH = os.environ["PFLU_LIB_PATH"]
 L = _lib.load()
 L.pflu_debug_panel_profile.argtypes = [ctypes.c_void_p]
 dev = torch.device("cuda:0")
-prof = torch.zeros(16384 + 32 * 256, dtype=torch.int64, device=dev)
+prof = torch.zeros(8192 + 256 * 64 * 4, dtype=torch.int64, device=dev)
 x0 = torch.rand(m, w, dtype=torch.float64, device=dev) * 2 - 1
 x = x0.clone()
 piv = torch.zeros(w, dtype=torch.int64, device=dev)
@@ -55,6 +58,20 @@ for jj in range(3):
           f"gather done {float(got.min() - t0) / 1e3:.2f}..{float(got.max() - t0) / 1e3:.2f} us after first publish")
 
 G = prof.cpu()[4096:4096 + w].double() / 1965.0
-print("   per-column gather us (CTA 0):", " ".join(f"{x:.1f}" for x in G.tolist()[:64]))
+
 print(f"   gather us: mean {G.mean():.2f} median {G.median():.2f} max {G.max():.1f}")
 
+
+# cross-CTA timeline (globaltimer ns) for the first 64 columns
+TL = prof.cpu()[8192:8192 + nz * 64 * 4].view(nz, 64, 4).double()
+print("   timeline per column (us): pub_last-pub_first | gather_first-pub_last | gather_last-pub_last | pass2 end(CTA mean)-pub")
+for col in range(2, min(w, 40)):
+    pub = TL[:, col, 2]
+    gat = TL[:, col, 1]
+    p2 = TL[:, col - 1, 3]
+    st = TL[:, col, 0]
+    if (pub == 0).any() or (gat == 0).any():
+        continue
+    pl = pub.max()
+    print(f"   col {col:3d}: pub spread {float(pub.max() - pub.min()) / 1e3:5.2f}  gather {float(gat.min() - pl) / 1e3:5.2f}..{float(gat.max() - pl) / 1e3:5.2f}"
+          f"  pass2 end {float(p2.mean() - pl) / 1e3:5.2f} (max {float(p2.max() - pl) / 1e3:5.2f})  start-after-pass2 {float((st - p2).mean()) / 1e3:5.2f}  last pub CTA {int(pub.argmax())}")
