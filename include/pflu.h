@@ -43,9 +43,11 @@ extern "C" {
 typedef struct pflu_options {
   int exact;        /* 1: every update in the reference's rounding (multiply, round, subtract):
                        results are bitwise equal to the reference; 0: trailing GEMM on DMMA */
-  int panel_ctas;   /* CTAs of the cooperative panel leaf (0 = automatic) */
+  int panel_ctas;   /* CTAs of the panel kernel (0 = automatic; at most 16 for the cluster kernel) */
   int leaf_width;   /* leaf columns: 8, 16 or 32 (0 = automatic) */
-  int reserved[5];
+  int panel_kernel; /* 0 automatic, 1 cooperative grid (LL exchange through L2), 2 one thread-block
+                       cluster (DSMEM exchange; PFLU_ERR_UNSUPPORTED if the panel does not fit) */
+  int reserved[4];
 } pflu_options;
 
 /* Trace record, one per timed task (labels as the reference's TraceEvent, factor.py:104-122). */

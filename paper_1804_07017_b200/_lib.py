@@ -30,7 +30,7 @@ EXPORTS = (
 
 class Options(ctypes.Structure):
     _fields_ = [("exact", ctypes.c_int), ("panel_ctas", ctypes.c_int),
-                ("leaf_width", ctypes.c_int), ("reserved", ctypes.c_int * 5)]
+                ("leaf_width", ctypes.c_int), ("panel_kernel", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
 
 
 class TraceEvent(ctypes.Structure):
@@ -108,10 +108,14 @@ def check(rc: int, what: str) -> None:
     raise RuntimeError(f"{what} failed (code {rc}): {msg}")
 
 
-def options(exact: bool = False, panel_ctas: int = 0, leaf_width: int = 0) -> Options:
+PANEL_AUTO, PANEL_GRID, PANEL_CLUSTER = 0, 1, 2
+
+
+def options(exact: bool = False, panel_ctas: int = 0, leaf_width: int = 0, panel_kernel: int = PANEL_AUTO) -> Options:
     o = Options()
     load().pflu_default_options(ctypes.byref(o))
     o.exact = 1 if exact else 0
     o.panel_ctas = int(panel_ctas)
     o.leaf_width = int(leaf_width)
+    o.panel_kernel = int(panel_kernel)
     return o

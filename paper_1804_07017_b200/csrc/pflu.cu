@@ -423,8 +423,10 @@ static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0
   p.prof = g_prof;
   p.resync = g_resync;
   // one thread-block cluster (DSMEM exchange) when the rows fit its CTAs' shared memory
-  if (g_cluster > 0 && rows <= g_cl_rows) {
-    const int Smax = std::max(1, std::min(g_cluster, PF_CL_MAX));
+  const bool want_cl = opt.panel_kernel == 2 || (opt.panel_kernel == 0 && g_cluster > 0 && rows <= g_cl_rows);
+  if (want_cl) {
+    const int Smax = opt.panel_ctas > 0 ? std::min(opt.panel_ctas, PF_CL_MAX)
+                                        : std::max(1, std::min(g_cluster > 0 ? g_cluster : PF_CL_MAX, PF_CL_MAX));
     for (int wi = 0; wi < 3; ++wi) {
       const int W = Ws[wi];
       if (W > Wpref) continue;
@@ -454,6 +456,9 @@ static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return PFLU_OK;
     }
+    if (opt.panel_kernel == 2)
+      return set_err(PFLU_ERR_UNSUPPORTED, "panel of %lld rows x %lld does not fit one thread-block cluster",
+                     (long long)rows, (long long)w);
   }
   for (int wi = 0; wi < 3; ++wi) {
     const int W = Ws[wi];

@@ -20,12 +20,15 @@
 // Exactness: every element still receives its updates in ascending pivot order, scaled by
 // division, so exact mode is bitwise equal to lu_unb_run on the panel.
 #pragma once
+#include <type_traits>
+
 #include "pflu_kernels.cuh"
 
 namespace pflu {
 
 constexpr int PF_THREADS = 256;
 constexpr int PF_UCH = 64;  // right-columns chunk of the block update
+constexpr int PF_WB = 32;   // super-block width of the two-level in-panel update
 constexpr size_t PF_MBOX_OFFSET = 2 * 257 * 80 + 512;  // words; after slots + sync words
 constexpr size_t PF_SBOX_OFFSET = PF_MBOX_OFFSET + 2 * 256 * 256 * 4;  // grid-sync mailboxes
 constexpr size_t PF_LL_WORDS = PF_SBOX_OFFSET + 256 * 256 * 2;
@@ -189,11 +192,15 @@ __device__ __forceinline__ void cl_sync() {
 template <int W>
 struct PanelSmem {
   static constexpr int LD = W + 1;
+  static constexpr int KM = W > PF_WB ? W : PF_WB;
+  __host__ __device__ static int64_t ubuf_doubles(int w) {  // U of a leaf block (W x rest) or of a super-block (PF_WB x rest)
+    const int64_t a = (int64_t)W * (w > W ? w - W : 8), b = (int64_t)PF_WB * (w - PF_WB > 8 ? w - PF_WB : 8);
+    return a > b ? a : b;
+  }
   static size_t bytes(int64_t R, int w, bool cl = false) {
-    // tile R x LD, U buffer W x (w - W) (>= W x 8), L_JJ W x W, u / dg W each, plan 4W ints
+    // tile R x LD, U buffer, L block KM x KM, u / dg W each, plan 4W ints
     // (+ cluster mode: keys [2][PF_CL_MAX][2], published rows [2][W] x 2, 2 mbarriers, alignment)
-    const int64_t nright = w > W ? w - W : 8;
-    return (size_t)(R * LD + (int64_t)W * nright + W * W + 4 * W) * 8 + 4 * W * 8 + 256 +
+    return (size_t)(R * LD + ubuf_doubles(w) + KM * KM + 4 * W) * 8 + 4 * W * 8 + 256 +
            (cl ? (size_t)(4 * PF_CL_MAX + 4 * W + 2 + 2) * 8 : 0);
   }
 };
@@ -215,9 +222,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   const int w = p.w;
   const int nright_max = w > W ? w - W : 8;
   double* tile = pf_smem;                                 // [R][LD]
-  double* ubuf = tile + p.R * LD;                         // [W][nright_max]  U_J (solved)
-  double* ljj = ubuf + (int64_t)W * nright_max;           // [W][W]
-  double* u = ljj + W * W;                                // [2][W] pivot row (double-buffered)
+  double* ubuf = tile + p.R * LD;                         // U (solved), ubuf_doubles(w)
+  double* ljj = ubuf + PanelSmem<W>::ubuf_doubles(w);     // [KM][KM] unit-lower L block
+  double* u = ljj + PanelSmem<W>::KM * PanelSmem<W>::KM;  // [2][W] pivot row (double-buffered)
   double* dg = u + 2 * W;                                 // [2][W] old diagonal row
   long long* plan_row = reinterpret_cast<long long*>(dg + 2 * W);  // [2W] slot -> destination row
   long long* plan_src_row = plan_row + 2 * W;                       // [2W] slot -> source row
@@ -638,43 +645,50 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     if constexpr (CL) cl_sync();
     else ll_grid_sync(sync_words, S, q, sync_flag());
     PF_PROF_MARK(7);
-    // ---------------- 5. U_J = L_JJ^-1 A[J rows, right] and the block update of own rows
-    const int right0 = jb + wb;
-    const int nright = w - right0;
-    if (nright > 0 && kb > 0) {
-      for (int idx = tid; idx < W * W; idx += PF_THREADS) {
-        const int r = idx / W, cc = idx - r * W;
-        ljj[idx] = (r < kb && cc < kb) ? p.a[(cJ + r) * p.lda + p.col0 + jb + cc] : 0.0;
+    // ---------------- 5. U = L^-1 A[pivot rows, target columns], then the update of own rows below.
+    // Two levels: every leaf block updates (K = W) only the rest of its PF_WB-wide super-block;
+    // the last block of a super-block then applies the whole super-block (K = PF_WB, L streamed
+    // from global memory) to the panel columns beyond it.  Each element still receives its
+    // updates in ascending k (exact mode stays bitwise equal to the unblocked order).
+    auto solve_update = [&](auto kconst, int64_t crow0, int kcnt, int kcol0, int c_lo, int ncols, bool a_tile) {
+      constexpr int K = decltype(kconst)::value;
+      for (int idx = tid; idx < K * K; idx += PF_THREADS) {
+        const int r = idx / K, cc = idx - r * K;
+        ljj[idx] = (r < kcnt && cc < kcnt) ? p.a[(crow0 + r) * p.lda + p.col0 + kcol0 + cc] : 0.0;
       }
       __syncthreads();
-      for (int col = tid; col < nright; col += PF_THREADS) {
-        double x[W];
+      for (int col = tid; col < ncols; col += PF_THREADS) {
+        double x[K];
 #pragma unroll
-        for (int i = 0; i < W; ++i) x[i] = (i < kb) ? p.a[(cJ + i) * p.lda + p.col0 + right0 + col] : 0.0;
+        for (int i = 0; i < K; ++i) x[i] = (i < kcnt) ? p.a[(crow0 + i) * p.lda + p.col0 + c_lo + col] : 0.0;
 #pragma unroll
-        for (int i = 0; i < W; ++i) {
+        for (int i = 0; i < K; ++i) {
 #pragma unroll
-          for (int r = i + 1; r < W; ++r) x[r] = sub_mul_exact(x[r], ljj[r * W + i], x[i]);
+          for (int r = i + 1; r < K; ++r) x[r] = sub_mul_exact(x[r], ljj[r * K + i], x[i]);
         }
 #pragma unroll
-        for (int i = 0; i < W; ++i) ubuf[i * nright + col] = x[i];
+        for (int i = 0; i < K; ++i) ubuf[i * ncols + col] = x[i];
       }
       __syncthreads();
       PF_PROF_MARK(8);
       // the owner of the U rows writes them back only after the NEXT grid sync: other CTAs may still
       // be reading the raw rows for their own (redundant) solve
-      pend_kb = kb; pend_cJ = cJ; pend_nright = nright; pend_right0 = right0;
-      // rows below the block: A[r, right] -= L[r, J] * U_J
-      const int64_t ub = max(rbeg, cJ + kb);
+      pend_kb = kcnt; pend_cJ = crow0; pend_nright = ncols; pend_right0 = c_lo;
+      // own rows below the pivot rows: A[r, cols] -= L[r, k-block] * U
+      const int64_t ub = max(rbeg, crow0 + kcnt);
       const int nupd = (int)max((int64_t)0, rend - ub);
       const int toff = (int)(ub - rbeg);
+      auto lval = [&](int rl, int k) -> double {
+        if (a_tile) return tile[(int64_t)(toff + rl) * LD + k];
+        return k < kcnt ? p.a[(ub + rl) * p.lda + p.col0 + kcol0 + k] : 0.0;
+      };
       if (!exact) {
         // DMMA: a warp tile is 4 row groups (32 rows) x 64 columns, so 64 C values per thread are in
-        // flight before the first MMA; K = W (zero padded)
+        // flight before the first MMA; K zero padded
         constexpr int GR = 4;
         const int ngroups = (nupd + 7) / 8;
         const int ntr = (ngroups + GR - 1) / GR;      // 32-row tiles
-        const int nch = (nright + PF_UCH - 1) / PF_UCH;
+        const int nch = (ncols + PF_UCH - 1) / PF_UCH;
         const int g = lane >> 2, t = lane & 3;
         for (int wt = warp; wt < ntr * nch; wt += PF_THREADS / 32) {
           const int tr_ = wt / nch, c0 = (wt - tr_ * nch) * PF_UCH;
@@ -683,26 +697,26 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           for (int gg = 0; gg < GR; ++gg) {
             const int rl = (tr_ * GR + gg) * 8 + g;
             const bool rok = rl < nupd;
-            const double* crow = p.a + (ub + rl) * p.lda + p.col0 + right0;
+            const double* crow = p.a + (ub + rl) * p.lda + p.col0 + c_lo;
 #pragma unroll
             for (int nb = 0; nb < 8; ++nb) {
               const int col = c0 + nb * 8 + 2 * t;
-              acc[gg][nb][0] = (rok && col < nright) ? crow[col] : 0.0;
-              acc[gg][nb][1] = (rok && col + 1 < nright) ? crow[col + 1] : 0.0;
+              acc[gg][nb][0] = (rok && col < ncols) ? crow[col] : 0.0;
+              acc[gg][nb][1] = (rok && col + 1 < ncols) ? crow[col + 1] : 0.0;
             }
           }
 #pragma unroll
-          for (int k4 = 0; k4 < W; k4 += 4) {
+          for (int k4 = 0; k4 < K; k4 += 4) {
             double bv[8];
 #pragma unroll
             for (int nb = 0; nb < 8; ++nb) {
               const int col = c0 + nb * 8 + g;
-              bv[nb] = (col < nright) ? -ubuf[(k4 + t) * nright + col] : 0.0;
+              bv[nb] = (col < ncols) ? -ubuf[(k4 + t) * ncols + col] : 0.0;
             }
 #pragma unroll
             for (int gg = 0; gg < GR; ++gg) {
               const int rl = (tr_ * GR + gg) * 8 + g;
-              const double av = rl < nupd ? tile[(int64_t)(toff + rl) * LD + k4 + t] : 0.0;
+              const double av = rl < nupd ? lval(rl, k4 + t) : 0.0;
 #pragma unroll
               for (int nb = 0; nb < 8; ++nb) dmma884(acc[gg][nb][0], acc[gg][nb][1], av, bv[nb]);
             }
@@ -711,24 +725,34 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           for (int gg = 0; gg < GR; ++gg) {
             const int rl = (tr_ * GR + gg) * 8 + g;
             if (rl >= nupd) continue;
-            double* crow = p.a + (ub + rl) * p.lda + p.col0 + right0;
+            double* crow = p.a + (ub + rl) * p.lda + p.col0 + c_lo;
 #pragma unroll
             for (int nb = 0; nb < 8; ++nb) {
               const int col = c0 + nb * 8 + 2 * t;
-              if (col < nright) crow[col] = acc[gg][nb][0];
-              if (col + 1 < nright) crow[col + 1] = acc[gg][nb][1];
+              if (col < ncols) crow[col] = acc[gg][nb][0];
+              if (col + 1 < ncols) crow[col + 1] = acc[gg][nb][1];
             }
           }
         }
       } else {
-        for (int idx = tid; idx < nupd * nright; idx += PF_THREADS) {
-          const int rl = idx / nright, col = idx - rl * nright;
-          double* cp = p.a + (ub + rl) * p.lda + p.col0 + right0 + col;
-          const double* arow = tile + (int64_t)(toff + rl) * LD;
+        for (int idx = tid; idx < nupd * ncols; idx += PF_THREADS) {
+          const int rl = idx / ncols, col = idx - rl * ncols;
+          double* cp = p.a + (ub + rl) * p.lda + p.col0 + c_lo + col;
           double acc = *cp;
-          for (int k = 0; k < kb; ++k) acc = sub_mul_exact(acc, arow[k], ubuf[k * nright + col]);
+          for (int k = 0; k < kcnt; ++k) acc = sub_mul_exact(acc, lval(rl, k), ubuf[k * ncols + col]);
           *cp = acc;
         }
+      }
+    };
+    {
+      const int sbeg = W >= PF_WB ? jb : (jb / PF_WB) * PF_WB;  // super-block of this leaf block
+      const int send = W >= PF_WB ? w : min(w, sbeg + PF_WB);
+      const int right0 = jb + wb;
+      if (send > right0 && kb > 0)
+        solve_update(std::integral_constant<int, W>{}, cJ, kb, jb, right0, send - right0, true);
+      if (W < PF_WB && right0 == send && send < w) {
+        const int kS = (int)min((int64_t)(send - sbeg), p.m - (p.r0 + sbeg));
+        if (kS > 0) solve_update(std::integral_constant<int, PF_WB>{}, p.r0 + sbeg, kS, sbeg, send, w - send, false);
       }
     }
     // re-align the CTAs before the next leaf: they leave the update at different times, and a

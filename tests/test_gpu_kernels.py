@@ -181,7 +181,8 @@ def test_laswp_roundtrip_and_identity(cuda):
 @pytest.mark.parametrize("m,w,ctas,leaf", [(64, 8, 0, 0), (300, 16, 0, 0), (1000, 64, 0, 0), (2048, 128, 3, 0),
                                           (5000, 256, 0, 0), (777, 100, 5, 8), (4096, 256, 16, 16),
                                           (20000, 256, 0, 0), (512, 512, 0, 0), (40, 40, 0, 32)])
-def test_panel_bitwise(cuda, m, w, ctas, leaf):
+@pytest.mark.parametrize("kernel", [1, 2], ids=["grid", "cluster"])
+def test_panel_bitwise(cuda, m, w, ctas, leaf, kernel):
     """Recursive panel + cooperative leaf == lu_unb_run on the panel (exact op order)."""
     import torch
     from paper_1804_07017_b200 import _lib as lb
@@ -192,8 +193,10 @@ def test_panel_bitwise(cuda, m, w, ctas, leaf):
     x = _t(p0, cuda)
     piv = torch.zeros(w, dtype=torch.int64, device=cuda)
     info = ctypes.c_int64(0)
-    opt = lb.options(exact=True, panel_ctas=ctas, leaf_width=leaf)
+    opt = lb.options(exact=True, panel_ctas=ctas if kernel == 1 else min(ctas, 16), leaf_width=leaf, panel_kernel=kernel)
     rc = lb.load().pflu_panel(x.data_ptr(), w, m, 0, 0, w, piv.data_ptr(), ctypes.byref(info), _stream(), ctypes.byref(opt))
+    if kernel == 2 and rc == 3:
+        pytest.skip("panel does not fit one cluster")
     lb.check(rc, "panel")
     assert np.array_equal(piv.cpu().numpy()[: len(wpiv)], wpiv)
     assert info.value == winfo
