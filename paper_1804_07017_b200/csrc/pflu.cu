@@ -68,6 +68,8 @@ struct DevCtx {
   std::vector<cudaStream_t> sC;              // trailing-update column-chunk streams
   int64_t* plans = nullptr;                  // per-step pivot plans
   size_t plans_cap = 0;                      // in int64 words
+  double* dinv = nullptr;                    // per-step inverted 32x32 diagonal blocks of L11 (fast mode)
+  size_t dinv_cap = 0;                       // in doubles
   int64_t* plan[2] = {nullptr, nullptr};
   unsigned long long* info = nullptr;
   unsigned long long* ll = nullptr;  // LL exchange words of the panel kernel
@@ -86,6 +88,7 @@ static int g_leaf = []() { const char* e = getenv("PFLU_LEAF"); return e ? atoi(
 static int g_cluster = []() { const char* e = getenv("PFLU_CLUSTER"); return e ? atoi(e) : 16; }();
 static int g_cl_minrows = []() { const char* e = getenv("PFLU_CL_MINROWS"); return e ? std::max(1, atoi(e)) : 128; }();
 static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
+static int g_trsm_dmma = []() { const char* e = getenv("PFLU_TRSM_DMMA"); return e ? atoi(e) : 1; }();
 static int g_resync = []() { const char* e = getenv("PFLU_PANEL_RESYNC"); return e ? atoi(e) : 4; }();
 static int g_chunks = []() { const char* e = getenv("PFLU_CHUNKS"); return e ? atoi(e) : 1; }();
 static int g_tur_grid = []() { const char* e = getenv("PFLU_TUR_GRID"); return e ? atoi(e) : 0; }();
@@ -206,6 +209,7 @@ static int ctx_get(DevCtx** out) {
         if (cl) CK(cudaFuncSetAttribute(pf_fn(W, cl), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       }
     CK(allow((const void*)swap_trsm_kernel<8>));
+    CK(allow((const void*)swap_trsm_dmma_kernel));
     CK(allow((const void*)swap_trsm_kernel<16>));
     CK(allow((const void*)swap_trsm_kernel<32>));
     CK(allow((const void*)trsm_kernel<8>));
@@ -344,12 +348,23 @@ static int launch_plan(const int64_t* piv, int64_t d, int np, int64_t* plan, cud
   return PFLU_OK;
 }
 
-// laswp by plan (+ optional trsm) on storage columns [c0, c1)
+static int launch_diag_inv(const double* L, int64_t ldl, int np, double* inv, cudaStream_t st) {
+  diag_inv_kernel<<<2, 128, 0, st>>>(L, ldl, np, inv);
+  CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return PFLU_OK;
+}
+
+// laswp by plan (+ optional trsm) on storage columns [c0, c1); with `inv` (the inverted diagonal
+// blocks of L, np <= 256) the solve runs on the tensor cores (fast mode)
 static int launch_swap(double* a, int64_t lda, int64_t d, int np, const int64_t* plan, int64_t c0, int64_t c1,
-                       const double* L, int64_t ldl, bool do_trsm, cudaStream_t st) {
+                       const double* L, int64_t ldl, bool do_trsm, cudaStream_t st, const double* inv = nullptr) {
   if (c1 <= c0 || np <= 0) return PFLU_OK;
   const int t = do_trsm ? 1 : 0;
-  if (np <= 256) {
+  if (do_trsm && inv && np <= 256) {
+    swap_trsm_dmma_kernel<<<(unsigned)((c1 - c0 + SD_BN - 1) / SD_BN), 256, SD_SMEM, st>>>(a, lda, d, np, plan, c0, c1,
+                                                                                        L, ldl, inv);
+  } else if (np <= 256) {
     size_t smem = (size_t)(np * 32 + std::max(np * 32, 1024)) * 8;
     swap_trsm_kernel<32><<<(unsigned)((c1 - c0 + 31) / 32), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl, t);
   } else if (np <= 512) {
@@ -508,6 +523,14 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     CK(cudaMalloc(&c.plans, sizeof(int64_t) * c.plans_cap));
   }
   auto plan_of = [&](int k) { return c.plans + plan_words * k; };
+  // fast mode: inverted 32x32 diagonal blocks of each step's L11 for the DMMA solve
+  const bool use_dinv = !exact && g_trsm_dmma && std::min(b, n) <= 256;
+  if (use_dinv && c.dinv_cap < (size_t)8192 * count) {
+    if (c.dinv) CK(cudaFree(c.dinv));
+    c.dinv_cap = (size_t)8192 * count;
+    CK(cudaMalloc(&c.dinv, sizeof(double) * c.dinv_cap));
+  }
+  auto inv_of = [&](int k) { return c.dinv + (size_t)8192 * k; };
   auto update_cols = [&](int k, int64_t lo, int64_t hi, cudaStream_t st, int label) -> int {
     // TU of step k on storage columns [lo, hi): laswp + trsm (fused), then the DMMA update
     if (hi <= lo) return PFLU_OK;
@@ -515,7 +538,8 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     const int np = (int)std::min(s.bw, m - s.col0);
     int t_tu = -1, t_g = -1;
     CKR(tr.begin(label, k, st, &t_tu));
-    CKR(launch_swap(a, lda, s.col0, np, plan_of(k), lo, hi, a + s.col0 * lda + s.col0, lda, true, st));
+    CKR(launch_swap(a, lda, s.col0, np, plan_of(k), lo, hi, a + s.col0 * lda + s.col0, lda, true, st,
+                    use_dinv ? inv_of(k) : nullptr));
     const int64_t below = s.col0 + s.bw;
     if (below < m) {
       if (label != PFLU_TRACE_TU_L)
@@ -540,6 +564,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     CKR(panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, opt, st));
     const int np = (int)std::min(s.bw, m - s.col0);
     CKR(launch_plan(piv, s.col0, np, plan_of(k), st));
+    if (use_dinv) CKR(launch_diag_inv(a + s.col0 * lda + s.col0, lda, np, inv_of(k), st));
     return tr.end(t_pf, st);
   };
 

@@ -304,13 +304,29 @@ __global__ void __launch_bounds__(256) swap_trsm_kernel(double* __restrict__ a, 
   const int ne = (int)plan[0];
   double* X = st_smem;              // [np][TW] new top block
   double* E = st_smem + np * TW;    // [ne][TW] values for extra rows, later the staged L panel
-  for (int i = rl; i < np; i += RL) {
-    const int64_t src = plan[1 + i];
-    X[i * TW + col] = cok ? a[src * lda + gc] : 0.0;
+  // gathers in batches of 8 independent (plan, row) loads per thread
+  constexpr int GB = 8;
+  for (int i0 = rl; i0 < np; i0 += GB * RL) {
+    int64_t src[GB];
+    double v[GB];
+#pragma unroll
+    for (int u = 0; u < GB; ++u) src[u] = i0 + u * RL < np ? plan[1 + i0 + u * RL] : 0;
+#pragma unroll
+    for (int u = 0; u < GB; ++u) v[u] = (cok && i0 + u * RL < np) ? a[src[u] * lda + gc] : 0.0;
+#pragma unroll
+    for (int u = 0; u < GB; ++u)
+      if (i0 + u * RL < np) X[(i0 + u * RL) * TW + col] = v[u];
   }
-  for (int e = rl; e < ne; e += RL) {
-    const int64_t src = plan[1 + np + 2 * e + 1];
-    E[e * TW + col] = cok ? a[src * lda + gc] : 0.0;
+  for (int e0 = rl; e0 < ne; e0 += GB * RL) {
+    int64_t src[GB];
+    double v[GB];
+#pragma unroll
+    for (int u = 0; u < GB; ++u) src[u] = e0 + u * RL < ne ? plan[1 + np + 2 * (e0 + u * RL) + 1] : 0;
+#pragma unroll
+    for (int u = 0; u < GB; ++u) v[u] = (cok && e0 + u * RL < ne) ? a[src[u] * lda + gc] : 0.0;
+#pragma unroll
+    for (int u = 0; u < GB; ++u)
+      if (e0 + u * RL < ne) E[(e0 + u * RL) * TW + col] = v[u];
   }
   __syncthreads();
   if (cok)
@@ -490,6 +506,170 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_exact_kernel(GemmArgs p) {
       if (col < p.N) p.c[row * p.ldc + col] = acc[i][j];
     }
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// Fast-mode (DMMA) laswp + unit-lower solve of the U12 block row, for np <= 256.
+//
+// diag_inv_kernel: the 32x32 diagonal blocks of L11 inverted once per step (one warp per block, lane j:
+// column j by forward substitution).  inv[blk][32][32], row-major, identity-padded past np.
+// swap_trsm_dmma_kernel: one CTA per 32-column strip; X = P * A12 strip (256 x 32) in shared
+// memory, then per 32-row block i:  X_i := inv(L_ii) X_i,  X_{>i} -= L_{>i,i} X_i  -- both on the
+// tensor cores (DMMA 8x8x4), L streamed from L2.  Not bitwise: exact mode keeps swap_trsm_kernel.
+
+constexpr int SD_BN = 32;              // strip width
+constexpr int SD_LDX = SD_BN + 4;      // padded row stride: conflict-free A/B/C fragment access
+constexpr int SD_SMEM = 256 * SD_LDX * 8;
+
+__global__ void __launch_bounds__(128) diag_inv_kernel(const double* __restrict__ L, int64_t ldl, int np,
+                                                       double* __restrict__ inv) {
+  __shared__ double lb[4][32][33];  // grid (2), 4 warps per CTA: one 32x32 block per warp
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int blk = blockIdx.x * 4 + warp; blk * 32 < np; blk += 4 * gridDim.x) {
+    const int r0 = blk * 32, nb = min(32, np - r0);
+    for (int i = 0; i < 32; ++i)
+      lb[warp][i][lane] = (i < nb && lane < nb) ? L[(int64_t)(r0 + i) * ldl + r0 + lane] : 0.0;
+    __syncwarp();
+    // column `lane` of inv(unit lower): x_i = delta_ij - sum_{k<i} L_ik x_k
+    double x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k) s = fma(-lb[warp][i][k], x[k], s);
+      x[i] = s;
+    }
+    double* out = inv + (size_t)blk * 1024;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) out[i * 32 + lane] = x[i];
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(256, 3) swap_trsm_dmma_kernel(double* __restrict__ a, int64_t lda, int64_t d,
+                                                              int np, const int64_t* __restrict__ plan,
+                                                              int64_t c0, int64_t c1,
+                                                              const double* __restrict__ L, int64_t ldl,
+                                                              const double* __restrict__ inv) {
+  extern __shared__ double sd_smem[];
+  double* X = sd_smem;  // [256][SD_LDX]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int col = tid % SD_BN, rl = tid / SD_BN;  // loads: 8 rows per pass
+  constexpr int RL = 256 / SD_BN;
+  const int64_t gc = c0 + (int64_t)blockIdx.x * SD_BN + col;
+  const bool cok = gc < c1;
+  const int ne = (int)plan[0];
+  // ---- laswp by plan: gather the new top block, extra rows staged in registers; fully unrolled
+  // so that all plan and row loads of a thread are in flight together
+  constexpr int EMAX = 256 / RL;
+  {
+    int64_t src[EMAX];
+#pragma unroll
+    for (int it = 0; it < EMAX; ++it) {
+      const int i = rl + it * RL;
+      src[it] = i < np ? plan[1 + i] : 0;
+    }
+    double xv[EMAX];
+#pragma unroll
+    for (int it = 0; it < EMAX; ++it) {
+      const int i = rl + it * RL;
+      xv[it] = (cok && i < np) ? a[src[it] * lda + gc] : 0.0;
+    }
+#pragma unroll
+    for (int it = 0; it < EMAX; ++it) X[(rl + it * RL) * SD_LDX + col] = xv[it];
+  }
+  double ev[EMAX];
+  {
+    int64_t src[EMAX];
+#pragma unroll
+    for (int it = 0; it < EMAX; ++it) {
+      const int e = rl + it * RL;
+      src[it] = e < ne ? plan[1 + np + 2 * e + 1] : 0;
+    }
+#pragma unroll
+    for (int it = 0; it < EMAX; ++it) {
+      const int e = rl + it * RL;
+      ev[it] = (cok && e < ne) ? a[src[it] * lda + gc] : 0.0;
+    }
+  }
+  __syncthreads();  // every original value read before any row is overwritten
+  if (cok) {
+#pragma unroll
+    for (int it = 0; it < EMAX; ++it) {
+      const int e = rl + it * RL;
+      if (e < ne) a[plan[1 + np + 2 * e] * lda + gc] = ev[it];
+    }
+  }
+  // ---- blocked solve on DMMA
+  const int g = lane >> 2, t = lane & 3;
+  const int nblk = (np + 31) / 32;
+  for (int ib = 0; ib < nblk; ++ib) {
+    const int rb = ib * 32;
+    {  // X_i := inv(L_ii) X_i: 16 8x8 output blocks, two per warp
+      const int gg = warp >> 1, nb0 = (warp & 1) * 2;
+      const double* iv = inv + (size_t)ib * 1024 + (gg * 8 + g) * 32;
+      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int k4 = 0; k4 < 32; k4 += 4) {
+        const double av = iv[k4 + t];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884(acc[j][0], acc[j][1], av, X[(rb + k4 + t) * SD_LDX + (nb0 + j) * 8 + g]);
+      }
+      __syncthreads();  // all reads of X_i done
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        double* xr = X + (rb + gg * 8 + g) * SD_LDX + (nb0 + j) * 8 + 2 * t;
+        xr[0] = acc[j][0];
+        xr[1] = acc[j][1];
+      }
+      __syncthreads();
+    }
+    const int below = rb + 32;
+    if (below < np) {  // X_{>i} -= L_{>i,i} X_i: warp w takes 16-row tiles of the rows below
+      constexpr int TG = 2;  // row groups of 8 per warp tile (registers: 3 CTAs per SM)
+      const int ntiles = (np - below + 8 * TG - 1) / (8 * TG);
+      for (int tt = warp; tt < ntiles; tt += 8) {
+        const int r0 = below + tt * 8 * TG;
+        double acc[TG][4][2];
+        double al[TG][8];
+#pragma unroll
+        for (int gg = 0; gg < TG; ++gg) {
+          const int r = r0 + gg * 8 + g;
+          const bool rok = r < np;
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) {
+            acc[gg][nb][0] = X[r * SD_LDX + nb * 8 + 2 * t];
+            acc[gg][nb][1] = X[r * SD_LDX + nb * 8 + 2 * t + 1];
+          }
+          const double* lr = L + (int64_t)r * ldl + rb;
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4) al[gg][k4] = (rok && rb + k4 * 4 + t < np) ? lr[k4 * 4 + t] : 0.0;
+        }
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4) {
+          double bv[4];
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) bv[nb] = -X[(rb + k4 * 4 + t) * SD_LDX + nb * 8 + g];
+#pragma unroll
+          for (int gg = 0; gg < TG; ++gg)
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) dmma884(acc[gg][nb][0], acc[gg][nb][1], al[gg][k4], bv[nb]);
+        }
+#pragma unroll
+        for (int gg = 0; gg < TG; ++gg) {
+          const int r = r0 + gg * 8 + g;
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) {
+            X[r * SD_LDX + nb * 8 + 2 * t] = acc[gg][nb][0];
+            X[r * SD_LDX + nb * 8 + 2 * t + 1] = acc[gg][nb][1];
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (cok)
+    for (int i = rl; i < np; i += RL) a[(d + i) * lda + gc] = X[i * SD_LDX + col];
 }
 
 }  // namespace pflu

@@ -280,9 +280,25 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       __syncthreads();
     }
     // ---------------- 1. load own rows x block columns
-    for (int idx = tid; idx < nrows * W; idx += PF_THREADS) {
-      const int r = idx / W, c = idx - r * W;
-      tile[r * LD + c] = (c < wb) ? p.a[(rbeg + r) * p.lda + p.col0 + jb + c] : 0.0;
+    {
+      // 8 loads in flight per thread (the rows are lda apart: latency, not bandwidth, bound)
+      constexpr int LB = 8;
+      const int tot = nrows * W;
+      for (int base = tid; base < tot; base += LB * PF_THREADS) {
+        double v[LB];
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int idx = base + u * PF_THREADS;
+          const int r = idx / W, cc = idx - r * W;
+          v[u] = (idx < tot && cc < wb) ? p.a[(rbeg + r) * p.lda + p.col0 + jb + cc] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+          const int idx = base + u * PF_THREADS;
+          const int r = idx / W, cc = idx - r * W;
+          if (idx < tot) tile[r * LD + cc] = v[u];
+        }
+      }
     }
     __syncthreads();
     PF_PROF_MARK(0);
@@ -650,8 +666,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     // the last block of a super-block then applies the whole super-block (K = PF_WB, L streamed
     // from global memory) to the panel columns beyond it.  Each element still receives its
     // updates in ascending k (exact mode stays bitwise equal to the unblocked order).
-    auto solve_update = [&](auto kconst, int64_t crow0, int kcnt, int kcol0, int c_lo, int ncols, bool a_tile) {
+    auto solve_update = [&](auto kconst, auto tconst, int64_t crow0, int kcnt, int kcol0, int c_lo, int ncols) {
       constexpr int K = decltype(kconst)::value;
+      constexpr bool a_tile = decltype(tconst)::value;  // L operand from the smem tile (else global)
       for (int idx = tid; idx < K * K; idx += PF_THREADS) {
         const int r = idx / K, cc = idx - r * K;
         ljj[idx] = (r < kcnt && cc < kcnt) ? p.a[(crow0 + r) * p.lda + p.col0 + kcol0 + cc] : 0.0;
@@ -683,9 +700,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         return k < kcnt ? p.a[(ub + rl) * p.lda + p.col0 + kcol0 + k] : 0.0;
       };
       if (!exact) {
-        // DMMA: a warp tile is 4 row groups (32 rows) x 64 columns, so 64 C values per thread are in
-        // flight before the first MMA; K zero padded
-        constexpr int GR = 4;
+        // DMMA: a warp tile is GR row groups x 64 columns; its C values (and, for L from global
+        // memory, its L fragment) are all in flight before the first MMA; K zero padded
+        constexpr int GR = a_tile ? 4 : 2;
         const int ngroups = (nupd + 7) / 8;
         const int ntr = (ngroups + GR - 1) / GR;      // 32-row tiles
         const int nch = (ncols + PF_UCH - 1) / PF_UCH;
@@ -705,6 +722,15 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
               acc[gg][nb][1] = (rok && col + 1 < ncols) ? crow[col + 1] : 0.0;
             }
           }
+          double areg[a_tile ? 1 : GR][a_tile ? 1 : K / 4];
+          if constexpr (!a_tile) {
+#pragma unroll
+            for (int gg = 0; gg < GR; ++gg) {
+              const int rl = (tr_ * GR + gg) * 8 + g;
+#pragma unroll
+              for (int k4 = 0; k4 < K; k4 += 4) areg[gg][k4 / 4] = rl < nupd ? lval(rl, k4 + t) : 0.0;
+            }
+          }
 #pragma unroll
           for (int k4 = 0; k4 < K; k4 += 4) {
             double bv[8];
@@ -716,7 +742,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
 #pragma unroll
             for (int gg = 0; gg < GR; ++gg) {
               const int rl = (tr_ * GR + gg) * 8 + g;
-              const double av = rl < nupd ? lval(rl, k4 + t) : 0.0;
+              double av;
+              if constexpr (a_tile) av = rl < nupd ? lval(rl, k4 + t) : 0.0;
+              else av = areg[gg][k4 / 4];
 #pragma unroll
               for (int nb = 0; nb < 8; ++nb) dmma884(acc[gg][nb][0], acc[gg][nb][1], av, bv[nb]);
             }
@@ -749,10 +777,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       const int send = W >= PF_WB ? w : min(w, sbeg + PF_WB);
       const int right0 = jb + wb;
       if (send > right0 && kb > 0)
-        solve_update(std::integral_constant<int, W>{}, cJ, kb, jb, right0, send - right0, true);
+        solve_update(std::integral_constant<int, W>{}, std::true_type{}, cJ, kb, jb, right0, send - right0);
       if (W < PF_WB && right0 == send && send < w) {
         const int kS = (int)min((int64_t)(send - sbeg), p.m - (p.r0 + sbeg));
-        if (kS > 0) solve_update(std::integral_constant<int, PF_WB>{}, p.r0 + sbeg, kS, sbeg, send, w - send, false);
+        if (kS > 0)
+          solve_update(std::integral_constant<int, PF_WB>{}, std::false_type{}, p.r0 + sbeg, kS, sbeg, send, w - send);
       }
     }
     // re-align the CTAs before the next leaf: they leave the update at different times, and a
