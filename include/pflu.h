@@ -71,11 +71,16 @@ const char* pflu_last_error(void);
 void pflu_default_options(pflu_options* opt);
 int pflu_device_count(void);
 
-/* Whole factorization, HOST buffers: stages H2D, factors, copies factors and pivots back.
- * a: m x n row-major (m >= n >= 1, lda >= n), overwritten with L\U in place.
- * ipiv: int64[n] host.  lookahead: 0 (dmf_mtb order) or 1 (dmf_la, static look-ahead). */
+/* Whole factorization, HOST buffers: stages H2D, factors, and streams every block row back as
+ * soon as it is final (the D2H overlaps the rest of the factorization); pivots follow the last step.
+ * a: m x n row-major (m >= n >= 1, lda >= n), overwritten with L\U in place; pinned memory gives
+ * full PCIe bandwidth.  ipiv: int64[n] host.  lookahead: 0 (dmf_mtb order) or 1 (dmf_la).
+ * The device copy is a grow-only workspace kept for the next call (see pflu_release_workspace). */
 int pflu_getrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
                int64_t* ipiv, int64_t* info, const pflu_options* opt);
+
+/* Frees pflu_getrf's device workspace (synchronizes the device). */
+int pflu_release_workspace(void);
 
 /* Whole factorization, DEVICE buffers on the current device, ordered on `stream`
  * (a cudaStream_t; NULL = legacy default).  d_ipiv: int64[n] device.  Blocks until done and

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -76,6 +77,12 @@ struct DevCtx {
   unsigned* epoch = nullptr;
   std::vector<cudaEvent_t> ev;  // event pool (ordering only)
   std::vector<cudaEvent_t> tev; // timing event pool (tracing)
+  std::vector<cudaEvent_t> rev; // row-final events of pflu_getrf's streamed D2H
+  cudaStream_t sH = nullptr, sD = nullptr;  // pflu_getrf: H2D + factorization / streamed D2H
+  double* hbuf = nullptr;                   // pflu_getrf device copy (grow-only)
+  size_t hbuf_cap = 0;
+  int64_t* hpiv = nullptr;
+  size_t hpiv_cap = 0;
 };
 
 static std::atomic<long long> g_launches{0};
@@ -183,6 +190,8 @@ static int ctx_get(DevCtx** out) {
     CK(cudaStreamCreateWithPriority(&c.sP, cudaStreamNonBlocking, hi));
     CK(cudaStreamCreateWithPriority(&c.sU, cudaStreamNonBlocking, lo));
     CK(cudaStreamCreateWithPriority(&c.sL, cudaStreamNonBlocking, lo));
+    CK(cudaStreamCreateWithPriority(&c.sH, cudaStreamNonBlocking, lo));
+    CK(cudaStreamCreateWithPriority(&c.sD, cudaStreamNonBlocking, lo));
     c.sC.resize(MAX_CHUNKS);
     for (auto& s : c.sC) CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, lo));
     CK(cudaMalloc(&c.plan[0], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
@@ -506,9 +515,22 @@ struct Step {
   int64_t col0, bw;
 };
 
+// Called when rows [r0, r1) of the matrix are final (every later step only touches rows below),
+// after the work on stream `after`; lets pflu_getrf stream results to the host during the run.
+using RowSink = std::function<int(int64_t r0, int64_t r1, cudaStream_t after)>;
+// Host source of the matrix for pflu_getrf (look-ahead 1): the H2D is issued per trailing-update
+// column chunk on the caller's stream, and each chunk's work waits only for its own columns, so
+// the transfer of later columns overlaps the first steps on earlier ones.
+struct HostIn {
+  const double* a;
+  int64_t lda;
+  int chunks;
+};
+static int g_h2d_chunks = []() { const char* e = getenv("PFLU_H2D_CHUNKS"); return e ? atoi(e) : 4; }();
+
 static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
                        int64_t* piv, unsigned long long* info, cudaStream_t user, const pflu_options& opt,
-                       Tracer& tr) {
+                       Tracer& tr, const RowSink* sink = nullptr, const HostIn* hin = nullptr) {
   std::vector<Step> grid;
   for (int64_t col0 = 0; col0 < n; col0 += b) grid.push_back({col0, std::min(b, n - col0)});
   const int count = (int)grid.size();
@@ -574,6 +596,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
       CKR(pf(k, user));
       CKR(left_swaps(k, user));
       CKR(update_cols(k, grid[k].col0 + grid[k].bw, n, user, PFLU_TRACE_TU));
+      if (sink && k + 1 < count) CKR((*sink)(grid[k].col0, grid[k].col0 + grid[k].bw, user));
     }
     return PFLU_OK;
   }
@@ -585,7 +608,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   //                          PF(k+1), plan(k+1)
   //   sC[c]:                 TU_R(k) restricted to chunk c (after PF(k))
   //   sL:                    left swaps(k) on blocks < k (after every reader of L21(k-1) finished)
-  const int nch = std::max(1, std::min({g_chunks, MAX_CHUNKS, count}));
+  const int nch = std::max(1, std::min({hin ? std::max(g_chunks, hin->chunks) : g_chunks, MAX_CHUNKS, count}));
   std::vector<int> chunk_blk(nch + 1);
   for (int ch = 0; ch <= nch; ++ch) chunk_blk[ch] = (int)((int64_t)count * ch / nch);
   auto chunk_of_block = [&](int blk) {
@@ -594,7 +617,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     return ch;
   };
   const size_t nev = 2 + (size_t)count * (nch + 2);
-  CKR(ctx_events(c, nev));
+  CKR(ctx_events(c, nev + nch));
   cudaEvent_t ev_start = c.ev[0];
   auto ev_pf = [&](int k) { return c.ev[2 + (size_t)k * (nch + 2)]; };
   auto ev_tul = [&](int k) { return c.ev[3 + (size_t)k * (nch + 2)]; };
@@ -603,6 +626,17 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   CK(cudaStreamWaitEvent(c.sP, ev_start, 0));
   CK(cudaStreamWaitEvent(c.sL, ev_start, 0));
   for (int ch = 0; ch < nch; ++ch) CK(cudaStreamWaitEvent(c.sC[ch], ev_start, 0));
+  if (hin) {  // per-chunk H2D on `user`, in column order
+    for (int ch = 0; ch < nch; ++ch) {
+      const int64_t lo = (int64_t)chunk_blk[ch] * b, hi = std::min<int64_t>(n, (int64_t)chunk_blk[ch + 1] * b);
+      if (hi > lo)
+        CK(cudaMemcpy2DAsync(a + lo, lda * 8, hin->a + lo, hin->lda * 8, (hi - lo) * 8, m, cudaMemcpyHostToDevice, user));
+      cudaEvent_t e = c.ev[nev + ch];
+      CK(cudaEventRecord(e, user));
+      CK(cudaStreamWaitEvent(c.sC[ch], e, 0));
+      if (ch == 0 || ch == chunk_of_block(std::min(1, count - 1))) CK(cudaStreamWaitEvent(c.sP, e, 0));
+    }
+  }
   CKR(pf(0, c.sP));
   CK(cudaEventRecord(ev_pf(0), c.sP));
   for (int k = 0; k < count; ++k) {
@@ -622,6 +656,8 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
       CK(cudaStreamWaitEvent(c.sL, ev_pf(k), 0));
       for (int ch = 0; ch < nch; ++ch) CK(cudaStreamWaitEvent(c.sL, ev_ck(ch, k - 1), 0));
       CK(cudaStreamWaitEvent(c.sL, ev_tul(k - 1), 0));
+      // block row k-1 is final here: its trailing updates and left swaps are complete
+      if (sink) CKR((*sink)(grid[k - 1].col0, grid[k - 1].col0 + grid[k - 1].bw, c.sL));
       CKR(left_swaps(k, c.sL));
     }
     if (k + 1 < count) {
@@ -719,42 +755,125 @@ int pflu_getrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b,
   return tr.collect(trace, trace_cap, trace_len);
 }
 
+// Host-buffer factorization: H2D, the blocked factorization, and a D2H that streams every block
+// row to the host as soon as it is final (overlapping the rest of the run); the remaining rows and
+// the pivots follow the last step.
+static int getrf_host_impl(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, int64_t* ipiv,
+                           int64_t* info, const pflu_options& opt) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  // device copy (grow-only workspace kept across calls; pflu_release_workspace frees it) with an
+  // even leading dimension (16-byte aligned rows for the vector paths)
+  const int64_t ldd = (n + 1) & ~(int64_t)1;
+  const size_t need = (size_t)m * ldd;
+  if (c->hbuf_cap < need) {
+    if (c->hbuf) CK(cudaFree(c->hbuf));
+    c->hbuf = nullptr;
+    c->hbuf_cap = 0;
+    if (cudaMalloc(&c->hbuf, sizeof(double) * need) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(PFLU_ERR_NOMEM, "cudaMalloc of the %zu-byte device copy failed", sizeof(double) * need);
+    }
+    c->hbuf_cap = need;
+  }
+  if (c->hpiv_cap < (size_t)n) {
+    if (c->hpiv) CK(cudaFree(c->hpiv));
+    c->hpiv = nullptr;
+    c->hpiv_cap = 0;
+    if (cudaMalloc(&c->hpiv, sizeof(int64_t) * n) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(PFLU_ERR_NOMEM, "cudaMalloc pivots failed");
+    }
+    c->hpiv_cap = n;
+  }
+  double* d_a = c->hbuf;
+  int64_t* d_piv = c->hpiv;
+  cudaStream_t st = c->sH, sD = c->sD;
+  static const bool timing = getenv("PFLU_HOST_TIMING") != nullptr;  // developer: split of the call
+  cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr, t3 = nullptr;
+  if (timing) {
+    for (cudaEvent_t* e : {&t0, &t1, &t2, &t3}) CK(cudaEventCreate(e));
+    CK(cudaEventRecord(t0, st));
+  }
+  HostIn hin{a, lda, g_h2d_chunks};
+  const bool chunked_in = lookahead == 1 && g_h2d_chunks > 1;
+  if (!chunked_in && cudaMemcpy2DAsync(d_a, ldd * 8, a, lda * 8, n * 8, m, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return set_err(PFLU_ERR_CUDA, "H2D copy failed");
+  if (timing) CK(cudaEventRecord(t1, st));
+  int64_t sent = 0;
+  size_t nev = 0;
+  auto next_event = [&](cudaEvent_t* e) -> int {
+    while (c->rev.size() <= nev) {
+      cudaEvent_t x;
+      CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+      c->rev.push_back(x);
+    }
+    *e = c->rev[nev++];
+    return PFLU_OK;
+  };
+  RowSink sink = [&](int64_t r0, int64_t r1, cudaStream_t after) -> int {
+    if (r0 != sent || r1 <= r0) return PFLU_OK;
+    cudaEvent_t e;
+    CKR(next_event(&e));
+    CK(cudaEventRecord(e, after));
+    CK(cudaStreamWaitEvent(sD, e, 0));
+    CK(cudaMemcpy2DAsync(a + r0 * lda, lda * 8, d_a + r0 * ldd, ldd * 8, n * 8, r1 - r0, cudaMemcpyDeviceToHost, sD));
+    sent = r1;
+    return PFLU_OK;
+  };
+  Tracer tr;
+  tr.c = c;
+  tr.on = false;
+  CKR(getrf_async(*c, d_a, m, n, ldd, std::min(b, n), lookahead, d_piv, c->info, st, opt, tr, &sink,
+                  chunked_in ? &hin : nullptr));
+  if (timing) CK(cudaEventRecord(t2, st));
+  cudaEvent_t e;
+  CKR(next_event(&e));
+  CK(cudaEventRecord(e, st));
+  CK(cudaStreamWaitEvent(sD, e, 0));
+  if (sent < m)
+    CK(cudaMemcpy2DAsync(a + sent * lda, lda * 8, d_a + sent * ldd, ldd * 8, n * 8, m - sent, cudaMemcpyDeviceToHost, sD));
+  CK(cudaMemcpyAsync(ipiv, d_piv, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, sD));
+  CKR(finish_info(*c, st, info));
+  CK(cudaStreamSynchronize(sD));
+  if (timing) {
+    CK(cudaEventRecord(t3, sD));
+    CK(cudaEventSynchronize(t3));
+    float h2d = 0, fac = 0, tail = 0;
+    cudaEventElapsedTime(&h2d, t0, t1);
+    cudaEventElapsedTime(&fac, t1, t2);
+    cudaEventElapsedTime(&tail, t2, t3);
+    fprintf(stderr, "pflu_getrf: H2D %.1f ms, factorization %.1f ms, D2H after the last step %.1f ms\n", h2d, fac, tail);
+    for (cudaEvent_t x : {t0, t1, t2, t3}) cudaEventDestroy(x);
+  }
+  return PFLU_OK;
+}
+
 int pflu_getrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, int64_t* ipiv, int64_t* info,
                const pflu_options* opt) {
   if (!a) return -1;
   CKR(check_dims(m, n, lda, b, lookahead));
   if (!ipiv) return -7;
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  // device copy with an even leading dimension (16-byte aligned rows for the vector paths)
-  const int64_t ldd = (n + 1) & ~(int64_t)1;
-  double* d_a = nullptr;
-  int64_t* d_piv = nullptr;
-  CK(cudaMalloc(&d_a, sizeof(double) * (size_t)m * ldd));
-  if (cudaMalloc(&d_piv, sizeof(int64_t) * (size_t)n) != cudaSuccess) {
-    cudaFree(d_a);
-    return set_err(PFLU_ERR_NOMEM, "cudaMalloc pivots failed");
-  }
-  int rc = PFLU_OK;
-  cudaStream_t st = nullptr;
-  do {
-    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) { rc = set_err(PFLU_ERR_CUDA, "stream"); break; }
-    if (cudaMemcpy2DAsync(d_a, ldd * 8, a, lda * 8, n * 8, m, cudaMemcpyHostToDevice, st) != cudaSuccess) {
-      rc = set_err(PFLU_ERR_CUDA, "H2D copy failed"); break;
-    }
-    rc = pflu_getrf_device(d_a, m, n, ldd, b, lookahead, d_piv, info, st, opt, nullptr, 0, nullptr);
-    if (rc != PFLU_OK) break;
-    if (cudaMemcpy2DAsync(a, lda * 8, d_a, ldd * 8, n * 8, m, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaMemcpyAsync(ipiv, d_piv, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess) {
-      rc = set_err(PFLU_ERR_CUDA, "D2H copy failed: %s", cudaGetErrorString(cudaGetLastError()));
-      break;
-    }
-  } while (0);
-  if (st) cudaStreamDestroy(st);
-  cudaFree(d_a);
-  cudaFree(d_piv);
+  pflu_options o;
+  pflu_default_options(&o);
+  if (opt) o = *opt;
+  const int rc = getrf_host_impl(a, m, n, lda, b, lookahead, ipiv, info, o);
+  if (rc != PFLU_OK) cudaGetLastError();
   return rc;
+}
+
+int pflu_release_workspace(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  CK(cudaDeviceSynchronize());
+  if (c->hbuf) CK(cudaFree(c->hbuf));
+  if (c->hpiv) CK(cudaFree(c->hpiv));
+  c->hbuf = nullptr;
+  c->hpiv = nullptr;
+  c->hbuf_cap = c->hpiv_cap = 0;
+  return PFLU_OK;
 }
 
 int pflu_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w, int64_t* d_ipiv, int64_t* info,
