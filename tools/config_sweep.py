@@ -1,5 +1,5 @@
 """Throughput of every BASELINE.json config on one B200 (device-resident, CUDA events, best of reps).
-Writes profiles/r01_configs.json."""
+Writes the JSON list to argv[1] (default profiles/r02_configs.json)."""
 import json
 import sys
 import time
@@ -60,4 +60,4 @@ for name, bs, las, reps in plan:
             out.append(rec)
     del a0
     torch.cuda.empty_cache()
-json.dump(out, open("profiles/r01_configs.json", "w"), indent=1)
+json.dump(out, open(sys.argv[1] if len(sys.argv) > 1 else "profiles/r02_configs.json", "w"), indent=1)
