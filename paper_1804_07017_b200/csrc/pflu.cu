@@ -398,6 +398,9 @@ static size_t pf_smem_bytes(int W, int64_t R, int w, bool cl = false) {
   if (W == 16) return PanelSmem<16>::bytes(R, w, cl);
   return PanelSmem<32>::bytes(R, w, cl);
 }
+static int64_t pf_swap_doubles(int W, int w) {
+  return W == 8 ? PanelSmem<8>::swap_doubles(w) : W == 16 ? PanelSmem<16>::swap_doubles(w) : PanelSmem<32>::swap_doubles(w);
+}
 
 // can a cluster of S panel CTAs (W, full shared memory) be resident?  cached per (W, S)
 static int pf_cluster_ok(DevCtx& c, int W, int S, bool* ok) {
@@ -446,6 +449,7 @@ static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0
   p.piv = piv; p.info = info; p.ll = c.ll; p.epoch = c.epoch; p.exact = opt.exact;
   p.prof = g_prof;
   p.resync = g_resync;
+  p.swcap = 0;
   // one thread-block cluster (DSMEM exchange) when the rows fit its CTAs' shared memory
   const bool want_cl = opt.panel_kernel == 2 || (opt.panel_kernel == 0 && g_cluster > 0 && rows <= g_cl_rows);
   if (want_cl) {
@@ -457,8 +461,12 @@ static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0
       const int S0 = (int)std::min<int64_t>(Smax, std::max<int64_t>(1, (rows + g_cl_minrows - 1) / g_cl_minrows));
       const int64_t R = (rows + S0 - 1) / S0;
       const int S = (int)((rows + R - 1) / R);
-      const size_t smem = pf_smem_bytes(W, R, (int)w, true);
+      size_t smem = pf_smem_bytes(W, R, (int)w, true);
       if (smem > smax) continue;
+      // dedicated row-swap staging from the shared memory left over (small panels)
+      const int64_t swcap = std::min<int64_t>(pf_swap_doubles(W, (int)w), (int64_t)(smax - smem) / 8);
+      p.swcap = swcap > 0 ? (int)swcap : 0;
+      smem += (size_t)p.swcap * 8;
       bool ok = false;
       CKR(pf_cluster_ok(c, W, S, &ok));
       if (!ok) continue;

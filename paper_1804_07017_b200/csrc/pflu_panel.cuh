@@ -47,22 +47,12 @@ struct PanelArgs {
   int exact;
   unsigned long long* prof;  // optional: per-phase clock64 totals of CTA 0 (tools/ only)
   int resync;                // re-align all CTAs every `resync` columns (0 = never)
+  int swcap;                 // cluster kernel: doubles of dedicated row-swap staging (0 = use the L block)
 };
 
 // key polling: spin this many misses before backing off with __nanosleep (whose granularity is
 // coarse, ~1 us: a sleep on the critical path costs a column's worth of time)
 constexpr int PF_POLL_SPINS = 64;
-
-__device__ __forceinline__ unsigned long long pf_gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// timeline (tools/panel_prof.py): prof[8192 + ((q * 64) + col) * 4 + event], globaltimer ns
-#define PF_TL(ev, col)                                                                          \
-  do {                                                                                          \
-    if (p.prof != nullptr && (col) < 64) p.prof[8192 + ((size_t)q * 64 + (col)) * 4 + (ev)] = pf_gtime(); \
-  } while (0)
 
 #define PF_PROF_MARK(i)                                              \
   do {                                                              \
@@ -203,6 +193,8 @@ struct PanelSmem {
     return (size_t)(R * LD + ubuf_doubles(w) + KM * KM + 4 * W) * 8 + 4 * W * 8 + 256 +
            (cl ? (size_t)(4 * PF_CL_MAX + 4 * W + 2 + 2) * 8 : 0);
   }
+  // row-swap staging that would make the cluster kernel's deferred swaps a single batch
+  static int64_t swap_doubles(int w) { return (int64_t)2 * W * (w > W ? w - W : 1); }
 };
 
 // CL = false: S co-resident CTAs exchange through LL words in global memory (any S <= 256).
@@ -234,6 +226,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   double* pubrow = xkey + 2 * PF_CL_MAX * 2;  // [2][W]
   double* pubdiag = pubrow + 2 * W;           // [2][W]
   unsigned long long* xbar = reinterpret_cast<unsigned long long*>(pubdiag + 2 * W);  // [2]
+  double* swbuf = reinterpret_cast<double*>(xbar + 2);  // CL: p.swcap doubles (may be 0)
   unsigned xs = 0;  // CL: exchanges so far (uniform over the cluster): buffer xs & 1, phase (xs >> 1) & 1
   if constexpr (CL) {
     if (tid == 0) {
@@ -241,7 +234,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(xbar + i)) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    cl_sync();  // peers may push into this CTA's barriers only once they are initialised
+    if (S > 1) cl_sync();  // peers may push into this CTA's barriers only once they are initialised
+    else __syncthreads();
   }
   __shared__ double red_key[PF_THREADS / 32];
   __shared__ long long red_row[PF_THREADS / 32];
@@ -259,24 +253,37 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   const int g_resync = p.resync;
   const bool prof_on = p.prof != nullptr && tid == 0;
   long long prof_t = clock64();
-  long long prof_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long prof_acc[16] = {};
 
   // grid-sync flags: epoch + w + (running count of syncs in this launch); the sync sequence is the same
   // on every CTA, and the epoch advance below exceeds w + the sync count
   unsigned nsync = 0;
   auto sync_flag = [&]() { return epoch + (unsigned)w + (++nsync); };
+  // grid-wide barrier with release/acquire for global memory: a cluster barrier (its release is a
+  // MEMBAR.GPU, ~2-5 us) only when the cluster has peers; one CTA needs only __syncthreads
+  auto grid_sync = [&]() {
+    if constexpr (CL) {
+      if (S > 1) cl_sync();
+      else __syncthreads();
+    } else {
+      ll_grid_sync(sync_words, S, q, sync_flag());
+    }
+  };
   int pend_kb = 0, pend_nright = 0, pend_right0 = 0;  // U rows awaiting write-back
   int64_t pend_cJ = 0;
+  auto write_pend = [&]() {
+    for (int idx = tid; idx < pend_kb * pend_nright; idx += PF_THREADS) {
+      const int i = idx / pend_nright, col = idx - i * pend_nright;
+      const int64_t r = pend_cJ + i;
+      if (r >= rbeg && r < rend) p.a[r * p.lda + p.col0 + pend_right0 + col] = ubuf[idx];
+    }
+    pend_kb = 0;
+  };
   for (int jb = 0; jb < w; jb += W) {
     const int wb = min(W, w - jb);
     const int64_t cJ = p.r0 + jb;  // diagonal row of the block's first column
-    if (pend_kb > 0) {  // previous block's U rows: every CTA finished reading the raw values
-      for (int idx = tid; idx < pend_kb * pend_nright; idx += PF_THREADS) {
-        const int i = idx / pend_nright, col = idx - i * pend_nright;
-        const int64_t r = pend_cJ + i;
-        if (r >= rbeg && r < rend) p.a[r * p.lda + p.col0 + pend_right0 + col] = ubuf[idx];
-      }
-      pend_kb = 0;
+    if (!CL && pend_kb > 0) {  // previous block's U rows: every CTA finished reading the raw values
+      write_pend();
       __syncthreads();
     }
     // ---------------- 1. load own rows x block columns
@@ -310,8 +317,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     const int kmax = (int)min((int64_t)wb, p.m - cJ);
     auto cta_best = [&](double& bk, long long& br) {
       warp_best(bk, br);
+      PF_PROF_MARK(11);
       if (lane == 0) { red_key[warp] = bk; red_row[warp] = br; }
       __syncthreads();
+      PF_PROF_MARK(12);
       constexpr int NW = PF_THREADS / 32;
       bk = lane < NW ? red_key[lane] : -3.0;
       br = lane < NW ? red_row[lane] : LLONG_MAX;
@@ -432,7 +441,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         }
       }
       if (lane == 0) { s_wkey = bk; s_wrow = br; }
-      if (tid == 0) PF_TL(1, jb + jn);
     };
     // warp 1: the owner of the next diagonal row publishes it and stages it as dg[jn & 1]
     auto stage_diag = [&](int jn, long long row) {
@@ -471,7 +479,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       double* ucur = u + (j & 1) * W;
       double* dcur = dg + (j & 1) * W;
       const bool nxt = j + 1 < kmax;
-      if (tid == 0) PF_TL(0, jb + j);
       PF_PROF_MARK(3);
       if (tid == 0) blk_piv[j] = (wkey > 0.0) ? prow : c;
       if (q == 0 && tid == 0) {
@@ -531,6 +538,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           }
         }
       }
+      PF_PROF_MARK(10);
       if (nxt) cta_best(ck, cr);
       PF_PROF_MARK(1);
       // the next column's candidate and diagonal rows are finished here by warps 0 / 1 and skipped
@@ -554,7 +562,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
             publish_cand(j + 1, ck, cr);
             if (!CL && diag_own && cand_own && cr == c + 1) publish_diag(j + 1, c + 1);
           }
-          if (lane == 0) PF_TL(2, jb + j + 1);
           PF_PROF_MARK(2);
           gather(j + 1, ck, cr);
           PF_PROF_MARK(4);
@@ -576,7 +583,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       }
       __syncthreads();
       PF_PROF_MARK(5);
-      if (tid == 0) PF_TL(3, jb + j);
       // periodic re-alignment: once CTAs drift apart by a column, early arrivals spin on lines the
       // late ones still have to write and the skew sustains itself
       if (nxt) ++xs;
@@ -638,28 +644,58 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       // columns of this CTA (cyclic over the S CTAs), gathered then scattered in batches that
       // fit the U buffer
       const int my_cols = (nother - q + S - 1) / S;
-      double* gbuf = ubuf;  // reuse: [ns][batch]
-      const int batch = max(1, (W * nright_max) / ns);
+      // staging [ns][batch]: the U buffer (grid kernel), or the free L-block buffer (cluster kernel,
+      // whose U buffer may still hold the previous block's U rows)
+      const bool own_buf = CL && p.swcap > PanelSmem<W>::KM * PanelSmem<W>::KM;
+      double* gbuf = CL ? (own_buf ? swbuf : ljj) : ubuf;
+      const int batch = max(1, (CL ? (own_buf ? p.swcap : PanelSmem<W>::KM * PanelSmem<W>::KM) : W * nright_max) / ns);
       for (int cb = 0; cb < my_cols; cb += batch) {
         const int nb_ = min(batch, my_cols - cb);
-        for (int idx = tid; idx < ns * nb_; idx += PF_THREADS) {
-          const int s = idx / nb_, ci = cb + idx - (idx / nb_) * nb_;
-          const int oc = q + ci * S;
-          const int pc = oc < jb ? oc : oc + wb;
-          gbuf[idx] = p.a[plan_src_row[s] * p.lda + p.col0 + pc];
+        // flattened (slot, column) items, 8 loads in flight per thread; the item's slot and column
+        // advance incrementally (one division per batch, none per element)
+        constexpr int GB = 8;
+        const int tot = ns * nb_;
+        const int dq = PF_THREADS / nb_, dr = PF_THREADS - dq * nb_;
+        auto pcol = [&](int ci) {
+          const int oc = q + (cb + ci) * S;
+          return oc < jb ? oc : oc + wb;
+        };
+        auto step = [&](int& s, int& ci) {
+          s += dq;
+          ci += dr;
+          if (ci >= nb_) { ci -= nb_; ++s; }
+        };
+        {
+          int s = tid / nb_, ci = tid - (tid / nb_) * nb_;
+          for (int base = tid; base < tot; base += GB * PF_THREADS) {
+            double v[GB];
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+              const bool ok = base + u * PF_THREADS < tot;
+              v[u] = ok ? p.a[plan_src_row[ok ? s : 0] * p.lda + p.col0 + pcol(ci)] : 0.0;
+              step(s, ci);
+            }
+#pragma unroll
+            for (int u = 0; u < GB; ++u)
+              if (base + u * PF_THREADS < tot) gbuf[base + u * PF_THREADS] = v[u];
+          }
         }
         __syncthreads();
-        for (int idx = tid; idx < ns * nb_; idx += PF_THREADS) {
-          const int s = idx / nb_, ci = cb + idx - (idx / nb_) * nb_;
-          const int oc = q + ci * S;
-          const int pc = oc < jb ? oc : oc + wb;
-          p.a[plan_row[s] * p.lda + p.col0 + pc] = gbuf[idx];
+        {
+          int s = tid / nb_, ci = tid - (tid / nb_) * nb_;
+          for (int idx = tid; idx < tot; idx += PF_THREADS) {
+            p.a[plan_row[s] * p.lda + p.col0 + pcol(ci)] = gbuf[idx];
+            step(s, ci);
+          }
         }
         __syncthreads();
       }
     }
-    if constexpr (CL) cl_sync();
-    else ll_grid_sync(sync_words, S, q, sync_flag());
+    grid_sync();
+    if (CL && pend_kb > 0) {  // the previous block's U rows: every CTA has finished reading the raw values
+      write_pend();
+      __syncthreads();
+    }
     PF_PROF_MARK(7);
     // ---------------- 5. U = L^-1 A[pivot rows, target columns], then the update of own rows below.
     // Two levels: every leaf block updates (K = W) only the rest of its PF_WB-wide super-block;
@@ -784,29 +820,22 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           solve_update(std::integral_constant<int, PF_WB>{}, std::false_type{}, p.r0 + sbeg, kS, sbeg, send, w - send);
       }
     }
-    // re-align the CTAs before the next leaf: they leave the update at different times, and a
-    // skewed start makes early CTAs spin on lines that late CTAs still have to write
-    if (jb + W < w) {
-      if constexpr (CL) cl_sync();
-      else ll_grid_sync(sync_words, S, q, sync_flag());
-    }
+    // grid kernel: re-align the CTAs before the next leaf (they leave the update at different
+    // times, and a skewed start makes early CTAs spin on lines that late CTAs still have to write);
+    // the cluster kernel waits on mbarriers instead of polling and needs no re-alignment
+    if (!CL && jb + W < w) grid_sync();
     __syncthreads();
     PF_PROF_MARK(9);
   }
-  if (pend_kb > 0) {  // only reachable if the last block had a right part (it never does)
-    if constexpr (CL) cl_sync();
-    else ll_grid_sync(sync_words, S, q, sync_flag());
-    for (int idx = tid; idx < pend_kb * pend_nright; idx += PF_THREADS) {
-      const int i = idx / pend_nright, col = idx - i * pend_nright;
-      const int64_t r = pend_cJ + i;
-      if (r >= rbeg && r < rend) p.a[r * p.lda + p.col0 + pend_right0 + col] = ubuf[idx];
-    }
+  if (pend_kb > 0) {  // the last super-block's U rows (cluster kernel: also the last leaf block's)
+    grid_sync();
+    write_pend();
   }
   if (prof_on)
-    for (int i = 0; i < 10; ++i) p.prof[q * 16 + i] += prof_acc[i];
+    for (int i = 0; i < 16; ++i) p.prof[q * 16 + i] += prof_acc[i];
   // advance the flag base for the next launch (all CTAs read it at their start)
   if constexpr (CL) {
-    cl_sync();  // no CTA may exit while peers can still push into its shared memory
+    if (S > 1) cl_sync();  // no CTA may exit while peers can still push into or read its shared memory
   } else {
     if (q == 0 && tid == 0) atomicAdd(p.epoch, (unsigned)(2 * w + 4 * ((w + W - 1) / W) + 32));
   }

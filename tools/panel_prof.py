@@ -7,7 +7,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_1804_07017_b200 import _lib  # noqa: E402
 
-NAMES = ["load", "pass1+reduce", "publish", "gather", "winner", "pass2", "wb+swaps", "sync", "U-trsm", "blk-update"]
+NAMES = ["load", "warp_best#2", "finish+publish", "top(after G)", "gather(w0)", "barrier G", "wb+swaps", "sync", "U-trsm", "blk-update", "pass1 loop", "warp_best#1", "red barrier"]
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 w = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 ctas = int(sys.argv[3]) if len(sys.argv) > 3 else 0
@@ -41,7 +41,7 @@ torch.cuda.synchronize()
 L.pflu_debug_panel_profile(None)
 ms = e0.elapsed_time(e1)
 PP = prof.cpu()[:4096].view(256, 16)
-P = PP[:, :10]
+P = PP[:, :13]
 nz = int((P.sum(1) > 0).sum())
 P = P[:nz].double() / 1965.0
 print(f"panel m={m} w={w} ctas={ctas} W={leaf} exact={exact}: {ms:.3f} ms; {nz} CTAs; phases us (min/mean/max over CTAs):")
@@ -49,29 +49,9 @@ for i, n in enumerate(NAMES):
     col = P[:, i]
     print(f"   {n:12s} {col.min():8.0f} {col.mean():8.0f} {col.max():8.0f}   argmax CTA {int(col.argmax())}")
 
-T = PP[:nz, 10:16].double()
-for jj in range(3):
-    pub = T[:, 2 * jj]
-    got = T[:, 2 * jj + 1]
-    t0 = pub.min()
-    print(f"   col {4 + jj}: publish spread {float(pub.max() - t0) / 1e3:.2f} us (last CTA {int(pub.argmax())}); "
-          f"gather done {float(got.min() - t0) / 1e3:.2f}..{float(got.max() - t0) / 1e3:.2f} us after first publish")
 
 G = prof.cpu()[4096:4096 + w].double() / 1965.0
 
 print(f"   gather us: mean {G.mean():.2f} median {G.median():.2f} max {G.max():.1f}")
 
 
-# cross-CTA timeline (globaltimer ns) for the first 64 columns
-TL = prof.cpu()[8192:8192 + nz * 64 * 4].view(nz, 64, 4).double()
-print("   timeline per column (us): pub_last-pub_first | gather_first-pub_last | gather_last-pub_last | pass2 end(CTA mean)-pub")
-for col in range(2, min(w, 40)):
-    pub = TL[:, col, 2]
-    gat = TL[:, col, 1]
-    p2 = TL[:, col - 1, 3]
-    st = TL[:, col, 0]
-    if (pub == 0).any() or (gat == 0).any():
-        continue
-    pl = pub.max()
-    print(f"   col {col:3d}: pub spread {float(pub.max() - pub.min()) / 1e3:5.2f}  gather {float(gat.min() - pl) / 1e3:5.2f}..{float(gat.max() - pl) / 1e3:5.2f}"
-          f"  pass2 end {float(p2.mean() - pl) / 1e3:5.2f} (max {float(p2.max() - pl) / 1e3:5.2f})  start-after-pass2 {float((st - p2).mean()) / 1e3:5.2f}  last pub CTA {int(pub.argmax())}")
