@@ -118,6 +118,15 @@ int pflu_pivot_plan(const int64_t* d_ipiv, int64_t d, int64_t nb, int64_t* d_pla
 int pflu_swap_trsm_plan(double* d_a, int64_t lda, int64_t d, int64_t nb, const int64_t* d_plan, int64_t c0,
                         int64_t c1, const double* d_l, int64_t ldl, void* stream);
 
+/* Fast-mode solve support (not in the reference's rounding): d_inv (device, ceil(nb/32) * 1024
+ * doubles) := the inverted 32x32 diagonal blocks of unit_lower(L), L = d_l (nb x nb, ld ldl). */
+int pflu_diag_inv(const double* d_l, int64_t ldl, int64_t nb, double* d_inv, void* stream);
+
+/* pflu_swap_trsm_plan with the solve on the DMMA tensor cores, using d_inv from pflu_diag_inv
+ * (nb <= 256; larger nb falls back to the substitution of pflu_swap_trsm_plan). */
+int pflu_swap_trsm_inv(double* d_a, int64_t lda, int64_t d, int64_t nb, const int64_t* d_plan, int64_t c0,
+                       int64_t c1, const double* d_l, int64_t ldl, const double* d_inv, void* stream);
+
 /* Row interchanges: for k = k1 .. k2-1 ascending, swap rows k and d_ipiv[k] on columns [c0, c1). */
 int pflu_laswp(double* d_a, int64_t lda, int64_t c0, int64_t c1, const int64_t* d_ipiv, int64_t k1,
                int64_t k2, void* stream);

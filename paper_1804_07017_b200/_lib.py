@@ -24,7 +24,7 @@ EXPORTS = (
     "pflu_version", "pflu_launch_count", "pflu_last_error", "pflu_default_options", "pflu_device_count",
     "pflu_getrf", "pflu_getrf_device", "pflu_panel", "pflu_laswp", "pflu_swap_trsm",
     "pflu_trsm", "pflu_gemm_update", "pflu_info_reset", "pflu_info_read", "pflu_pivot_plan",
-    "pflu_swap_trsm_plan", "pflu_copy2d", "pflu_release_workspace",
+    "pflu_swap_trsm_plan", "pflu_copy2d", "pflu_release_workspace", "pflu_diag_inv", "pflu_swap_trsm_inv",
 )
 
 
@@ -95,6 +95,10 @@ def load():
         L.pflu_release_workspace.argtypes = []
         L.pflu_swap_trsm_plan.restype = ctypes.c_int
         L.pflu_swap_trsm_plan.argtypes = [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp]
+        L.pflu_diag_inv.restype = ctypes.c_int
+        L.pflu_diag_inv.argtypes = [_vp, _i64, _i64, _vp, _vp]
+        L.pflu_swap_trsm_inv.restype = ctypes.c_int
+        L.pflu_swap_trsm_inv.argtypes = [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _vp]
         _lib = L
         return L
 

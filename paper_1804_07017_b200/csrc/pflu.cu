@@ -963,6 +963,35 @@ int pflu_swap_trsm_plan(double* d_a, int64_t lda, int64_t d, int64_t nb, const i
   return launch_swap(d_a, lda, d, (int)nb, d_plan, c0, c1, d_l, ldl, d_l != nullptr, (cudaStream_t)stream);
 }
 
+int pflu_diag_inv(const double* d_l, int64_t ldl, int64_t nb, double* d_inv, void* stream) {
+  if (!d_l) return -1;
+  if (nb < 1 || nb > PLAN_MAX) return -3;
+  if (ldl < nb) return -2;
+  if (!d_inv) return -4;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  return launch_diag_inv(d_l, ldl, (int)nb, d_inv, (cudaStream_t)stream);
+}
+
+int pflu_swap_trsm_inv(double* d_a, int64_t lda, int64_t d, int64_t nb, const int64_t* d_plan, int64_t c0,
+                       int64_t c1, const double* d_l, int64_t ldl, const double* d_inv, void* stream) {
+  if (!d_a) return -1;
+  if (lda < 1) return -2;
+  if (d < 0) return -3;
+  if (nb < 1 || nb > PLAN_MAX) return -4;
+  if (!d_plan) return -5;
+  if (c0 < 0) return -6;
+  if (c1 < c0 || c1 > lda) return -7;
+  if (!d_l) return -8;
+  if (ldl < nb) return -9;
+  if (!d_inv) return -10;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  return launch_swap(d_a, lda, d, (int)nb, d_plan, c0, c1, d_l, ldl, true, (cudaStream_t)stream, nb <= 256 ? d_inv : nullptr);
+}
+
 int pflu_laswp(double* d_a, int64_t lda, int64_t c0, int64_t c1, const int64_t* d_ipiv, int64_t k1, int64_t k2,
                void* stream) {
   if (!d_a) return -1;

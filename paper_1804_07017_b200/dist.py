@@ -97,11 +97,18 @@ class CudaKernels:
 
     is_cuda = True
 
+    # panels taller than this run on the cooperative-grid panel kernel (more SMs, lower latency);
+    # the panel is on every rank's critical path here, unlike on one GPU where the 16-SM cluster
+    # kernel leaves more SMs to the concurrent trailing update
+    GRID_PANEL_ROWS = 8192
+
     def __init__(self, device: torch.device, exact: bool = False):
         self.L = _lib.load()
         self.device = device
         self.opt = _lib.options(exact=exact)
+        self.opt_grid = _lib.options(exact=exact, panel_kernel=_lib.PANEL_GRID)
         self.exact = exact
+        self.fast_solve = not exact  # U12 solve on DMMA with inverted diagonal blocks
         lo, hi = torch.cuda.Stream.priority_range()
         self.sP = torch.cuda.Stream(device=device, priority=hi)
         self.sU = torch.cuda.Stream(device=device, priority=lo)
@@ -142,18 +149,28 @@ class CudaKernels:
         return int(v.value)
 
     def panel(self, a, m: int, d: int, col: int, w: int, piv):
+        opt = self.opt_grid if m - d > self.GRID_PANEL_ROWS else self.opt
         rc = self.L.pflu_panel(a.data_ptr(), a.stride(0), m, d, col, w, piv.data_ptr(), None, self._st(),
-                               ctypes.byref(self.opt))
+                               ctypes.byref(opt))
         _lib.check(rc, "pflu_panel")
 
     def plan(self, piv, d: int, nb: int, plan):
         _lib.check(self.L.pflu_pivot_plan(piv.data_ptr(), d, nb, plan.data_ptr(), self._st()), "pflu_pivot_plan")
 
-    def swap_trsm(self, a, d: int, nb: int, plan, c0: int, c1: int, l11=None):
+    def diag_inv(self, l11, inv):
+        _lib.check(self.L.pflu_diag_inv(l11.data_ptr(), l11.stride(0), l11.shape[0], inv.data_ptr(), self._st()),
+                   "pflu_diag_inv")
+
+    def swap_trsm(self, a, d: int, nb: int, plan, c0: int, c1: int, l11=None, inv=None):
         if c1 <= c0:
             return
         lp = l11.data_ptr() if l11 is not None else None
         ldl = l11.stride(0) if l11 is not None else nb
+        if inv is not None and l11 is not None:
+            rc = self.L.pflu_swap_trsm_inv(a.data_ptr(), a.stride(0), d, nb, plan.data_ptr(), c0, c1, lp, ldl,
+                                           inv.data_ptr(), self._st())
+            _lib.check(rc, "pflu_swap_trsm_inv")
+            return
         rc = self.L.pflu_swap_trsm_plan(a.data_ptr(), a.stride(0), d, nb, plan.data_ptr(), c0, c1, lp, ldl,
                                         self._st())
         _lib.check(rc, "pflu_swap_trsm_plan")
@@ -192,6 +209,8 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
     pbuf = [torch.empty(n * b, dtype=torch.float64, device=dev) for _ in range(2)]
     ppiv = [torch.empty(b, dtype=torch.int64, device=dev) for _ in range(2)]
     plans = [torch.empty(1 + 3 * b, dtype=torch.int64, device=dev) for _ in range(2)]
+    fast = getattr(kernels, "fast_solve", False) and b <= 256
+    invs = [torch.empty(8 * 1024, dtype=torch.float64, device=dev) for _ in range(2)] if fast else [None, None]
     ev_bc = [kernels.event() for _ in range(2)]
     ev_tu = [kernels.event() for _ in range(2)]
     kernels.begin()
@@ -219,6 +238,8 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
             if r != o:
                 piv[col0: col0 + bw].copy_(ppiv[k % 2][:bw])
         kernels.plan(piv, col0, bw, plans[k % 2])
+        if fast:
+            kernels.diag_inv(buf[:bw, :bw], invs[k % 2])
         return buf
 
     def update(k, buf, c0, c1):
@@ -227,7 +248,10 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
             return
         col0 = k * b
         bw = min(b, n - col0)
-        kernels.swap_trsm(a_loc, col0, bw, plans[k % 2], c0, c1, buf[:bw, :bw])
+        if fast:
+            kernels.swap_trsm(a_loc, col0, bw, plans[k % 2], c0, c1, buf[:bw, :bw], invs[k % 2])
+        else:
+            kernels.swap_trsm(a_loc, col0, bw, plans[k % 2], c0, c1, buf[:bw, :bw])
         if col0 + bw < n:
             kernels.gemm(a_loc[col0 + bw:, c0:c1], buf[bw:, :], a_loc[col0: col0 + bw, c0:c1])
 

@@ -229,3 +229,35 @@ def test_cli_sweep_with_check(cuda, capsys):
     assert len(recs) == 6 and {r.strategy for r in recs} == {"MTB", "LA", "LA_MB"}
     for r in recs:
         assert r.gflops > 0 and 0 < r.residual <= 50      # reference test_factor.py:391-398 bound
+
+
+@pytest.mark.parametrize("nb,ncols,d", [(256, 1000, 0), (256, 37, 300), (100, 300, 5), (33, 64, 0), (512, 40, 0)])
+def test_swap_trsm_inv_matches_substitution(cuda, nb, ncols, d):
+    """Fast-mode U12 solve (inverted 32x32 diagonal blocks + DMMA) == the substitution path up to
+    rounding; pivots from a real partial-pivoting panel so the row interchanges are exercised."""
+    import torch
+
+    m = d + nb + 400
+    rng = np.random.default_rng(nb + ncols + d)
+    panel = rng.uniform(-1, 1, (m - d, nb))
+    lu, piv, _ = oracle.lu_unb(panel.copy())  # |l| <= 1, pivots relative to row d
+    full_piv = np.arange(m, dtype=np.int64)
+    full_piv[d: d + nb] = np.asarray(piv[:nb], dtype=np.int64) + d
+    a0 = rng.uniform(-1, 1, (m, ncols))
+    l11 = _t(np.ascontiguousarray(lu[:nb, :nb]), cuda)
+    L = _lib().load()
+    dpiv = torch.from_numpy(full_piv).to(cuda)
+    plan = torch.empty(1 + 3 * nb, dtype=torch.int64, device=cuda)
+    _lib().check(L.pflu_pivot_plan(dpiv.data_ptr(), d, nb, plan.data_ptr(), _stream()), "plan")
+    inv = torch.empty(((nb + 31) // 32) * 1024, dtype=torch.float64, device=cuda)
+    _lib().check(L.pflu_diag_inv(l11.data_ptr(), nb, nb, inv.data_ptr(), _stream()), "diag_inv")
+    x_sub, x_inv = _t(a0, cuda), _t(a0, cuda)
+    _lib().check(L.pflu_swap_trsm_plan(x_sub.data_ptr(), ncols, d, nb, plan.data_ptr(), 0, ncols, l11.data_ptr(), nb,
+                                       _stream()), "swap_trsm_plan")
+    _lib().check(L.pflu_swap_trsm_inv(x_inv.data_ptr(), ncols, d, nb, plan.data_ptr(), 0, ncols, l11.data_ptr(), nb,
+                                      inv.data_ptr(), _stream()), "swap_trsm_inv")
+    ws, wi = x_sub.cpu().numpy(), x_inv.cpu().numpy()
+    assert np.array_equal(ws[d + nb:], wi[d + nb:])  # rows below the block: swaps only, exact
+    assert np.array_equal(ws[:d], wi[:d])
+    top_s, top_i = ws[d: d + nb], wi[d: d + nb]
+    assert np.abs(top_s - top_i).max() <= 1e-11 * max(1.0, np.abs(top_s).max())
