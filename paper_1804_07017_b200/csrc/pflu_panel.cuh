@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         const uint32_t bar = smem_addr(xbar + (xs & 1));
         if (lane == 0) cl_expect(bar, (unsigned)S * 16u);
         cl_wait(bar, (xs >> 1) & 1u);
+        PF_PROF_MARK(13);
         if (lane < S) {
           const double* kk = xkey + ((xs & 1) * PF_CL_MAX + lane) * 2;
           const double k = kk[0];
@@ -390,6 +391,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           if (k > -2.0) { bk = k; br = rr; }
         }
         bq = warp_best(bk, br);
+        PF_PROF_MARK(14);
       } else if (S > 1) {
         const unsigned long long* mb = mbox + (size_t)(jn & 1) * 256 * 256 * 4 + (size_t)q * 256 * 4;
         for (int t = lane; t < S; t += 32) {
@@ -429,6 +431,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
             un[lane] = x;
             if (need_d) dn[lane] = y;
           }
+          PF_PROF_MARK(15);
         } else if (!own_p) {
           const unsigned long long* wsl = sl + (size_t)bq * rec;
           for (int cc = lane; cc < wb; cc += 32) un[cc] = ll_get2_d(wsl + 16 + 2 * cc, flag, PF_POLL_SPINS);
@@ -551,13 +554,15 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         for (int cc = j + 2 + lane; cc < wb; cc += 32) tr[cc] = sub_mul_exact(tr[cc], l, ucur[cc]);
         __syncwarp();
       };
+      // cluster: the diagonal row is finished and staged by warp 1 in parallel with warp 0's candidate
+      // row; warp 0 waits for it (named barrier 1, 64 threads) before pushing its key, since peers
+      // pull the diagonal row once they have seen every key
+      const bool diag_split = CL && diag_own && !(cand_own && cr == c + 1);
       if (nxt) {
         if (warp == 0) {
           if (cand_own) finish_row(cr);
-          if (CL && diag_own) {  // cluster: warp 0 also finishes and publishes the diagonal row
-            if (!(cand_own && cr == c + 1)) finish_row(c + 1);
-            stage_diag(j + 1, c + 1);
-          }
+          if (CL && diag_own && !diag_split) stage_diag(j + 1, c + 1);  // the candidate is the diagonal row
+          if (diag_split) asm volatile("bar.sync 1, 64;\n" ::: "memory");
           if (S > 1) {
             publish_cand(j + 1, ck, cr);
             if (!CL && diag_own && cand_own && cr == c + 1) publish_diag(j + 1, c + 1);
@@ -565,9 +570,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           PF_PROF_MARK(2);
           gather(j + 1, ck, cr);
           PF_PROF_MARK(4);
-        } else if (!CL && warp == 1 && diag_own && !(cand_own && cr == c + 1)) {
+        } else if (warp == 1 && diag_own && !(cand_own && cr == c + 1)) {
           finish_row(c + 1);
           stage_diag(j + 1, c + 1);
+          if (diag_split) asm volatile("bar.arrive 1, 64;\n" ::: "memory");
         }
       }
       // pass 2 (warps 1..7): remaining columns (mul then sub, _jit.py:183-186)

@@ -371,6 +371,9 @@ def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
     import numpy as np
 
     if not dist.is_initialized():
+        for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"), ("MASTER_ADDR", "127.0.0.1"),
+                     ("MASTER_PORT", "29533")):
+            os.environ.setdefault(k, v)  # plain `python bench.py --dist`: a one-rank group
         dist.init_process_group("nccl")
     P, r = dist.get_world_size(), dist.get_rank()
     local = int(os.environ.get("LOCAL_RANK", r))

@@ -7,7 +7,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_1804_07017_b200 import _lib  # noqa: E402
 
-NAMES = ["load", "warp_best#2", "finish+publish", "top(after G)", "gather(w0)", "barrier G", "wb+swaps", "sync", "U-trsm", "blk-update", "pass1 loop", "warp_best#1", "red barrier"]
+NAMES = ["load", "warp_best#2", "finish+publish", "top(after G)", "gather(w0)", "barrier G", "wb+swaps", "sync", "U-trsm", "blk-update", "pass1 loop", "warp_best#1", "red barrier", "g:wait keys", "g:reduce", "g:pull"]
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 w = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 ctas = int(sys.argv[3]) if len(sys.argv) > 3 else 0
@@ -41,7 +41,7 @@ torch.cuda.synchronize()
 L.pflu_debug_panel_profile(None)
 ms = e0.elapsed_time(e1)
 PP = prof.cpu()[:4096].view(256, 16)
-P = PP[:, :13]
+P = PP[:, :16]
 nz = int((P.sum(1) > 0).sum())
 P = P[:nz].double() / 1965.0
 print(f"panel m={m} w={w} ctas={ctas} W={leaf} exact={exact}: {ms:.3f} ms; {nz} CTAs; phases us (min/mean/max over CTAs):")
