@@ -96,6 +96,7 @@ static int g_cluster = []() { const char* e = getenv("PFLU_CLUSTER"); return e ?
 static int g_cl_minrows = []() { const char* e = getenv("PFLU_CL_MINROWS"); return e ? std::max(1, atoi(e)) : 128; }();
 static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
 static int g_trsm_dmma = []() { const char* e = getenv("PFLU_TRSM_DMMA"); return e ? atoi(e) : 1; }();
+static int64_t g_grid_rows = []() { const char* e = getenv("PFLU_GRID_ROWS"); return e ? atoll(e) : 8192; }();
 static int g_resync = []() { const char* e = getenv("PFLU_PANEL_RESYNC"); return e ? atoi(e) : 4; }();
 static int g_chunks = []() { const char* e = getenv("PFLU_CHUNKS"); return e ? atoi(e) : 1; }();
 static int g_tur_grid = []() { const char* e = getenv("PFLU_TUR_GRID"); return e ? atoi(e) : 0; }();
@@ -315,14 +316,18 @@ static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, con
       case 10: CKR(launch_gemm_p<GV0>(*g_dc, p, v2, 0, st)); break;
       case 11: CKR((launch_gemm_p<GV0, true>(*g_dc, p, v2, 0, st))); break;
       case 13: CKR(launch_gemm_p<GV3>(*g_dc, p, v2, 0, st)); break;
+      case 16: CKR(launch_gemm_p<GV6>(*g_dc, p, v2, 0, st)); break;
+      case 8: CKR(launch_gemm_t<GV8>(p, v2, st)); break;
+      case 40: CKR(launch_gemm_t<GV0>(p, v2, st)); break;
       case 17: CKR(launch_gemm_p<GV7>(*g_dc, p, v2, 0, st)); break;
       case 20: CKR(launch_gemm_p<GV0>(*g_dc, p, v2, g_dc->sms, st)); break;
       case 21: CKR(launch_gemm_p<GV3>(*g_dc, p, v2, g_dc->sms, st)); break;
-      case 0:
+      case 41:  // round-1 depth-0 choice (persistent GV0)
         if (pgrid != 0) CKR(launch_gemm_p<GV0>(*g_dc, p, v2, pgrid > 0 ? pgrid : 0, st));
         else CKR(launch_gemm_t<GV0>(p, v2, st));
         break;
-      default: CKR(launch_gemm_t<GV0>(p, v2, st)); break;
+      case 0:
+      default: CKR(launch_gemm_t<GV6>(p, v2, st)); break;
     }
   }
   CK(cudaGetLastError());
@@ -587,11 +592,16 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     const int np = (int)std::min(s.bw, m - s.col0);
     return launch_swap(a, lda, s.col0, np, plan_of(k), 0, s.col0, nullptr, lda, false, st);
   };
+  // Depth 0 runs each panel alone on the critical path: tall panels take the cooperative-grid kernel
+  // (more SMs, lower latency).  Depth 1 keeps the 16-SM cluster kernel, which leaves the other SMs to
+  // the concurrent trailing update.
   auto pf = [&](int k, cudaStream_t st) -> int {
     const Step s = grid[k];
     int t_pf = -1;
     CKR(tr.begin(PFLU_TRACE_PF, k, st, &t_pf));
-    CKR(panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, opt, st));
+    pflu_options popt = opt;
+    if (lookahead == 0 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;
+    CKR(panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, popt, st));
     const int np = (int)std::min(s.bw, m - s.col0);
     CKR(launch_plan(piv, s.col0, np, plan_of(k), st));
     if (use_dinv) CKR(launch_diag_inv(a + s.col0 * lda + s.col0, lda, np, inv_of(k), st));
