@@ -123,7 +123,7 @@ int pflu_swap_trsm_plan(double* d_a, int64_t lda, int64_t d, int64_t nb, const i
 int pflu_diag_inv(const double* d_l, int64_t ldl, int64_t nb, double* d_inv, void* stream);
 
 /* pflu_swap_trsm_plan with the solve on the DMMA tensor cores, using d_inv from pflu_diag_inv
- * (nb <= 256; larger nb falls back to the substitution of pflu_swap_trsm_plan). */
+ * (nb <= 512; larger nb falls back to the substitution of pflu_swap_trsm_plan). */
 int pflu_swap_trsm_inv(double* d_a, int64_t lda, int64_t d, int64_t nb, const int64_t* d_plan, int64_t c0,
                        int64_t c1, const double* d_l, int64_t ldl, const double* d_inv, void* stream);
 

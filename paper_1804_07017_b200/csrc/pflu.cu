@@ -219,7 +219,8 @@ static int ctx_get(DevCtx** out) {
         if (cl) CK(cudaFuncSetAttribute(pf_fn(W, cl), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       }
     CK(allow((const void*)swap_trsm_kernel<8>));
-    CK(allow((const void*)swap_trsm_dmma_kernel));
+    CK(allow((const void*)swap_trsm_dmma_kernel<256>));
+    CK(allow((const void*)swap_trsm_dmma_kernel<512>));
     CK(allow((const void*)swap_trsm_kernel<16>));
     CK(allow((const void*)swap_trsm_kernel<32>));
     CK(allow((const void*)trsm_kernel<8>));
@@ -376,8 +377,11 @@ static int launch_swap(double* a, int64_t lda, int64_t d, int np, const int64_t*
   if (c1 <= c0 || np <= 0) return PFLU_OK;
   const int t = do_trsm ? 1 : 0;
   if (do_trsm && inv && np <= 256) {
-    swap_trsm_dmma_kernel<<<(unsigned)((c1 - c0 + SD_BN - 1) / SD_BN), 256, SD_SMEM, st>>>(a, lda, d, np, plan, c0, c1,
-                                                                                        L, ldl, inv);
+    swap_trsm_dmma_kernel<256><<<(unsigned)((c1 - c0 + SD_BN - 1) / SD_BN), 256, SdCfg<256>::SMEM, st>>>(
+        a, lda, d, np, plan, c0, c1, L, ldl, inv);
+  } else if (do_trsm && inv && np <= 512) {
+    swap_trsm_dmma_kernel<512><<<(unsigned)((c1 - c0 + SD_BN - 1) / SD_BN), 256, SdCfg<512>::SMEM, st>>>(
+        a, lda, d, np, plan, c0, c1, L, ldl, inv);
   } else if (np <= 256) {
     size_t smem = (size_t)(np * 32 + std::max(np * 32, 1024)) * 8;
     swap_trsm_kernel<32><<<(unsigned)((c1 - c0 + 31) / 32), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl, t);
@@ -559,13 +563,14 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   }
   auto plan_of = [&](int k) { return c.plans + plan_words * k; };
   // fast mode: inverted 32x32 diagonal blocks of each step's L11 for the DMMA solve
-  const bool use_dinv = !exact && g_trsm_dmma && std::min(b, n) <= 256;
-  if (use_dinv && c.dinv_cap < (size_t)8192 * count) {
+  const bool use_dinv = !exact && g_trsm_dmma && std::min(b, n) <= 512;
+  const size_t inv_words = (size_t)1024 * ((std::min(b, n) + 31) / 32);  // one 32x32 block per 32 rows
+  if (use_dinv && c.dinv_cap < inv_words * count) {
     if (c.dinv) CK(cudaFree(c.dinv));
-    c.dinv_cap = (size_t)8192 * count;
+    c.dinv_cap = inv_words * count;
     CK(cudaMalloc(&c.dinv, sizeof(double) * c.dinv_cap));
   }
-  auto inv_of = [&](int k) { return c.dinv + (size_t)8192 * k; };
+  auto inv_of = [&](int k) { return c.dinv + inv_words * k; };
   auto update_cols = [&](int k, int64_t lo, int64_t hi, cudaStream_t st, int label) -> int {
     // TU of step k on storage columns [lo, hi): laswp + trsm (fused), then the DMMA update
     if (hi <= lo) return PFLU_OK;
@@ -999,7 +1004,7 @@ int pflu_swap_trsm_inv(double* d_a, int64_t lda, int64_t d, int64_t nb, const in
   std::lock_guard<std::mutex> lk(g_mu);
   DevCtx* c = nullptr;
   CKR(ctx_get(&c));
-  return launch_swap(d_a, lda, d, (int)nb, d_plan, c0, c1, d_l, ldl, true, (cudaStream_t)stream, nb <= 256 ? d_inv : nullptr);
+  return launch_swap(d_a, lda, d, (int)nb, d_plan, c0, c1, d_l, ldl, true, (cudaStream_t)stream, nb <= 512 ? d_inv : nullptr);
 }
 
 int pflu_laswp(double* d_a, int64_t lda, int64_t c0, int64_t c1, const int64_t* d_ipiv, int64_t k1, int64_t k2,

@@ -519,7 +519,12 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_exact_kernel(GemmArgs p) {
 
 constexpr int SD_BN = 32;              // strip width
 constexpr int SD_LDX = SD_BN + 4;      // padded row stride: conflict-free A/B/C fragment access
-constexpr int SD_SMEM = 256 * SD_LDX * 8;
+template <int NPMAX>
+struct SdCfg {  // NPMAX 256: 74 KB smem, 80 regs, 3 CTAs/SM; 512 (b = 512): 147 KB, 1 CTA/SM
+  static constexpr int SMEM = NPMAX * SD_LDX * 8;
+  static constexpr int MINB = NPMAX <= 256 ? 3 : 1;
+};
+constexpr int SD_SMEM = SdCfg<256>::SMEM;
 
 __global__ void __launch_bounds__(128) diag_inv_kernel(const double* __restrict__ L, int64_t ldl, int np,
                                                        double* __restrict__ inv) {
@@ -546,13 +551,14 @@ __global__ void __launch_bounds__(128) diag_inv_kernel(const double* __restrict_
   }
 }
 
-__global__ void __launch_bounds__(256, 3) swap_trsm_dmma_kernel(double* __restrict__ a, int64_t lda, int64_t d,
+template <int NPMAX>
+__global__ void __launch_bounds__(256, SdCfg<NPMAX>::MINB) swap_trsm_dmma_kernel(double* __restrict__ a, int64_t lda, int64_t d,
                                                               int np, const int64_t* __restrict__ plan,
                                                               int64_t c0, int64_t c1,
                                                               const double* __restrict__ L, int64_t ldl,
                                                               const double* __restrict__ inv) {
   extern __shared__ double sd_smem[];
-  double* X = sd_smem;  // [256][SD_LDX]
+  double* X = sd_smem;  // [NPMAX][SD_LDX]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int col = tid % SD_BN, rl = tid / SD_BN;  // loads: 8 rows per pass
   constexpr int RL = 256 / SD_BN;
@@ -561,7 +567,7 @@ __global__ void __launch_bounds__(256, 3) swap_trsm_dmma_kernel(double* __restri
   const int ne = (int)plan[0];
   // ---- laswp by plan: gather the new top block, extra rows staged in registers; fully unrolled
   // so that all plan and row loads of a thread are in flight together
-  constexpr int EMAX = 256 / RL;
+  constexpr int EMAX = NPMAX / RL;
   {
     int64_t src[EMAX];
 #pragma unroll

@@ -209,8 +209,8 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
     pbuf = [torch.empty(n * b, dtype=torch.float64, device=dev) for _ in range(2)]
     ppiv = [torch.empty(b, dtype=torch.int64, device=dev) for _ in range(2)]
     plans = [torch.empty(1 + 3 * b, dtype=torch.int64, device=dev) for _ in range(2)]
-    fast = getattr(kernels, "fast_solve", False) and b <= 256
-    invs = [torch.empty(8 * 1024, dtype=torch.float64, device=dev) for _ in range(2)] if fast else [None, None]
+    fast = getattr(kernels, "fast_solve", False) and b <= 512
+    invs = [torch.empty(((b + 31) // 32) * 1024, dtype=torch.float64, device=dev) for _ in range(2)] if fast else [None, None]
     ev_bc = [kernels.event() for _ in range(2)]
     ev_tu = [kernels.event() for _ in range(2)]
     kernels.begin()

@@ -231,7 +231,7 @@ def test_cli_sweep_with_check(cuda, capsys):
         assert r.gflops > 0 and 0 < r.residual <= 50      # reference test_factor.py:391-398 bound
 
 
-@pytest.mark.parametrize("nb,ncols,d", [(256, 1000, 0), (256, 37, 300), (100, 300, 5), (33, 64, 0), (512, 40, 0)])
+@pytest.mark.parametrize("nb,ncols,d", [(256, 1000, 0), (256, 37, 300), (100, 300, 5), (33, 64, 0), (512, 40, 0), (512, 700, 3), (300, 200, 0)])
 def test_swap_trsm_inv_matches_substitution(cuda, nb, ncols, d):
     """Fast-mode U12 solve (inverted 32x32 diagonal blocks + DMMA) == the substitution path up to
     rounding; pivots from a real partial-pivoting panel so the row interchanges are exercised."""
