@@ -219,8 +219,8 @@ static int ctx_get(DevCtx** out) {
         if (cl) CK(cudaFuncSetAttribute(pf_fn(W, cl), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       }
     CK(allow((const void*)swap_trsm_kernel<8>));
-    CK(allow((const void*)swap_trsm_dmma_kernel<256>));
-    CK(allow((const void*)swap_trsm_dmma_kernel<512>));
+    CK(allow((const void*)swap_trsm_dmma_kernel<256, 32>));
+    CK(allow((const void*)swap_trsm_dmma_kernel<512, 16>));
     CK(allow((const void*)swap_trsm_kernel<16>));
     CK(allow((const void*)swap_trsm_kernel<32>));
     CK(allow((const void*)trsm_kernel<8>));
@@ -377,10 +377,10 @@ static int launch_swap(double* a, int64_t lda, int64_t d, int np, const int64_t*
   if (c1 <= c0 || np <= 0) return PFLU_OK;
   const int t = do_trsm ? 1 : 0;
   if (do_trsm && inv && np <= 256) {
-    swap_trsm_dmma_kernel<256><<<(unsigned)((c1 - c0 + SD_BN - 1) / SD_BN), 256, SdCfg<256>::SMEM, st>>>(
+    swap_trsm_dmma_kernel<256, 32><<<(unsigned)((c1 - c0 + 31) / 32), 256, SdCfg<256, 32>::SMEM, st>>>(
         a, lda, d, np, plan, c0, c1, L, ldl, inv);
   } else if (do_trsm && inv && np <= 512) {
-    swap_trsm_dmma_kernel<512><<<(unsigned)((c1 - c0 + SD_BN - 1) / SD_BN), 256, SdCfg<512>::SMEM, st>>>(
+    swap_trsm_dmma_kernel<512, 16><<<(unsigned)((c1 - c0 + 15) / 16), 256, SdCfg<512, 16>::SMEM, st>>>(
         a, lda, d, np, plan, c0, c1, L, ldl, inv);
   } else if (np <= 256) {
     size_t smem = (size_t)(np * 32 + std::max(np * 32, 1024)) * 8;

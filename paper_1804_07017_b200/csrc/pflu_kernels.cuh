@@ -517,14 +517,14 @@ __global__ void __launch_bounds__(GM_THREADS, 2) gemm_exact_kernel(GemmArgs p) {
 // memory, then per 32-row block i:  X_i := inv(L_ii) X_i,  X_{>i} -= L_{>i,i} X_i  -- both on the
 // tensor cores (DMMA 8x8x4), L streamed from L2.  Not bitwise: exact mode keeps swap_trsm_kernel.
 
-constexpr int SD_BN = 32;              // strip width
-constexpr int SD_LDX = SD_BN + 4;      // padded row stride: conflict-free A/B/C fragment access
-template <int NPMAX>
-struct SdCfg {  // NPMAX 256: 74 KB smem, 80 regs, 3 CTAs/SM; 512 (b = 512): 147 KB, 1 CTA/SM
-  static constexpr int SMEM = NPMAX * SD_LDX * 8;
-  static constexpr int MINB = NPMAX <= 256 ? 3 : 1;
+// NPMAX rows x BN-column strip, rows padded to BN + 4 doubles (conflict-free B fragments; 32-wide
+// strips also conflict-free A/C).  (256, 32): 74 KB, 3 CTAs/SM; (512, 16): 82 KB, 2 CTAs/SM.
+template <int NPMAX, int BN>
+struct SdCfg {
+  static constexpr int LDX = BN + 4;
+  static constexpr int SMEM = NPMAX * LDX * 8;
+  static constexpr int MINB = (227 * 1024) / (SMEM + 1024) >= 3 ? 3 : 2;
 };
-constexpr int SD_SMEM = SdCfg<256>::SMEM;
 
 __global__ void __launch_bounds__(128) diag_inv_kernel(const double* __restrict__ L, int64_t ldl, int np,
                                                        double* __restrict__ inv) {
@@ -551,13 +551,15 @@ __global__ void __launch_bounds__(128) diag_inv_kernel(const double* __restrict_
   }
 }
 
-template <int NPMAX>
-__global__ void __launch_bounds__(256, SdCfg<NPMAX>::MINB) swap_trsm_dmma_kernel(double* __restrict__ a, int64_t lda, int64_t d,
+template <int NPMAX, int SD_BN>
+__global__ void __launch_bounds__(256, (SdCfg<NPMAX, SD_BN>::MINB)) swap_trsm_dmma_kernel(double* __restrict__ a, int64_t lda, int64_t d,
                                                               int np, const int64_t* __restrict__ plan,
                                                               int64_t c0, int64_t c1,
                                                               const double* __restrict__ L, int64_t ldl,
                                                               const double* __restrict__ inv) {
   extern __shared__ double sd_smem[];
+  constexpr int SD_LDX = SdCfg<NPMAX, SD_BN>::LDX;
+  constexpr int NBK = SD_BN / 8;  // 8-column DMMA blocks per strip
   double* X = sd_smem;  // [NPMAX][SD_LDX]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int col = tid % SD_BN, rl = tid / SD_BN;  // loads: 8 rows per pass
@@ -611,19 +613,22 @@ __global__ void __launch_bounds__(256, SdCfg<NPMAX>::MINB) swap_trsm_dmma_kernel
   const int nblk = (np + 31) / 32;
   for (int ib = 0; ib < nblk; ++ib) {
     const int rb = ib * 32;
-    {  // X_i := inv(L_ii) X_i: 16 8x8 output blocks, two per warp
-      const int gg = warp >> 1, nb0 = (warp & 1) * 2;
+    {  // X_i := inv(L_ii) X_i: 4 x NBK 8x8 output blocks, NBK / 2 per warp
+      constexpr int JB = NBK / 2;
+      const int gg = warp >> 1, nb0 = (warp & 1) * JB;
       const double* iv = inv + (size_t)ib * 1024 + (gg * 8 + g) * 32;
-      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      double acc[JB][2];
+#pragma unroll
+      for (int j = 0; j < JB; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll
       for (int k4 = 0; k4 < 32; k4 += 4) {
         const double av = iv[k4 + t];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma884(acc[j][0], acc[j][1], av, X[(rb + k4 + t) * SD_LDX + (nb0 + j) * 8 + g]);
+        for (int j = 0; j < JB; ++j) dmma884(acc[j][0], acc[j][1], av, X[(rb + k4 + t) * SD_LDX + (nb0 + j) * 8 + g]);
       }
       __syncthreads();  // all reads of X_i done
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < JB; ++j) {
         double* xr = X + (rb + gg * 8 + g) * SD_LDX + (nb0 + j) * 8 + 2 * t;
         xr[0] = acc[j][0];
         xr[1] = acc[j][1];
@@ -636,14 +641,14 @@ __global__ void __launch_bounds__(256, SdCfg<NPMAX>::MINB) swap_trsm_dmma_kernel
       const int ntiles = (np - below + 8 * TG - 1) / (8 * TG);
       for (int tt = warp; tt < ntiles; tt += 8) {
         const int r0 = below + tt * 8 * TG;
-        double acc[TG][4][2];
+        double acc[TG][NBK][2];
         double al[TG][8];
 #pragma unroll
         for (int gg = 0; gg < TG; ++gg) {
           const int r = r0 + gg * 8 + g;
           const bool rok = r < np;
 #pragma unroll
-          for (int nb = 0; nb < 4; ++nb) {
+          for (int nb = 0; nb < NBK; ++nb) {
             acc[gg][nb][0] = X[r * SD_LDX + nb * 8 + 2 * t];
             acc[gg][nb][1] = X[r * SD_LDX + nb * 8 + 2 * t + 1];
           }
@@ -653,19 +658,19 @@ __global__ void __launch_bounds__(256, SdCfg<NPMAX>::MINB) swap_trsm_dmma_kernel
         }
 #pragma unroll
         for (int k4 = 0; k4 < 8; ++k4) {
-          double bv[4];
+          double bv[NBK];
 #pragma unroll
-          for (int nb = 0; nb < 4; ++nb) bv[nb] = -X[(rb + k4 * 4 + t) * SD_LDX + nb * 8 + g];
+          for (int nb = 0; nb < NBK; ++nb) bv[nb] = -X[(rb + k4 * 4 + t) * SD_LDX + nb * 8 + g];
 #pragma unroll
           for (int gg = 0; gg < TG; ++gg)
 #pragma unroll
-            for (int nb = 0; nb < 4; ++nb) dmma884(acc[gg][nb][0], acc[gg][nb][1], al[gg][k4], bv[nb]);
+            for (int nb = 0; nb < NBK; ++nb) dmma884(acc[gg][nb][0], acc[gg][nb][1], al[gg][k4], bv[nb]);
         }
 #pragma unroll
         for (int gg = 0; gg < TG; ++gg) {
           const int r = r0 + gg * 8 + g;
 #pragma unroll
-          for (int nb = 0; nb < 4; ++nb) {
+          for (int nb = 0; nb < NBK; ++nb) {
             X[r * SD_LDX + nb * 8 + 2 * t] = acc[gg][nb][0];
             X[r * SD_LDX + nb * 8 + 2 * t + 1] = acc[gg][nb][1];
           }
