@@ -46,7 +46,9 @@ typedef struct pflu_options {
   int panel_ctas;   /* CTAs of the panel kernel (0 = automatic; at most 16 for the cluster kernel) */
   int leaf_width;   /* leaf columns: 8, 16 or 32 (0 = automatic) */
   int panel_kernel; /* 0 automatic, 1 cooperative grid (LL exchange through L2), 2 one thread-block
-                       cluster (DSMEM exchange; PFLU_ERR_UNSUPPORTED if the panel does not fit) */
+                       cluster (DSMEM exchange; PFLU_ERR_UNSUPPORTED if the panel does not fit),
+                       3 recursive: halves split down to 32-column leaves (persistent kernel), the
+                       halves joined by swap+TRSM and a full-height DMMA GEMM */
   int reserved[4];
 } pflu_options;
 

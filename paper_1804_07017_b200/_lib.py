@@ -114,7 +114,7 @@ def check(rc: int, what: str) -> None:
     raise RuntimeError(f"{what} failed (code {rc}): {msg}")
 
 
-PANEL_AUTO, PANEL_GRID, PANEL_CLUSTER = 0, 1, 2
+PANEL_AUTO, PANEL_GRID, PANEL_CLUSTER, PANEL_RECURSIVE = 0, 1, 2, 3
 
 
 def options(exact: bool = False, panel_ctas: int = 0, leaf_width: int = 0, panel_kernel: int = PANEL_AUTO) -> Options:

@@ -140,21 +140,23 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def getrf_host(a: np.ndarray, b: int, lookahead: int, exact: bool = False, panel_ctas: int = 0):
+def getrf_host(a: np.ndarray, b: int, lookahead: int, exact: bool = False, panel_ctas: int = 0,
+               panel_kernel: int = 0):
     """Factor a row-major C-contiguous float64 host array in place through pflu_getrf.
     Returns (piv0 int64[n], info)."""
     L = _lib.load()
     m, n = a.shape
     piv = np.empty(n, dtype=np.int64)
     info = ctypes.c_int64(0)
-    opt = _lib.options(exact=exact, panel_ctas=panel_ctas)
+    opt = _lib.options(exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel)
     rc = L.pflu_getrf(a.ctypes.data, m, n, a.strides[0] // 8, int(b), int(lookahead), piv.ctypes.data,
                       ctypes.byref(info), ctypes.byref(opt))
     _lib.check(rc, "pflu_getrf")
     return piv, int(info.value)
 
 
-def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int = 0, piv=None, trace=None):
+def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int = 0, piv=None, trace=None,
+                 panel_kernel: int = 0):
     """Factor a row-major CUDA float64 torch tensor in place through pflu_getrf_device on the
     current torch stream.  Returns (piv0 int64 CUDA tensor, info).  If ``trace`` is a list, it
     receives :class:`TraceEvent` records (labels PF / TU / TU_L / TU_R / GEMM, seconds from the
@@ -166,7 +168,7 @@ def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int
     if piv is None:
         piv = torch.empty(n, dtype=torch.int64, device=a.device)
     info = ctypes.c_int64(0)
-    opt = _lib.options(exact=exact, panel_ctas=panel_ctas)
+    opt = _lib.options(exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel)
     stream = torch.cuda.current_stream(a.device).cuda_stream
     tbuf, tcap, tlen = None, 0, ctypes.c_int(0)
     if trace is not None:
@@ -187,7 +189,7 @@ def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int
 
 
 def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a: bool = True,
-              exact: bool = False, return_info: bool = False, panel_ctas: int = 0):
+              exact: bool = False, return_info: bool = False, panel_ctas: int = 0, panel_kernel: int = 0):
     """Blocked right-looking LU with partial pivoting on the B200.
 
     ``a``: float64 m x n (m >= n) row-major -- a numpy array (host buffers: staged through
@@ -195,7 +197,8 @@ def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a:
     reference's dmf_la, 0 its dmf_mtb.  ``exact=True`` reproduces the reference's rounding in
     every update (bitwise-equal factors); the default runs the trailing update on DMMA tensor
     cores.  ``n_gpus > 1`` runs the 1-D block-cyclic multi-GPU driver (requires an initialised
-    torch.distributed NCCL process group with one rank per GPU).
+    torch.distributed NCCL process group with one rank per GPU).  ``panel_kernel`` forces the
+    panel factorization of every step (0 automatic, 1 cooperative grid, 2 cluster, 3 recursive).
 
     Returns ``(lu, piv)`` (``(lu, piv, info)`` with ``return_info``): packed unit-lower L below
     the diagonal and U on/above it, and 0-based LAPACK pivots (row i swapped with piv[i]).
@@ -217,7 +220,7 @@ def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a:
         if not a.is_cuda:
             raise ValueError("torch input must be a CUDA tensor (use a numpy array for host buffers)")
         work = a if (overwrite_a and a.stride(1) == 1) else a.contiguous().clone()
-        piv, info = getrf_device(work, b, lookahead, exact=exact, panel_ctas=panel_ctas)
+        piv, info = getrf_device(work, b, lookahead, exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel)
     else:
         arr = np.asarray(a)
         if arr.dtype != np.float64 or arr.ndim != 2:
@@ -229,7 +232,7 @@ def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a:
             work = arr
         else:
             work = np.array(arr, dtype=np.float64, order="C", copy=True)
-        piv, info = getrf_host(work, b, lookahead, exact=exact, panel_ctas=panel_ctas)
+        piv, info = getrf_host(work, b, lookahead, exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel)
     if info:
         warnings.warn(f"exactly singular: zero pivot in column {info} (1-based)", RuntimeWarning, stacklevel=2)
     return (work, piv, info) if return_info else (work, piv)

@@ -72,6 +72,8 @@ struct DevCtx {
   double* dinv = nullptr;                    // per-step inverted 32x32 diagonal blocks of L11 (fast mode)
   size_t dinv_cap = 0;                       // in doubles
   int64_t* plan[2] = {nullptr, nullptr};
+  int64_t* rplan = nullptr;                  // recursive panel: pivot plan of the current split
+  double* rinv = nullptr;                    // recursive panel: inverted diagonal blocks of that split
   unsigned long long* info = nullptr;
   unsigned long long* ll = nullptr;  // LL exchange words of the panel kernel
   unsigned* epoch = nullptr;
@@ -100,6 +102,14 @@ static int64_t g_grid_rows = []() { const char* e = getenv("PFLU_GRID_ROWS"); re
 static int g_resync = []() { const char* e = getenv("PFLU_PANEL_RESYNC"); return e ? atoi(e) : 4; }();
 static int g_chunks = []() { const char* e = getenv("PFLU_CHUNKS"); return e ? atoi(e) : 1; }();
 static int g_tur_grid = []() { const char* e = getenv("PFLU_TUR_GRID"); return e ? atoi(e) : 0; }();
+// recursive panel (panel_kernel 3): leaf width and leaf kernel (0 auto, 1 grid, 2 cluster)
+static int g_rec_leaf = []() { const char* e = getenv("PFLU_REC_LEAF"); return e ? atoi(e) : 32; }();
+static int g_rec_leafk = []() { const char* e = getenv("PFLU_REC_LEAFK"); return e ? atoi(e) : 0; }();
+// force the panel kernel of every PF step of getrf (-1 = the schedule's own choice)
+static int g_pf_force = []() { const char* e = getenv("PFLU_PF_KERNEL"); return e ? atoi(e) : -1; }();
+// scaling model (tools/emu_scaling.py): emulate one rank of a P-GPU 1-D block-cyclic run whose
+// rank owns EVERY panel (the per-step critical path: TU_L + PF) but only 1/P of each trailing update
+static int g_emu_ranks = []() { const char* e = getenv("PFLU_EMU_RANKS"); return e ? atoi(e) : 0; }();
 static int g_variant = []() { const char* e = getenv("PFLU_PANEL_VARIANT"); return e ? atoi(e) : 0; }();  // device buffer for panel-kernel phase clocks (tools only)
 
 // Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.
@@ -197,6 +207,8 @@ static int ctx_get(DevCtx** out) {
     for (auto& s : c.sC) CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, lo));
     CK(cudaMalloc(&c.plan[0], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
     CK(cudaMalloc(&c.plan[1], sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
+    CK(cudaMalloc(&c.rplan, sizeof(int64_t) * (1 + 3 * PLAN_MAX)));
+    CK(cudaMalloc(&c.rinv, sizeof(double) * 1024 * (PLAN_MAX / 32)));
     CK(cudaMalloc(&c.info, 64));
     CK(cudaMalloc(&c.ll, sizeof(unsigned long long) * LL_WORDS));
     CK(cudaMemset(c.ll, 0, sizeof(unsigned long long) * LL_WORDS));
@@ -446,7 +458,7 @@ static int pf_cluster_ok(DevCtx& c, int W, int S, bool* ok) {
 }
 
 // Persistent panel factorization: rows [r0, m) of storage columns [c0, c0 + w).
-static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, int64_t c0, int64_t w,
+static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, int64_t c0, int64_t w,
                         int64_t* piv, unsigned long long* info, const pflu_options& opt, cudaStream_t st) {
   const int64_t rows = m - r0;
   if (rows <= 0 || w <= 0) return PFLU_OK;
@@ -525,6 +537,49 @@ static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0
                  (long long)rows, (long long)w);
 }
 
+// Recursive panel (panel_kernel 3; Toledo's recursive LU restricted to the panel's columns):
+//   left half recursively -> its swaps + U12 := L11^-1 A12 on the right half (swap+TRSM kernel) ->
+//   A22 -= L21 U12 over the full panel height (DMMA GEMM on every free SM) -> right half
+//   recursively -> its swaps applied back to the left half's columns.
+// Leaves of <= g_rec_leaf columns run on the persistent panel kernel.  Every element still receives
+// its updates in ascending pivot order (multiply, then subtract in exact mode), so exact mode stays
+// bitwise equal to the unblocked getf2 of the reference (_jit.py:154-187), like the outer blocking.
+static int panel_rec(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, int64_t c0, int64_t w,
+                     int64_t* piv, unsigned long long* info, const pflu_options& opt, cudaStream_t st) {
+  const int64_t rows = m - r0;
+  if (rows <= 0 || w <= 0) return PFLU_OK;
+  const int leaf = std::max(8, g_rec_leaf);
+  if (w <= leaf) {
+    pflu_options lo = opt;
+    lo.panel_kernel = g_rec_leafk;
+    return panel_leaf(c, a, lda, m, r0, c0, w, piv, info, lo, st);
+  }
+  // split at a multiple of the leaf width near the middle
+  int64_t h = ((w / 2 + leaf - 1) / leaf) * leaf;
+  if (h >= w) h = w - leaf;
+  CKR(panel_rec(c, a, lda, m, r0, c0, h, piv, info, opt, st));
+  const int np = (int)std::min<int64_t>(h, rows);
+  const bool exact = opt.exact != 0;
+  CKR(launch_plan(piv, r0, np, c.rplan, st));
+  const double* l11 = a + r0 * lda + c0;
+  const bool dinv = !exact && g_trsm_dmma && np <= 512;
+  if (dinv) CKR(launch_diag_inv(l11, lda, np, c.rinv, st));
+  CKR(launch_swap(a, lda, r0, np, c.rplan, c0 + h, c0 + w, l11, lda, true, st, dinv ? c.rinv : nullptr));
+  if (rows <= np) return PFLU_OK;
+  CKR(launch_gemm(a + (r0 + np) * lda + c0 + h, lda, a + (r0 + np) * lda + c0, lda, a + r0 * lda + c0 + h, lda,
+                  rows - np, w - h, np, exact, st));
+  CKR(panel_rec(c, a, lda, m, r0 + np, c0 + h, w - h, piv, info, opt, st));
+  const int np2 = (int)std::min<int64_t>(w - h, rows - np);
+  CKR(launch_plan(piv, r0 + np, np2, c.rplan, st));
+  return launch_swap(a, lda, r0 + np, np2, c.rplan, c0, c0 + h, nullptr, lda, false, st);
+}
+
+static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, int64_t c0, int64_t w,
+                        int64_t* piv, unsigned long long* info, const pflu_options& opt, cudaStream_t st) {
+  if (opt.panel_kernel == 3) return panel_rec(c, a, lda, m, r0, c0, w, piv, info, opt, st);
+  return panel_leaf(c, a, lda, m, r0, c0, w, piv, info, opt, st);
+}
+
 // ------------------------------------------------------------------------------------------
 // the blocked factorization
 
@@ -595,7 +650,8 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     const Step s = grid[k];
     if (s.col0 == 0) return PFLU_OK;
     const int np = (int)std::min(s.bw, m - s.col0);
-    return launch_swap(a, lda, s.col0, np, plan_of(k), 0, s.col0, nullptr, lda, false, st);
+    const int64_t hi = g_emu_ranks > 1 ? std::min<int64_t>(s.col0, (s.col0 / g_emu_ranks + b - 1) / b * b) : s.col0;
+    return launch_swap(a, lda, s.col0, np, plan_of(k), 0, hi, nullptr, lda, false, st);
   };
   // Depth 0 runs each panel alone on the critical path: tall panels take the cooperative-grid kernel
   // (more SMs, lower latency).  Depth 1 keeps the 16-SM cluster kernel, which leaves the other SMs to
@@ -606,6 +662,8 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     CKR(tr.begin(PFLU_TRACE_PF, k, st, &t_pf));
     pflu_options popt = opt;
     if (lookahead == 0 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;
+    if (g_emu_ranks > 1 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;  // = dist.py
+    if (g_pf_force >= 0 && opt.panel_kernel == 0) popt.panel_kernel = g_pf_force;
     CKR(panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, popt, st));
     const int np = (int)std::min(s.bw, m - s.col0);
     CKR(launch_plan(piv, s.col0, np, plan_of(k), st));
@@ -664,10 +722,12 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   CK(cudaEventRecord(ev_pf(0), c.sP));
   for (int k = 0; k < count; ++k) {
     const int64_t lo_r = (k + 1 < count) ? grid[k + 1].col0 + grid[k + 1].bw : n;
+    int64_t hi_r = n;
+    if (g_emu_ranks > 1) hi_r = std::min<int64_t>(n, lo_r + ((n - lo_r + g_emu_ranks - 1) / g_emu_ranks + b - 1) / b * b);
     for (int ch = 0; ch < nch; ++ch) {
       cudaStream_t st = c.sC[ch];
       const int64_t c_lo = std::max<int64_t>(lo_r, (int64_t)chunk_blk[ch] * b);
-      const int64_t c_hi = std::min<int64_t>(n, (int64_t)chunk_blk[ch + 1] * b);
+      const int64_t c_hi = std::min<int64_t>(hi_r, (int64_t)chunk_blk[ch + 1] * b);
       if (c_hi > c_lo) {
         CK(cudaStreamWaitEvent(st, ev_pf(k), 0));
         CKR(update_cols(k, c_lo, c_hi, st, PFLU_TRACE_TU_R));

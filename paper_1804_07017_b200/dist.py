@@ -206,8 +206,8 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
     nblk = num_blocks(n, b)
     if piv is None:
         piv = torch.zeros(n, dtype=torch.int64, device=dev)
-    pbuf = [torch.empty(n * b, dtype=torch.float64, device=dev) for _ in range(2)]
-    ppiv = [torch.empty(b, dtype=torch.int64, device=dev) for _ in range(2)]
+    # broadcast buffers: the packed panel ((n - kb) x bw) followed by its bw pivots (int64 bits)
+    pbuf = [torch.empty(n * b + b, dtype=torch.float64, device=dev) for _ in range(2)]
     plans = [torch.empty(1 + 3 * b, dtype=torch.int64, device=dev) for _ in range(2)]
     fast = getattr(kernels, "fast_solve", False) and b <= 512
     invs = [torch.empty(((b + 31) // 32) * 1024, dtype=torch.float64, device=dev) for _ in range(2)] if fast else [None, None]
@@ -226,17 +226,18 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
         bw = min(b, n - col0)
         rows = n - col0
         o = k % P
-        buf = pbuf[k % 2][: rows * bw].view(rows, bw)
+        msg = pbuf[k % 2][: rows * bw + bw]
+        buf = msg[: rows * bw].view(rows, bw)
+        pv = msg[rows * bw:].view(torch.int64)
         if r == o:
             lc = local_col_of_block(k, b, P)
             kernels.panel(a_loc, n, col0, lc, bw, piv)
             buf.copy_(a_loc[col0:, lc: lc + bw])
-            ppiv[k % 2][:bw].copy_(piv[col0: col0 + bw])
+            pv.copy_(piv[col0: col0 + bw])
         if P > 1:
-            dist.broadcast(buf, src=o, group=group)
-            dist.broadcast(ppiv[k % 2][:bw], src=o, group=group)
+            dist.broadcast(msg, src=o, group=group)  # one message per step: panel + pivots
             if r != o:
-                piv[col0: col0 + bw].copy_(ppiv[k % 2][:bw])
+                piv[col0: col0 + bw].copy_(pv)
         kernels.plan(piv, col0, bw, plans[k % 2])
         if fast:
             kernels.diag_inv(buf[:bw, :bw], invs[k % 2])
@@ -361,6 +362,56 @@ def lu_factor_dist(a, b: int = 256, lookahead: int = 1, exact: bool = False, ret
     return (lu, piv, info) if return_info else (lu, piv)
 
 
+def lu_factor_local(a_loc, n: int, b: int = 256, lookahead: int = 1, exact: bool = False,
+                    return_info: bool = False):
+    r"""Distributed-input form of ``lu_factor(..., n_gpus=P)`` (ScaLAPACK style): each rank passes
+    ONLY its block-cyclic columns -- ``a_loc`` of shape (n, local_cols(n, b, P, rank)), row-major,
+    host (numpy / torch, ideally pinned) or CUDA -- and gets its columns of the packed L\U back in
+    place, plus the full 0-based pivot vector.  Host traffic per rank is 1/P of the matrix."""
+    import numpy as np
+
+    if not dist.is_initialized():
+        raise RuntimeError("lu_factor_local needs an initialised torch.distributed process group")
+    P, r = dist.get_world_size(), dist.get_rank()
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", r % max(1, torch.cuda.device_count()))))
+    torch.cuda.set_device(dev)
+    t = a_loc if isinstance(a_loc, torch.Tensor) else torch.from_numpy(a_loc)
+    if t.dim() != 2 or t.shape[0] != n or t.shape[1] != local_cols(n, b, P, r) or t.dtype != torch.float64 \
+            or t.stride(1) != 1:
+        raise ValueError("a_loc must be this rank's (n x local_cols) row-major float64 block-cyclic columns")
+    if t.is_cuda:
+        piv, info = getrf_block_cyclic(t, n, b, lookahead, CudaKernels(dev, exact=exact))
+        return (t, piv, info) if return_info else (t, piv)
+    d = torch.empty(t.shape, dtype=torch.float64, device=dev)
+    d.copy_(t, non_blocking=True)
+    piv, info = getrf_block_cyclic(d, n, b, lookahead, CudaKernels(dev, exact=exact))
+    t.copy_(d, non_blocking=True)
+    piv_h = piv.cpu()
+    torch.cuda.synchronize()
+    out_piv = piv_h.numpy() if not isinstance(a_loc, torch.Tensor) else piv_h
+    return (a_loc, out_piv, info) if return_info else (a_loc, out_piv)
+
+
+def local_columns_seeded(n: int, b: int, P: int, r: int, seed: int, dist_name: str = "uniform",
+                         chunk_rows: int = 1024):
+    """Rank r's block-cyclic columns of the seeded BASELINE matrix (numpy default_rng(seed), row-major
+    draw order), generated in row chunks so no rank ever holds the full n x n matrix."""
+    import numpy as np
+
+    g = np.random.default_rng(seed)
+    blocks = local_blocks(n, b, P, r)
+    out = np.empty((n, local_cols(n, b, P, r)), dtype=np.float64)
+    for r0 in range(0, n, chunk_rows):
+        r1 = min(n, r0 + chunk_rows)
+        rows = g.uniform(-1.0, 1.0, size=(r1 - r0, n)) if dist_name == "uniform" else g.standard_normal((r1 - r0, n))
+        c = 0
+        for j in blocks:
+            w = min(b, n - j * b)
+            out[r0:r1, c: c + w] = rows[:, j * b: j * b + w]
+            c += w
+    return out
+
+
 # ---------------------------------------------------------------------------------------------
 # bench.py --gpus N (torchrun, one rank per GPU)
 
@@ -380,10 +431,7 @@ def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     n, b, la = args.n, args.b, args.lookahead
-    full = np.random.default_rng(3).uniform(-1.0, 1.0, size=(n, n))
-    cols = [full[:, j * b: min(n, (j + 1) * b)] for j in local_blocks(n, b, P, r)]
-    host_loc = np.ascontiguousarray(np.concatenate(cols, axis=1))
-    del full, cols
+    host_loc = local_columns_seeded(n, b, P, r, seed=3)  # 1/P of the matrix per rank
     a0 = torch.from_numpy(host_loc).to(dev)
     a = torch.empty_like(a0)
     piv = torch.zeros(n, dtype=torch.int64, device=dev)
@@ -418,19 +466,18 @@ def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
     ms_step = float(ms.item()) / args.steps
     value = lu_flops(n) / (ms_step * 1e-3) / 1e9
     peak, peak_src = fp64_peak()
-    # end to end through the public API: full pinned host matrix in, each rank's L\U columns and
-    # the pivots back to the host (gather="local": the distributed result)
+    # end to end through the public API: each rank's block-cyclic columns in pinned host memory,
+    # H2D, factorization, its L\U columns and the pivots back to the host (lu_factor_local)
     e2e = None
     if args.e2e_steps > 0:
-        pristine = torch.from_numpy(np.random.default_rng(3).uniform(-1.0, 1.0, size=(n, n)))
-        host = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        pristine = torch.from_numpy(host_loc)
+        host = torch.empty(pristine.shape, dtype=torch.float64).pin_memory()
         ts = []
         for it in range(args.e2e_steps + 1):
             host.copy_(pristine)
             dist.barrier()
             t0 = time.perf_counter()
-            lu, pv = lu_factor_dist(host, b=b, lookahead=la, gather="local")
-            pv = pv.cpu()
+            lu, pv = lu_factor_local(host, n, b=b, lookahead=la)
             dist.barrier()
             ts.append(time.perf_counter() - t0)
         tmax = torch.tensor([sum(ts[1:]) / len(ts[1:])], dtype=torch.float64, device=dev)
@@ -438,7 +485,7 @@ def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
         nloc = local_cols(n, b, P, r)
         e2e = {"value": lu_flops(n) / float(tmax.item()) / 1e9, "unit": unit, "h2d_bytes_per_step": n * nloc * 8,
                "d2h_bytes_per_step": n * nloc * 8 + n * 8,
-               "api": "paper_1804_07017_b200.dist.lu_factor_dist(pinned host matrix, gather='local') per rank"}
+               "api": "paper_1804_07017_b200.dist.lu_factor_local(pinned host block-cyclic columns) per rank"}
         del host, pristine
     if r == 0:
         line = {

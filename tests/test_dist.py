@@ -94,3 +94,18 @@ def test_block_cyclic_bookkeeping():
                     lc = pd.local_col_of_block(k, b, P)
                     assert torch.equal(parts[r][:, lc: lc + min(b, n - k * b)], a[:, k * b: min(n, (k + 1) * b)])
                     assert pd.local_cols_before(k, n, b, P, r) == lc
+
+
+@pytest.mark.parametrize("dist_name,seed", [("uniform", 3), ("normal", 2)])
+def test_local_columns_seeded_match_full_matrix(dist_name, seed):
+    """Chunked per-rank generation == the block-cyclic columns of the full seeded BASELINE matrix."""
+    sys.path.insert(0, ROOT)
+    from paper_1804_07017_b200 import dist as pd
+
+    n, b = 530, 64
+    g = np.random.default_rng(seed)
+    full = g.uniform(-1.0, 1.0, (n, n)) if dist_name == "uniform" else g.standard_normal((n, n))
+    for P in (1, 3):
+        for r in range(P):
+            loc = pd.local_columns_seeded(n, b, P, r, seed, dist_name, chunk_rows=100)
+            assert loc.tobytes() == pd.scatter_columns(torch.from_numpy(full), b, P, r).numpy().tobytes()

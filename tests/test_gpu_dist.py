@@ -114,3 +114,34 @@ def test_lu_factor_dist_api(cuda, tmp_path, gather):
             for j in pd.local_blocks(n, b, world, r):
                 sl = slice(j * b, min(n, (j + 1) * b))
                 assert lu[:, sl].tobytes() == np.ascontiguousarray(ref[:, sl]).tobytes()
+
+
+def _worker_local(rank, world, port, n, b, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["LOCAL_RANK"] = "0"
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1804_07017_b200 import dist as pd
+
+    loc = torch.from_numpy(pd.local_columns_seeded(n, b, world, rank, seed=9)).pin_memory()
+    out, piv, info = pd.lu_factor_local(loc, n, b=b, lookahead=1, exact=True, return_info=True)
+    np.save(os.path.join(out_dir, f"loc{rank}.npy"), out.numpy())
+    np.save(os.path.join(out_dir, f"piv{rank}.npy"), np.asarray(piv))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_lu_factor_local_api(cuda, tmp_path):
+    """ScaLAPACK-style distributed input: each rank passes only its block-cyclic columns."""
+    from paper_1804_07017_b200 import dist as pd
+
+    n, b, world = 600, 64, 2
+    a = np.random.default_rng(9).uniform(-1.0, 1.0, (n, n))
+    ref, rpiv, _ = oracle.getrf(a, b)
+    mp.spawn(_worker_local, args=(world, _free_port(), n, b, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"piv{r}.npy"), rpiv)
+        want = pd.scatter_columns(torch.from_numpy(ref), b, world, r).numpy()
+        assert np.load(tmp_path / f"loc{r}.npy").tobytes() == want.tobytes()

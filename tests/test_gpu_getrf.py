@@ -63,10 +63,11 @@ def gpu_residual(a0, lu, piv, block=4096):
     return np.sqrt(err2) / (n * oracle.UNIT_ROUNDOFF * np.linalg.norm(a0))
 
 
-def run(a0, b, lookahead, exact):
+def run(a0, b, lookahead, exact, panel_kernel=0):
     from paper_1804_07017_b200 import lu_factor
 
-    lu, piv, info = lu_factor(a0.copy(), b=b, lookahead=lookahead, exact=exact, return_info=True)
+    lu, piv, info = lu_factor(a0.copy(), b=b, lookahead=lookahead, exact=exact, return_info=True,
+                              panel_kernel=panel_kernel)
     return lu, piv, info
 
 
@@ -107,6 +108,34 @@ def test_c1_exact_matches_reference_sha(cuda, lookahead):
     assert info == 0
     assert np.array_equal(piv, PIVOTS["c1"])
     assert sha(lu) == CONFIGS["c1"]["sha256_factors"]
+
+
+@pytest.mark.parametrize("lookahead", [0, 1])
+def test_c1_recursive_panel(cuda, lookahead):
+    """Every step's panel on the recursive panel (panel_kernel 3): exact mode keeps the reference's
+    bitwise factors, DMMA mode its pivots."""
+    a0 = config_matrix("c1")
+    lu, piv, info = run(a0, 128, lookahead, exact=True, panel_kernel=3)
+    assert info == 0 and np.array_equal(piv, PIVOTS["c1"])
+    assert sha(lu) == CONFIGS["c1"]["sha256_factors"]
+    lu2, piv2, _ = run(a0, 256, lookahead, exact=False, panel_kernel=3)
+    assert np.array_equal(piv2, PIVOTS["c1"])
+    assert gpu_residual(a0, lu2, piv2) <= 10
+    assert oracle.max_rel_diff(lu2, lu, a0) <= 1e-8
+
+
+@pytest.mark.parametrize("tag", SMALL)
+def test_small_golden_recursive_panel(cuda, golden_small, tag):
+    a0 = golden_small[f"{tag}__a"]
+    b, info, _ = golden_small[f"{tag}__meta"]
+    import warnings
+
+    with np.errstate(all="ignore"), warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        lu, piv, inf = run(a0, int(b), 1, exact=True, panel_kernel=3)
+    assert inf == info
+    assert np.array_equal(piv, golden_small[f"{tag}__piv"])
+    assert bitwise_equal(lu, golden_small[f"{tag}__f"])
 
 
 @pytest.mark.parametrize("lookahead", [0, 1])

@@ -181,7 +181,7 @@ def test_laswp_roundtrip_and_identity(cuda):
 @pytest.mark.parametrize("m,w,ctas,leaf", [(64, 8, 0, 0), (300, 16, 0, 0), (1000, 64, 0, 0), (2048, 128, 3, 0),
                                           (5000, 256, 0, 0), (777, 100, 5, 8), (4096, 256, 16, 16),
                                           (20000, 256, 0, 0), (512, 512, 0, 0), (40, 40, 0, 32)])
-@pytest.mark.parametrize("kernel", [1, 2], ids=["grid", "cluster"])
+@pytest.mark.parametrize("kernel", [1, 2, 3], ids=["grid", "cluster", "recursive"])
 def test_panel_bitwise(cuda, m, w, ctas, leaf, kernel):
     """Recursive panel + cooperative leaf == lu_unb_run on the panel (exact op order)."""
     import torch
@@ -193,7 +193,7 @@ def test_panel_bitwise(cuda, m, w, ctas, leaf, kernel):
     x = _t(p0, cuda)
     piv = torch.zeros(w, dtype=torch.int64, device=cuda)
     info = ctypes.c_int64(0)
-    opt = lb.options(exact=True, panel_ctas=ctas if kernel == 1 else min(ctas, 16), leaf_width=leaf, panel_kernel=kernel)
+    opt = lb.options(exact=True, panel_ctas=ctas if kernel != 2 else min(ctas, 16), leaf_width=leaf, panel_kernel=kernel)
     rc = lb.load().pflu_panel(x.data_ptr(), w, m, 0, 0, w, piv.data_ptr(), ctypes.byref(info), _stream(), ctypes.byref(opt))
     if kernel == 2 and rc == 3:
         pytest.skip("panel does not fit one cluster")
@@ -201,6 +201,25 @@ def test_panel_bitwise(cuda, m, w, ctas, leaf, kernel):
     assert np.array_equal(piv.cpu().numpy()[: len(wpiv)], wpiv)
     assert info.value == winfo
     assert bitwise_equal(x.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("m,w", [(300, 64), (5000, 256), (20000, 256), (2048, 512), (100, 200)])
+def test_panel_recursive_dmma(cuda, m, w):
+    """Recursive panel in DMMA mode: the oracle's pivots, factors within rounding of getf2's."""
+    import torch
+    from paper_1804_07017_b200 import _lib as lb
+
+    p0 = np.random.default_rng(m * 3 + w).uniform(-1, 1, (m, w))
+    want, wpiv, _ = oracle.lu_unb(p0.copy())
+    x = _t(p0, cuda)
+    piv = torch.zeros(w, dtype=torch.int64, device=cuda)
+    info = ctypes.c_int64(0)
+    opt = lb.options(exact=False, panel_kernel=lb.PANEL_RECURSIVE)
+    lb.check(lb.load().pflu_panel(x.data_ptr(), w, m, 0, 0, w, piv.data_ptr(), ctypes.byref(info), _stream(),
+                                  ctypes.byref(opt)), "panel")
+    assert np.array_equal(piv.cpu().numpy()[: len(wpiv)], wpiv)
+    assert info.value == 0
+    assert np.max(np.abs(x.cpu().numpy() - want)) <= 1e-10
 
 
 def test_panel_zero_column_info(cuda):

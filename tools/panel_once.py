@@ -11,13 +11,14 @@ m = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 w = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 ctas = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 leaf = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+kern = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 L = _lib.load()
 dev = torch.device("cuda:0")
 x0 = torch.rand(m, w, dtype=torch.float64, device=dev) * 2 - 1
 x = x0.clone()
 piv = torch.zeros(w, dtype=torch.int64, device=dev)
 info = ctypes.c_int64(0)
-opt = _lib.options(exact=False, panel_ctas=ctas, leaf_width=leaf)
+opt = _lib.options(exact=False, panel_ctas=ctas, leaf_width=leaf, panel_kernel=kern)
 st = torch.cuda.current_stream().cuda_stream
 for _ in range(3):
     x.copy_(x0)

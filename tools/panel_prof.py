@@ -13,6 +13,7 @@ w = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 ctas = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 leaf = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 exact = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+kern = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 import os
 if os.environ.get("PFLU_LIB_PATH"):
     _lib.LIB_PATH = os.environ["PFLU_LIB_PATH"]
@@ -24,7 +25,7 @@ x0 = torch.rand(m, w, dtype=torch.float64, device=dev) * 2 - 1
 x = x0.clone()
 piv = torch.zeros(w, dtype=torch.int64, device=dev)
 info = ctypes.c_int64(0)
-opt = _lib.options(exact=bool(exact), panel_ctas=ctas, leaf_width=leaf)
+opt = _lib.options(exact=bool(exact), panel_ctas=ctas, leaf_width=leaf, panel_kernel=kern)
 st = torch.cuda.current_stream().cuda_stream
 run = lambda: _lib.check(L.pflu_panel(x.data_ptr(), w, m, 0, 0, w, piv.data_ptr(), ctypes.byref(info), st, ctypes.byref(opt)), "p")  # noqa
 for _ in range(2):

@@ -19,6 +19,7 @@ ap.add_argument("--w", type=int, default=256)
 ap.add_argument("--ctas", default="0")
 ap.add_argument("--leaf", default="0")
 ap.add_argument("--reps", type=int, default=9)
+ap.add_argument("--kernel", default="0", help="panel_kernel values: 0 auto, 1 grid, 2 cluster, 3 recursive")
 ap.add_argument("--tag", default="")
 args = ap.parse_args()
 if args.lib:
@@ -32,8 +33,8 @@ for m in [int(x) for x in args.m.split(",")]:
     x = x0.clone()
     piv = torch.zeros(w, dtype=torch.int64, device=dev)
     for ctas in [int(x) for x in args.ctas.split(",")]:
-        for leaf in [int(x) for x in args.leaf.split(",")]:
-            opt = _lib.options(exact=False, panel_ctas=ctas, leaf_width=leaf)
+        for leaf, kern in [(int(x), int(y)) for x in args.leaf.split(",") for y in args.kernel.split(",")]:
+            opt = _lib.options(exact=False, panel_ctas=ctas, leaf_width=leaf, panel_kernel=kern)
             times = []
             ok = True
             for r in range(args.reps + 2):
@@ -49,7 +50,7 @@ for m in [int(x) for x in args.m.split(",")]:
                 if r >= 2:
                     times.append(e0.elapsed_time(e1))
             if not ok:
-                print(f"{args.tag} m={m} ctas={ctas} leaf={leaf}: unsupported")
+                print(f"{args.tag} m={m} ctas={ctas} leaf={leaf} kernel={kern}: unsupported")
                 continue
-            print(f"{args.tag} m={m} w={w} ctas={ctas} leaf={leaf}: median {statistics.median(times):.3f} ms "
+            print(f"{args.tag} m={m} w={w} ctas={ctas} leaf={leaf} kernel={kern}: median {statistics.median(times):.3f} ms "
                   f"min {min(times):.3f} max {max(times):.3f}")
