@@ -300,6 +300,67 @@ static int launch_gemm_p(DevCtx& dc, const GemmArgs& p0, bool v2, int ctas, cuda
   return PFLU_OK;
 }
 
+// TMA-fed GEMM: tensor maps of the A (M x K) and B (K x N) views, encoded on the host per launch
+// (cuTensorMapEncodeTiled through the runtime's driver entry point; no libcuda link dependency).
+typedef CUresult (*PfnEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PfnEncodeTiled tma_encoder() {
+  static PfnEncodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PfnEncodeTiled)f;
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+static int g_gemm_tma = []() { const char* e = getenv("PFLU_GEMM_TMA"); return e ? atoi(e) : 0; }();
+
+// returns PFLU_OK with *done = false when the views do not meet TMA's alignment rules
+template <class C>
+static int launch_gemm_tma(const GemmArgs& p, cudaStream_t st, bool* done) {
+  *done = false;
+  PfnEncodeTiled enc = tma_encoder();
+  if (!enc) return PFLU_OK;
+  if ((reinterpret_cast<uintptr_t>(p.a) & 15) || (reinterpret_cast<uintptr_t>(p.b) & 15) ||
+      (reinterpret_cast<uintptr_t>(p.c) & 15) || (p.lda & 1) || (p.ldb & 1) || (p.ldc & 1) ||
+      p.M >= (int64_t)1 << 31 || p.N >= (int64_t)1 << 31 || p.K >= (int64_t)1 << 31)
+    return PFLU_OK;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(gemm_dmma_tma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, TmaCfg<C>::SMEM));
+    attr = true;
+  }
+  CUtensorMap ta, tb;
+  const cuuint32_t es[2] = {1, 1};
+  const cuuint64_t da[2] = {(cuuint64_t)p.K, (cuuint64_t)p.M}, sa[1] = {(cuuint64_t)p.lda * 8};
+  const cuuint32_t ba[2] = {8, (cuuint32_t)C::BM};
+  CUresult r = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p.a), da, sa, ba, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(PFLU_ERR_CUDA, "cuTensorMapEncodeTiled(A) failed: %d", (int)r);
+  const cuuint64_t db[2] = {(cuuint64_t)p.N, (cuuint64_t)p.K}, sb[1] = {(cuuint64_t)p.ldb * 8};
+  const cuuint32_t bb[2] = {8, (cuuint32_t)C::BK};
+  r = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p.b), db, sb, bb, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(PFLU_ERR_CUDA, "cuTensorMapEncodeTiled(B) failed: %d", (int)r);
+  const int64_t tm = (p.M + C::BM - 1) / C::BM, tn = (p.N + C::BN - 1) / C::BN;
+  if (tm * tn > INT_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "gemm grid too large");
+  TmaGemmArgs q;
+  q.c = p.c; q.ldc = p.ldc; q.M = p.M; q.N = p.N; q.K = p.K;
+  q.tiles_m = (int)tm; q.tiles_n = (int)tn;
+  gemm_dmma_tma<C><<<(unsigned)(tm * tn), C::THREADS, TmaCfg<C>::SMEM, st>>>(ta, tb, q);
+  *done = true;
+  return PFLU_OK;
+}
+
 static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, const double* b, int64_t ldb,
                        int64_t M, int64_t N, int64_t K, bool exact, cudaStream_t st, int pgrid = 0) {
   if (M <= 0 || N <= 0 || K <= 0) return PFLU_OK;
@@ -318,7 +379,9 @@ static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, con
     if (v2) gemm_exact_kernel<2><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
     else gemm_exact_kernel<1><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
   } else {
-    switch (g_gemm_variant) {
+    bool done = false;
+    if (g_gemm_tma) CKR(launch_gemm_tma<GV6>(p, st, &done));
+    if (!done) switch (g_gemm_variant) {
       case 1: CKR(launch_gemm_t<GV1>(p, v2, st)); break;
       case 2: CKR(launch_gemm_t<GV2>(p, v2, st)); break;
       case 3: CKR(launch_gemm_t<GV3>(p, v2, st)); break;
@@ -516,7 +579,9 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
   for (int wi = 0; wi < 3; ++wi) {
     const int W = Ws[wi];
     if (W > Wpref) continue;
-    int S = opt.panel_ctas > 0 ? opt.panel_ctas : (int)std::min<int64_t>(g_pf_cap, (rows + 255) / 256);
+    // tall panels: 64 CTAs (measured: 32768 x 256 1.65 -> 1.50 ms, 16384 x 256 1.33 -> 1.21 ms)
+    const int cap = rows >= 16384 ? std::max(g_pf_cap, 64) : g_pf_cap;
+    int S = opt.panel_ctas > 0 ? opt.panel_ctas : (int)std::min<int64_t>(cap, (rows + 255) / 256);
     S = std::max(1, std::min(S, PF_MAX_CTAS));
     for (; S <= PF_MAX_CTAS; ++S) {
       const int64_t R = (rows + S - 1) / S;

@@ -8,6 +8,8 @@
 // XOR-swizzled shared tiles: A[m][k] at k ^ ((m & 3) << 2), B[k][n] at n ^ ((k & 3) << 2), which
 // makes every 64-bit fragment load conflict free (two 128-byte wavefronts per warp).
 #pragma once
+#include <cuda.h>
+
 #include "pflu_kernels.cuh"
 
 namespace pflu {
@@ -335,6 +337,177 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_persistent(Gemm
     }
   }
   cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------------------------
+// TMA-fed variant.  One elected thread issues the operand tiles with cp.async.bulk.tensor (TMA,
+// 64-byte swizzle, out-of-bounds elements zero-filled by the hardware) into a 2-stage ring whose
+// "full" mbarriers carry the transaction bytes; the compute warps only wait on the barrier and read
+// fragments.  Boxes are 8 doubles (64 B) wide: A stage = BK/8 boxes of [BM][8] (k inner), B stage
+// = BN/8 boxes of [BK][8] (n inner).  With the 64-byte swizzle, 16-byte chunk c of box row r lives
+// at chunk c ^ ((r >> 1) & 3).  The k slots of each DMMA k-quad are permuted inside every group of
+// 8 k values -- thread t of quad q (q = 0, 1) takes k = 2q + (t & 1) + 4 (t >> 1) -- which makes
+// every 64-bit fragment load of A and B hit 16 distinct bank pairs per half-warp (the minimum two
+// wavefronts per warp).  A and B use the same permutation, so each DMMA sums over 4 distinct k.
+struct TmaGemmArgs {
+  double* c;
+  int64_t ldc, M, N, K;
+  int tiles_m, tiles_n;
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done)
+                 : "r"(a), "r"(parity)
+                 : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(double* dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+template <class C>
+struct TmaCfg {
+  static_assert(C::BK % 8 == 0 && C::BN % 8 == 0 && C::TN % 8 == 0, "8-wide boxes");
+  static constexpr int ABOX = C::BM * 8, BBOX = C::BK * 8;     // doubles per box
+  static constexpr int STAGE = C::BM * C::BK + C::BK * C::BN;  // doubles per stage
+  static constexpr int SMEM = C::ST * STAGE * 8 + 64;           // + the stage mbarriers, counters
+  static constexpr int MINB = (2 * SMEM <= 227 * 1024) ? 2 : 1;
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, TmaCfg<C>::MINB)
+    gemm_dmma_tma(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, TmaGemmArgs p) {
+  using T = TmaCfg<C>;
+  // no static shared memory: the dynamic block starts at offset 0 (1024-aligned for the swizzle), and
+  // fragment loads through `sm` stay LDS (a pointer re-aligned by integer arithmetic would compile
+  // to generic loads); the stage barriers sit after the stages
+  extern __shared__ __align__(1024) double gt_smem[];
+  double* sm = gt_smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(gt_smem + C::ST * T::STAGE);
+  int* drained = reinterpret_cast<int*>(full + C::ST);  // per slot: warps done with it
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp / C::WN, wn = warp % C::WN;
+  int tm, tn;
+  tile_coords(blockIdx.x, p.tiles_m, p.tiles_n, tm, tn);
+  const int m0 = tm * C::BM, n0 = tn * C::BN;
+  const int KT = (int)((p.K + C::BK - 1) / C::BK);
+  if (tid == 0) {
+    for (int s = 0; s < C::ST; ++s) {
+      mbar_init(&full[s], 1);
+      drained[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int s, int kt) {  // one thread
+    double* st = sm + s * T::STAGE;
+    mbar_expect_tx(&full[s], (unsigned)(T::STAGE * 8));
+    const int k0 = kt * C::BK;
+#pragma unroll
+    for (int kb = 0; kb < C::BK / 8; ++kb) tma_load_2d(st + kb * T::ABOX, &ta, k0 + kb * 8, m0, &full[s]);
+#pragma unroll
+    for (int nb = 0; nb < C::BN / 8; ++nb)
+      tma_load_2d(st + C::BM * C::BK + nb * T::BBOX, &tb, n0 + nb * 8, k0, &full[s]);
+  };
+  if (tid == 0)
+    for (int s = 0; s < C::ST && s < KT; ++s) issue(s, s);
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i) {
+    const int64_t row = m0 + wm * C::TM + i * 8 + g;
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) {
+      const int64_t col = n0 + wn * C::TN + j * 8 + 2 * t;
+      const double* cp = p.c + row * p.ldc + col;
+      if (row < p.M && col + 1 < p.N) {
+        const double2 v = *reinterpret_cast<const double2*>(cp);
+        acc[i][j][0] = v.x;
+        acc[i][j][1] = v.y;
+      } else {
+        acc[i][j][0] = (row < p.M && col < p.N) ? cp[0] : 0.0;
+        acc[i][j][1] = (row < p.M && col + 1 < p.N) ? cp[1] : 0.0;
+      }
+    }
+  }
+  // per-thread fragment offsets (doubles).  k slot of thread t in quad q of an 8-group:
+  // kl = 2q + (t & 1) + 4 (t >> 1).  A (box = 8-k group): row m = wm TM + 8i + g, chunk (kl >> 1) ^
+  // ((m >> 1) & 3) = (q + 2 (t >> 1)) ^ (g >> 1).  B (box = 8 columns n = wn TN + 8j + g): row kl,
+  // chunk (g >> 1) ^ ((kl >> 1) & 3).
+  const int tlo = t & 1, thi = t >> 1;
+  const int a_base = (wm * C::TM + g) * 8 + tlo;
+  const int b_base = (wn * C::TN / 8) * T::BBOX + (g & 1);
+  int xa[2], xb[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int h2 = q + 2 * thi;  // kl >> 1
+    xa[q] = ((h2 ^ (g >> 1)) << 1);
+    xb[q] = (2 * q + tlo + 4 * thi) * 8 + (((g >> 1) ^ h2) << 1);
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % C::ST;
+    mbar_wait(&full[s], (unsigned)((kt / C::ST) & 1));
+    const double* cA = sm + s * T::STAGE + a_base;
+    const double* cB = sm + s * T::STAGE + C::BM * C::BK + b_base;
+#pragma unroll
+    for (int kb = 0; kb < C::BK / 8; ++kb) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        double af[C::FM], bf[C::FN];
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i) af[i] = cA[kb * T::ABOX + i * 64 + xa[q]];
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) bf[j] = -cB[j * T::BBOX + kb * 64 + xb[q]];
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    }
+    // the last warp to finish slot s refills it (no CTA-wide barrier in the main loop)
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&drained[s], 1) == C::THREADS / 32 - 1) {
+        drained[s] = 0;
+        if (kt + C::ST < KT) issue(s, kt + C::ST);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i) {
+    const int64_t row = m0 + wm * C::TM + i * 8 + g;
+    if (row >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) {
+      const int64_t col = n0 + wn * C::TN + j * 8 + 2 * t;
+      double* cp = p.c + row * p.ldc + col;
+      if (col + 1 < p.N) {
+        *reinterpret_cast<double2*>(cp) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else if (col < p.N) {
+        cp[0] = acc[i][j][0];
+      }
+    }
+  }
 }
 
 // variants swept by tools/gemm_once.py (PFLU_GEMM_VARIANT); the production choice is GV6

@@ -5,6 +5,7 @@ BITWISE equal to the oracle; the DMMA GEMM must match within the FP64 accumulati
 |dC| <= 2 k u sum|a||b| (stated per test).
 """
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -60,6 +61,31 @@ def test_gemm_update(cuda, m, n, k, exact):
     else:
         bound = 2 * k * U * (np.abs(a0) @ np.abs(b0)) + 4 * U * np.abs(c0)
         assert np.all(np.abs(got - want) <= bound)
+
+
+def test_gemm_update_tma_variant(cuda):
+    """The TMA-fed GEMM (PFLU_GEMM_TMA=1: cp.async.bulk.tensor + mbarrier ring, permuted k quads)
+    against the oracle, in a child process (the variant is chosen when libpflu loads)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, ctypes, numpy as np, torch; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');\n"
+        "import oracle; from paper_1804_07017_b200 import _lib as lb; L = lb.load(); U = 2.0 ** -53\n"
+        "for (m, n, k) in [(1000, 700, 256), (128, 64, 16), (3, 500, 64), (777, 130, 40), (4096, 512, 512)]:\n"
+        "    r = np.random.default_rng(m + n + k); c0 = r.standard_normal((m, n)); a0 = r.standard_normal((m, k));"
+        " b0 = r.standard_normal((k, n))\n"
+        "    want = oracle.gemm_sub(c0.copy(), a0, b0)\n"
+        "    c, a, b = (torch.from_numpy(x).cuda() for x in (c0, a0, b0))\n"
+        "    lb.check(L.pflu_gemm_update(c.data_ptr(), n, a.data_ptr(), k, b.data_ptr(), n, m, n, k, 0,"
+        " torch.cuda.current_stream().cuda_stream), 'gemm')\n"
+        "    got = c.cpu().numpy(); bound = 2 * k * U * (np.abs(a0) @ np.abs(b0)) + 4 * U * np.abs(c0)\n"
+        "    assert np.all(np.abs(got - want) <= bound), (m, n, k)\n"
+        "print('tma ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PFLU_GEMM_TMA="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "tma ok" in out.stdout, out.stderr[-2000:]
 
 
 def test_gemm_update_strided_unaligned(cuda):
