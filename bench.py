@@ -127,9 +127,10 @@ def load_traffic() -> tuple[float | None, str | None]:
         return None, None
 
 
-def cpu_sample(n: int, b: int, threads: int | None = None) -> dict:
+def cpu_sample(n: int, b: int, threads: int | None = None):
     """The oracle port (bitwise the reference's arithmetic, all host threads) on the first blocked
-    step of the same matrix; GFLOP/s = that step's flops / wall time."""
+    step of the same matrix; GFLOP/s = that step's flops / wall time.  Also returns the step's final
+    outputs (pivots [0, b) and factor rows [0, b)) for the bench's parity check."""
     import oracle
 
     cores = threads or os.cpu_count() or 1
@@ -140,9 +141,10 @@ def cpu_sample(n: int, b: int, threads: int | None = None) -> dict:
     oracle.getrf_steps_inplace(a, b, 1, piv)
     dt = time.perf_counter() - t0
     fl = oracle.step_flops(n, n, b, 0)
-    return {"value": fl / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"first blocked step (panel {n}x{b} + laswp + trsm + {n - b}^2x{b} gemm) of the n={n} "
-                      f"C4 matrix, {fl / 1e9:.1f} GFLOP in {dt:.2f} s, oracle/pflu_oracle.c -O3 OpenMP"}
+    return ({"value": fl / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
+             "sample": f"first blocked step (panel {n}x{b} + laswp + trsm + {n - b}^2x{b} gemm) of the n={n} "
+                       f"C4 matrix, {fl / 1e9:.1f} GFLOP in {dt:.2f} s, oracle/pflu_oracle.c -O3 OpenMP"},
+            piv[:b].copy(), a[:b].copy())
 
 
 def run_reference(args) -> None:
@@ -276,7 +278,21 @@ def run_single(args) -> None:
                "ms_per_step": 1e3 * statistics.mean(ts)}
         del pinned, host
 
-    cpu = None if args.no_cpu else cpu_sample(n, b)
+    cpu = None
+    parity = None
+    if not args.no_cpu:
+        cpu, ref_piv, ref_rows = cpu_sample(n, b)
+    if not args.no_check:
+        # parity of the timed run's own output (last step): the oracle's first blocked step (pivots
+        # and factor rows [0, b) are final after it) and the full backward error on the GPU
+        from paper_1804_07017_b200.cli import lu_residual_gpu
+
+        parity = {"residual": lu_residual_gpu(d_a0, d_a, piv), "residual_bound": 10.0,
+                  "residual_def": "||PA - LU||_F / (||A||_F n 2^-53), torch fp64 checker on the GPU"}
+        if not args.no_cpu:
+            amax = float(np.max(np.abs(a_host)))
+            parity["pivots_0_b_equal_oracle"] = bool(np.array_equal(piv[:b].cpu().numpy(), ref_piv))
+            parity["rows_0_b_max_abs_diff_over_amax"] = float(np.max(np.abs(d_a[:b].cpu().numpy() - ref_rows))) / amax
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -297,6 +313,7 @@ def run_single(args) -> None:
         "e2e": e2e,
         "gpu_launches": launches,
         "cpu_baseline": cpu,
+        "parity": parity,
     }
     print(json.dumps(line), flush=True)
 
@@ -312,6 +329,7 @@ def main():
     ap.add_argument("--lookahead", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip the parity check of the timed run's output")
     ap.add_argument("--dist", action="store_true", help="force the block-cyclic multi-GPU path (testing at N=1)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -110,6 +110,8 @@ static int g_pf_force = []() { const char* e = getenv("PFLU_PF_KERNEL"); return 
 // scaling model (tools/emu_scaling.py): emulate one rank of a P-GPU 1-D block-cyclic run whose
 // rank owns EVERY panel (the per-step critical path: TU_L + PF) but only 1/P of each trailing update
 static int g_emu_ranks = []() { const char* e = getenv("PFLU_EMU_RANKS"); return e ? atoi(e) : 0; }();
+// look-ahead-1 schedule with the swap+TRSM of every step overlapped with the previous GEMM
+static int g_tur_split = []() { const char* e = getenv("PFLU_TUR_SPLIT"); return e ? atoi(e) : 0; }();
 static int g_variant = []() { const char* e = getenv("PFLU_PANEL_VARIANT"); return e ? atoi(e) : 0; }();  // device buffer for panel-kernel phase clocks (tools only)
 
 // Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.
@@ -743,6 +745,111 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
       CKR(left_swaps(k, user));
       CKR(update_cols(k, grid[k].col0 + grid[k].bw, n, user, PFLU_TRACE_TU));
       if (sink && k + 1 < count) CKR((*sink)(grid[k].col0, grid[k].col0 + grid[k].bw, user));
+    }
+    return PFLU_OK;
+  }
+  // lookahead 1, split-overlap schedule (PFLU_TUR_SPLIT=1, device buffers): the trailing columns of
+  // every step are cut into a left part [lo_r, q) and a right part [q, n) at a boundary q taken from
+  // the fixed sequence n/2, 3n/4, 7n/8, ... (the first one right of lo_r), so every part is contained
+  // in one part of the previous step.  All GEMMs run in order on ONE stream (no concurrent GEMMs),
+  // all swap+TRSMs on another: the swap+TRSM of step k's left part runs while GEMM(k-1)'s right
+  // part computes, and step k's right part while GEMM(k)'s left part computes.
+  if (g_tur_split && !hin && !sink) {
+    cudaStream_t sG = c.sC[0], sS = c.sC[1];
+    std::vector<int64_t> qs;  // boundary sequence (block aligned), ascending
+    for (int64_t lo = 0, q; ; lo = q) {
+      q = std::min<int64_t>(n, ((lo + (n - lo) / 2) + b - 1) / b * b);
+      if (q <= lo || q >= n) break;
+      qs.push_back(q);
+    }
+    auto bound_of = [&](int64_t lo_r) -> int64_t {  // right end of the left part
+      for (int64_t q : qs)
+        if (q > lo_r) return q;
+      return n;
+    };
+    // events: [k][0] PF done, [k][1] TU_L done, [k][2..3] swap parts, [k][4..5] GEMM parts
+    const size_t ne = 6;
+    CKR(ctx_events(c, 2 + (size_t)count * ne));
+    auto evk = [&](int k, int i) { return c.ev[2 + (size_t)k * ne + i]; };
+    std::vector<int64_t> pb((size_t)count * 3);  // per step: lo_r, q, hi
+    for (int k = 0; k < count; ++k) {
+      const int64_t lo_r = (k + 1 < count) ? grid[k + 1].col0 + grid[k + 1].bw : n;
+      int64_t hi_r = n;
+      if (g_emu_ranks > 1) hi_r = std::min<int64_t>(n, lo_r + ((n - lo_r + g_emu_ranks - 1) / g_emu_ranks + b - 1) / b * b);
+      pb[3 * k] = lo_r;
+      pb[3 * k + 1] = std::min(bound_of(lo_r), hi_r);
+      pb[3 * k + 2] = hi_r;
+    }
+    // which part of step k contains column col (0 left, 1 right, -1 none)
+    auto part_of = [&](int k, int64_t col) -> int {
+      if (col < pb[3 * k] || col >= pb[3 * k + 2]) return -1;
+      return col < pb[3 * k + 1] ? 0 : 1;
+    };
+    cudaEvent_t ev_start = c.ev[0];
+    CK(cudaEventRecord(ev_start, user));
+    for (cudaStream_t st : {c.sP, c.sL, sG, sS}) CK(cudaStreamWaitEvent(st, ev_start, 0));
+    CKR(pf(0, c.sP));
+    CK(cudaEventRecord(evk(0, 0), c.sP));
+    for (int k = 0; k < count; ++k) {
+      const Step sk = grid[k];
+      const int np = (int)std::min(sk.bw, m - sk.col0);
+      const int64_t below = sk.col0 + sk.bw;
+      for (int part = 0; part < 2; ++part) {
+        const int64_t lo = part == 0 ? pb[3 * k] : pb[3 * k + 1], hi = part == 0 ? pb[3 * k + 1] : pb[3 * k + 2];
+        if (hi > lo) {
+          CK(cudaStreamWaitEvent(sS, evk(k, 0), 0));
+          if (k > 0)  // the GEMM(k-1) part(s) that wrote these columns
+            for (int pp = 0; pp < 2; ++pp) {
+              const int64_t plo = pp == 0 ? pb[3 * (k - 1)] : pb[3 * (k - 1) + 1];
+              const int64_t phi = pp == 0 ? pb[3 * (k - 1) + 1] : pb[3 * (k - 1) + 2];
+              if (plo < hi && lo < phi) CK(cudaStreamWaitEvent(sS, evk(k - 1, 4 + pp), 0));
+            }
+          int t_s = -1;
+          CKR(tr.begin(PFLU_TRACE_TU_R, k, sS, &t_s));
+          CKR(launch_swap(a, lda, sk.col0, np, plan_of(k), lo, hi, a + sk.col0 * lda + sk.col0, lda, true, sS,
+                          use_dinv ? inv_of(k) : nullptr));
+          CKR(tr.end(t_s, sS));
+        }
+        CK(cudaEventRecord(evk(k, 2 + part), sS));
+      }
+      for (int part = 0; part < 2; ++part) {
+        const int64_t lo = part == 0 ? pb[3 * k] : pb[3 * k + 1], hi = part == 0 ? pb[3 * k + 1] : pb[3 * k + 2];
+        if (hi > lo && below < m) {
+          CK(cudaStreamWaitEvent(sG, evk(k, 2 + part), 0));
+          int t_g = -1;
+          CKR(tr.begin(PFLU_TRACE_GEMM, k, sG, &t_g, 2.0 * (double)(m - below) * (double)(hi - lo) * (double)sk.bw));
+          CKR(launch_gemm(a + below * lda + lo, lda, a + below * lda + sk.col0, lda, a + sk.col0 * lda + lo, lda,
+                          m - below, hi - lo, sk.bw, exact, sG, g_tur_grid));
+          CKR(tr.end(t_g, sG));
+        }
+        CK(cudaEventRecord(evk(k, 4 + part), sG));
+      }
+      if (k > 0) {  // left swaps(k): every reader of L21(k-1) finished
+        CK(cudaStreamWaitEvent(c.sL, evk(k, 0), 0));
+        CK(cudaStreamWaitEvent(c.sL, evk(k - 1, 4), 0));
+        CK(cudaStreamWaitEvent(c.sL, evk(k - 1, 5), 0));
+        CK(cudaStreamWaitEvent(c.sL, evk(k - 1, 1), 0));
+        CKR(left_swaps(k, c.sL));
+      }
+      if (k + 1 < count) {
+        if (k > 0) {  // block k+1 was last updated by GEMM(k-1)
+          const int pp = part_of(k - 1, grid[k + 1].col0);
+          if (pp >= 0) CK(cudaStreamWaitEvent(c.sP, evk(k - 1, 4 + pp), 0));
+        }
+        CKR(update_cols(k, grid[k + 1].col0, grid[k + 1].col0 + grid[k + 1].bw, c.sP, PFLU_TRACE_TU_L));
+        CK(cudaEventRecord(evk(k, 1), c.sP));
+        CKR(pf(k + 1, c.sP));
+        CK(cudaEventRecord(evk(k + 1, 0), c.sP));
+      } else {
+        CK(cudaEventRecord(evk(k, 1), c.sP));
+      }
+    }
+    CK(cudaEventRecord(c.ev[1], c.sP));
+    CK(cudaStreamWaitEvent(user, c.ev[1], 0));
+    for (cudaStream_t st : {sG, sS, c.sL}) {
+      cudaEvent_t e = evk(count - 1, 2);  // reuse: recorded last on each stream in turn
+      CK(cudaEventRecord(e, st));
+      CK(cudaStreamWaitEvent(user, e, 0));
     }
     return PFLU_OK;
   }

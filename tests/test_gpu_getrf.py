@@ -254,3 +254,33 @@ def test_nan_inf_pivot_rules(cuda, lookahead):
             assert info == rinfo
             if exact:
                 assert np.array_equal(lu, ref, equal_nan=True)
+
+
+@pytest.mark.parametrize("env", [{"PFLU_TUR_SPLIT": "1"}, {"PFLU_TUR_SPLIT": "0"}])
+def test_schedule_variants_child(cuda, env):
+    """The look-ahead schedules selected when libpflu loads (split-overlap vs column-chunk dataflow)
+    in a child process: exact mode bitwise = the reference (C1 sha, a ragged case), DMMA mode the
+    reference's pivots at C1 and C2."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, json, hashlib, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')\n"
+        "import oracle; from paper_1804_07017_b200 import lu_factor\n"
+        "cf = json.load(open('tests/golden/configs.json')); pv = np.load('tests/golden/configs_pivots.npz')\n"
+        "a = np.random.default_rng(0).uniform(-1.0, 1.0, size=(2048, 2048))\n"
+        "lu, piv = lu_factor(a.copy(), b=128, lookahead=1, exact=True)\n"
+        "assert hashlib.sha256(lu.tobytes()).hexdigest() == cf['c1']['sha256_factors']\n"
+        "lu2, piv2 = lu_factor(a.copy(), b=128, lookahead=1)\n"
+        "assert np.array_equal(piv2, pv['c1']) and oracle.max_rel_diff(lu2, lu, a) <= 1e-8\n"
+        "r = np.random.default_rng(11).uniform(-1, 1, (1000, 1000)); ref, rp, _ = oracle.getrf(r, 96)\n"
+        "lu3, p3 = lu_factor(r.copy(), b=96, lookahead=1, exact=True)\n"
+        "assert lu3.tobytes() == ref.tobytes() and np.array_equal(p3, rp)\n"
+        "c2 = np.random.default_rng(1).uniform(-1.0, 1.0, size=(8192, 8192))\n"
+        "lu4, p4 = lu_factor(c2, b=256, lookahead=1)\n"
+        "assert np.array_equal(p4, pv['c2'])\n"
+        "print('schedule ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env), capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "schedule ok" in out.stdout, out.stderr[-3000:]

@@ -6,7 +6,7 @@ python bench.py > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err
 tail -1 gpurun_out/bench_$R.json
 L=$(python -c "import json;d=json.loads(open('gpurun_out/bench_$R.json').read().strip().splitlines()[-1]);print(d['gpu_launches']//d['steps'])")
 echo "launches per step: $L"
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s $((3*L)) -c $L --csv python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu > gpurun_out/launches_$R.csv 2> gpurun_out/launches_$R.err
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s $((3*L)) -c $L --csv python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu --no-check > gpurun_out/launches_$R.csv 2> gpurun_out/launches_$R.err
 tail -2 gpurun_out/launches_$R.err
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:panel_kernel -s 3 -c 1 -o gpurun_out/panel_cl_full_$R python tools/panel_once.py 32768 256 > gpurun_out/ncu_panel_full.log 2>&1
 tail -2 gpurun_out/ncu_panel_full.log
