@@ -183,8 +183,10 @@ template <int W>
 struct PanelSmem {
   static constexpr int LD = W + 1;
   static constexpr int KM = W > PF_WB ? W : PF_WB;
-  __host__ __device__ static int64_t ubuf_doubles(int w) {  // U of a leaf block (W x rest) or of a super-block (PF_WB x rest)
-    const int64_t a = (int64_t)W * (w > W ? w - W : 8), b = (int64_t)PF_WB * (w - PF_WB > 8 ? w - PF_WB : 8);
+  // U of a leaf block (W x rest) or of a super-block (PF_WB x rest), rows padded to ldu(rest)
+  __host__ __device__ static int ldu(int ncols) { return (ncols + 15) / 16 * 16 + 4; }
+  __host__ __device__ static int64_t ubuf_doubles(int w) {
+    const int64_t a = (int64_t)W * ldu(w > W ? w - W : 8), b = (int64_t)PF_WB * ldu(w - PF_WB > 8 ? w - PF_WB : 8);
     return a > b ? a : b;
   }
   static size_t bytes(int64_t R, int w, bool cl = false) {
@@ -269,13 +271,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       ll_grid_sync(sync_words, S, q, sync_flag());
     }
   };
-  int pend_kb = 0, pend_nright = 0, pend_right0 = 0;  // U rows awaiting write-back
+  int pend_kb = 0, pend_nright = 0, pend_right0 = 0, pend_ldu = 0;  // U rows awaiting write-back
   int64_t pend_cJ = 0;
   auto write_pend = [&]() {
     for (int idx = tid; idx < pend_kb * pend_nright; idx += PF_THREADS) {
       const int i = idx / pend_nright, col = idx - i * pend_nright;
       const int64_t r = pend_cJ + i;
-      if (r >= rbeg && r < rend) p.a[r * p.lda + p.col0 + pend_right0 + col] = ubuf[idx];
+      if (r >= rbeg && r < rend) p.a[r * p.lda + p.col0 + pend_right0 + col] = ubuf[i * pend_ldu + col];
     }
     pend_kb = 0;
   };
@@ -710,6 +712,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     // updates in ascending k (exact mode stays bitwise equal to the unblocked order).
     auto solve_update = [&](auto kconst, auto tconst, int64_t crow0, int kcnt, int kcol0, int c_lo, int ncols) {
       constexpr int K = decltype(kconst)::value;
+      // U rows padded to ldu = 4 (mod 16) doubles: the four k rows of a DMMA B fragment
+      // ((k4 + t) * ldu + col) then sit in four different 32-byte bank groups (conflict free)
+      const int ldu = PanelSmem<W>::ldu(ncols);
       constexpr bool a_tile = decltype(tconst)::value;  // L operand from the smem tile (else global)
       for (int idx = tid; idx < K * K; idx += PF_THREADS) {
         const int r = idx / K, cc = idx - r * K;
@@ -726,13 +731,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           for (int r = i + 1; r < K; ++r) x[r] = sub_mul_exact(x[r], ljj[r * K + i], x[i]);
         }
 #pragma unroll
-        for (int i = 0; i < K; ++i) ubuf[i * ncols + col] = x[i];
+        for (int i = 0; i < K; ++i) ubuf[i * ldu + col] = x[i];
       }
       __syncthreads();
       PF_PROF_MARK(8);
       // the owner of the U rows writes them back only after the NEXT grid sync: other CTAs may still
       // be reading the raw rows for their own (redundant) solve
-      pend_kb = kcnt; pend_cJ = crow0; pend_nright = ncols; pend_right0 = c_lo;
+      pend_kb = kcnt; pend_cJ = crow0; pend_nright = ncols; pend_right0 = c_lo; pend_ldu = ldu;
       // own rows below the pivot rows: A[r, cols] -= L[r, k-block] * U
       const int64_t ub = max(rbeg, crow0 + kcnt);
       const int nupd = (int)max((int64_t)0, rend - ub);
@@ -779,7 +784,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
 #pragma unroll
             for (int nb = 0; nb < 8; ++nb) {
               const int col = c0 + nb * 8 + g;
-              bv[nb] = (col < ncols) ? -ubuf[(k4 + t) * ncols + col] : 0.0;
+              bv[nb] = (col < ncols) ? -ubuf[(k4 + t) * ldu + col] : 0.0;
             }
 #pragma unroll
             for (int gg = 0; gg < GR; ++gg) {
@@ -809,7 +814,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           const int rl = idx / ncols, col = idx - rl * ncols;
           double* cp = p.a + (ub + rl) * p.lda + p.col0 + c_lo + col;
           double acc = *cp;
-          for (int k = 0; k < kcnt; ++k) acc = sub_mul_exact(acc, lval(rl, k), ubuf[k * ncols + col]);
+          for (int k = 0; k < kcnt; ++k) acc = sub_mul_exact(acc, lval(rl, k), ubuf[k * ldu + col]);
           *cp = acc;
         }
       }

@@ -425,7 +425,10 @@ def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
         for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"), ("MASTER_ADDR", "127.0.0.1"),
                      ("MASTER_PORT", "29533")):
             os.environ.setdefault(k, v)  # plain `python bench.py --dist`: a one-rank group
-        dist.init_process_group("nccl")
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        # device_id binds the rank to its GPU up front (no guessed rank -> device mapping)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     P, r = dist.get_world_size(), dist.get_rank()
     local = int(os.environ.get("LOCAL_RANK", r))
     dev = torch.device("cuda", local)
