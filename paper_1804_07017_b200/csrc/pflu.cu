@@ -729,7 +729,8 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     CKR(tr.begin(PFLU_TRACE_PF, k, st, &t_pf));
     pflu_options popt = opt;
     if (lookahead == 0 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;
-    if (g_emu_ranks > 1 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;  // = dist.py
+    // = dist.py: the owner's tall panels on the grid kernel from 8 ranks up (chain-bound there)
+    if (g_emu_ranks >= 8 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;
     if (g_pf_force >= 0 && opt.panel_kernel == 0) popt.panel_kernel = g_pf_force;
     CKR(panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, popt, st));
     const int np = (int)std::min(s.bw, m - s.col0);

@@ -97,13 +97,15 @@ class CudaKernels:
 
     is_cuda = True
 
-    # panels taller than this run on the cooperative-grid panel kernel (more SMs, lower latency);
-    # the panel is on every rank's critical path here, unlike on one GPU where the 16-SM cluster
-    # kernel leaves more SMs to the concurrent trailing update
+    # panels taller than grid_rows run on the cooperative-grid panel kernel (more SMs, lower latency)
+    # when the panel chain, not the per-rank trailing update, bounds the run (many ranks); with few
+    # ranks the 16-SM cluster kernel leaves more SMs to the update.  None: decided per call from P.
     GRID_PANEL_ROWS = 8192
+    GRID_MIN_RANKS = int(os.environ.get("PFLU_DIST_GRID_MIN_RANKS", "8"))  # scaling model: 2, 4 -> cluster
 
-    def __init__(self, device: torch.device, exact: bool = False):
+    def __init__(self, device: torch.device, exact: bool = False, grid_rows: int | None = None):
         self.L = _lib.load()
+        self.grid_rows = grid_rows
         self.device = device
         self.opt = _lib.options(exact=exact)
         self.opt_grid = _lib.options(exact=exact, panel_kernel=_lib.PANEL_GRID)
@@ -149,7 +151,8 @@ class CudaKernels:
         return int(v.value)
 
     def panel(self, a, m: int, d: int, col: int, w: int, piv):
-        opt = self.opt_grid if m - d > self.GRID_PANEL_ROWS else self.opt
+        gr = self.grid_rows if self.grid_rows is not None else self.GRID_PANEL_ROWS
+        opt = self.opt_grid if m - d > gr else self.opt
         rc = self.L.pflu_panel(a.data_ptr(), a.stride(0), m, d, col, w, piv.data_ptr(), None, self._st(),
                                ctypes.byref(opt))
         _lib.check(rc, "pflu_panel")
@@ -200,6 +203,8 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
     r = dist.get_rank(group)
     if kernels is None:
         kernels = CudaKernels(a_loc.device)
+    if getattr(kernels, "is_cuda", False) and kernels.grid_rows is None:
+        kernels.grid_rows = kernels.GRID_PANEL_ROWS if P >= kernels.GRID_MIN_RANKS else 1 << 62
     dev = a_loc.device
     if a_loc.shape[0] != n or a_loc.shape[1] != local_cols(n, b, P, r) or a_loc.stride(1) != 1:
         raise ValueError("a_loc must be the row-major local block-cyclic columns (n x local_cols)")
