@@ -88,7 +88,7 @@ struct DevCtx {
 };
 
 static std::atomic<long long> g_launches{0};
-static unsigned long long* g_prof = nullptr;
+static unsigned long long* g_prof = nullptr;  // device buffer for panel-kernel phase clocks (tools only)
 static int g_pf_cap = []() { const char* e = getenv("PFLU_PANEL_CAP"); return e ? atoi(e) : 32; }();
 static int g_gemm_variant = []() { const char* e = getenv("PFLU_GEMM_VARIANT"); return e ? atoi(e) : 0; }();
 static DevCtx* g_dc = nullptr;  // context of the current call (set by ctx_get)
@@ -112,7 +112,6 @@ static int g_pf_force = []() { const char* e = getenv("PFLU_PF_KERNEL"); return 
 static int g_emu_ranks = []() { const char* e = getenv("PFLU_EMU_RANKS"); return e ? atoi(e) : 0; }();
 // look-ahead-1 schedule with the swap+TRSM of every step overlapped with the previous GEMM
 static int g_tur_split = []() { const char* e = getenv("PFLU_TUR_SPLIT"); return e ? atoi(e) : 0; }();
-static int g_variant = []() { const char* e = getenv("PFLU_PANEL_VARIANT"); return e ? atoi(e) : 0; }();  // device buffer for panel-kernel phase clocks (tools only)
 
 // Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.
 struct Tracer {
