@@ -10,7 +10,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpflu.so")
+LIB_PATH = os.environ.get("PFLU_LIB_PATH") or os.path.join(_HERE, "libpflu.so")
 
 PFLU_OK = 0
 PFLU_ERR_CUDA = 1
