@@ -192,8 +192,12 @@ class CudaKernels:
 # the distributed driver
 
 def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, kernels=None, group=None,
-                       piv: torch.Tensor | None = None):
+                       piv: torch.Tensor | None = None, row_sink=None):
     """Factor the block-cyclic distributed n x n matrix in place.
+
+    ``row_sink(r0, r1, events)`` (CUDA only, optional) is called once per step as soon as local rows
+    [r0, r1) are final (their trailing update, TU_L and left swaps are enqueued); ``events`` are the
+    CUDA events to wait for -- lu_factor_local streams those rows back to the host with it.
 
     ``a_loc``: this rank's local columns (row-major, n rows, ``local_cols(n, b, P, rank)`` columns).
     Returns ``(piv, info)``: the full 0-based pivot vector (identical on every rank) and the
@@ -273,6 +277,10 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
                 buf = pf_pack_bcast(k)
                 left_swaps(k)
                 update(k, buf, cols_before(k + 1), ncl)
+                if row_sink is not None:
+                    e = kernels.event()
+                    kernels.record(e, "P")
+                    row_sink(k * b, min(n, (k + 1) * b), [e])
     else:
         bufs = {}
         with kernels.stream("P"):
@@ -288,14 +296,24 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
                 update(k, bufs[k], lo_r, ncl)
                 left_swaps(k)
                 kernels.record(ev_tu[k % 2], "U")
+            e_tl = None
             if nxt:
                 with kernels.stream("P"):
                     if k > 0:
                         kernels.wait(ev_tu[(k - 1) % 2], "P")
                     if own_next:
                         update(k, bufs[k], cols_before(k + 1), cols_before(k + 2))
+                        if row_sink is not None:
+                            e_tl = kernels.event()
+                            kernels.record(e_tl, "P")
                     bufs[k + 1] = pf_pack_bcast(k + 1)
                     kernels.record(ev_bc[(k + 1) % 2], "P")
+            if row_sink is not None:
+                # rows of block row k are final once TU_R(k) + left swaps(k) (U) and TU_L(k) (P) are
+                # done: later steps only touch rows below
+                e_u = kernels.event()
+                kernels.record(e_u, "U")
+                row_sink(k * b, min(n, (k + 1) * b), [e_u] + ([e_tl] if e_tl is not None else []))
             bufs.pop(k - 1, None)
     if kernels.is_cuda:
         kernels.join()
@@ -389,9 +407,18 @@ def lu_factor_local(a_loc, n: int, b: int = 256, lookahead: int = 1, exact: bool
         return (t, piv, info) if return_info else (t, piv)
     d = torch.empty(t.shape, dtype=torch.float64, device=dev)
     d.copy_(t, non_blocking=True)
-    piv, info = getrf_block_cyclic(d, n, b, lookahead, CudaKernels(dev, exact=exact))
-    t.copy_(d, non_blocking=True)
+    # every block row streams back to the host as soon as it is final (D2H overlaps the rest)
+    cs = torch.cuda.Stream(device=dev)
+
+    def sink(r0, r1, events):
+        for e in events:
+            cs.wait_event(e)
+        with torch.cuda.stream(cs):
+            t[r0:r1].copy_(d[r0:r1], non_blocking=True)
+
+    piv, info = getrf_block_cyclic(d, n, b, lookahead, CudaKernels(dev, exact=exact), row_sink=sink)
     piv_h = piv.cpu()
+    cs.synchronize()
     torch.cuda.synchronize()
     out_piv = piv_h.numpy() if not isinstance(a_loc, torch.Tensor) else piv_h
     return (a_loc, out_piv, info) if return_info else (a_loc, out_piv)
