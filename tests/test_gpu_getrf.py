@@ -284,3 +284,44 @@ def test_schedule_variants_child(cuda, env):
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env), capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "schedule ok" in out.stdout, out.stderr[-3000:]
+
+
+@pytest.mark.parametrize("lookahead", [0, 1])
+def test_trace_hook(cuda, lookahead):
+    """The reference's trace semantics (factor.py:104-122, test_factor.py:423-441): a PF record for every
+    step, TU (depth 0) or TU_L/TU_R (depth 1) records, ordered timestamps; the GEMM records carry the
+    trailing update's algorithmic flops."""
+    import torch
+    from paper_1804_07017_b200 import getrf_device
+
+    n, b = 1000, 128
+    a = torch.from_numpy(np.random.default_rng(21).uniform(-1, 1, (n, n))).cuda()
+    tr = []
+    piv, info = getrf_device(a, b, lookahead, trace=tr)
+    steps = -(-n // b)
+    assert info == 0
+    pf = sorted(e.k for e in tr if e.label == "PF")
+    assert pf == list(range(steps))
+    for e in tr:
+        assert 0.0 <= e.start <= e.end
+    pf_ev = {e.k: e for e in tr if e.label == "PF"}
+    for k in range(1, steps):
+        assert pf_ev[k].start >= pf_ev[k - 1].end - 1e-6      # panels are a chain
+    gemm = sum(e.flop for e in tr if e.label == "GEMM")
+    if lookahead == 0:
+        assert sorted(e.k for e in tr if e.label == "TU") == list(range(steps - 1))  # the last has no trailing columns
+        want = sum(2.0 * (n - (k + 1) * b) ** 2 * b for k in range(steps) if (k + 1) * b < n)
+    else:
+        assert sorted(e.k for e in tr if e.label == "TU_L") == list(range(steps - 1))
+        assert {e.k for e in tr if e.label == "TU_R"} <= set(range(steps))
+        want = sum(2.0 * (n - (k + 1) * b) * (n - (k + 2) * b) * b for k in range(steps) if (k + 2) * b < n)
+    assert gemm == pytest.approx(want, rel=1e-12)
+
+
+def test_multipliers_bounded(cuda):
+    """Partial pivoting keeps every multiplier |l| <= 1 (+ rounding), test_factor.py:48-53 / 391-398 --
+    in the DMMA path too."""
+    a0 = config_matrix("c1")
+    lu, piv, _ = run(a0, 128, 1, exact=False)
+    low = np.tril(lu, -1)
+    assert np.max(np.abs(low)) <= 1.0 + 4 * oracle.UNIT_ROUNDOFF
