@@ -395,6 +395,7 @@ static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, con
       case 13: CKR(launch_gemm_p<GV3>(*g_dc, p, v2, 0, st)); break;
       case 16: CKR(launch_gemm_p<GV6>(*g_dc, p, v2, 0, st)); break;
       case 8: CKR(launch_gemm_t<GV8>(p, v2, st)); break;
+      case 9: CKR(launch_gemm_t<GV9>(p, v2, st)); break;
       case 40: CKR(launch_gemm_t<GV0>(p, v2, st)); break;
       case 17: CKR(launch_gemm_p<GV7>(*g_dc, p, v2, 0, st)); break;
       case 20: CKR(launch_gemm_p<GV0>(*g_dc, p, v2, g_dc->sms, st)); break;

@@ -521,5 +521,6 @@ using GV5 = GemmCfg<256, 64, 16, 3, 4, 2>;   // 8 warps of 64x32, tall tile
 using GV6 = GemmCfg<128, 64, 32, 2, 2, 2>;   // 4 warps of 64x32, K stage 32 double-buffered, 2 CTAs/SM
 using GV7 = GemmCfg<64, 64, 32, 3, 2, 2>;    // 4 warps of 32x32, K stage 32, 2 CTAs/SM
 using GV8 = GemmCfg<128, 64, 32, 2, 4, 2>;   // 8 warps of 32x32, K stage 32 double-buffered, 2 CTAs/SM
+using GV9 = GemmCfg<128, 32, 16, 2, 2, 1>;   // 2 warps of 64x32 per CTA, 40 KB: 4 independent CTAs/SM
 
 }  // namespace pflu
