@@ -665,7 +665,7 @@ struct HostIn {
   int64_t lda;
   int chunks;
 };
-static int g_h2d_chunks = []() { const char* e = getenv("PFLU_H2D_CHUNKS"); return e ? atoi(e) : 4; }();
+static int g_h2d_chunks = []() { const char* e = getenv("PFLU_H2D_CHUNKS"); return e ? atoi(e) : 6; }();  // e2e: 4 -> 819.5, 5 -> 815.5, 6 -> 812.9, 8 -> 891 ms
 
 static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
                        int64_t* piv, unsigned long long* info, cudaStream_t user, const pflu_options& opt,
