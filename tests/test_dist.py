@@ -55,7 +55,7 @@ def _run(tmp_path, world, n, b, lookahead, seed=0, singular=False):
 
 
 @pytest.mark.parametrize("world,n,b,lookahead", [(2, 96, 16, 1), (2, 100, 16, 0), (3, 101, 8, 1), (2, 64, 64, 1),
-                                                 (3, 40, 16, 1)])
+                                                 (3, 40, 16, 1), (4, 150, 16, 1), (4, 72, 8, 0)])
 def test_block_cyclic_matches_reference_bitwise(tmp_path, world, n, b, lookahead):
     import oracle
 
