@@ -175,7 +175,7 @@ def run_reference(args) -> None:
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"C4: LUpp n={n} U[-1,1) seed 3, b={b}, look-ahead 1",
                    "sample": "first blocked step of C4 per step"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -295,7 +295,7 @@ def run_single(args) -> None:
             parity["rows_0_b_max_abs_diff_over_amax"] = float(np.max(np.abs(d_a[:b].cpu().numpy() - ref_rows))) / amax
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"C4: LUpp n={n} U[-1,1) numpy seed 3, b={b}, look-ahead {la}",
                    "n": n, "b": b, "lookahead": la, "parallelism": "single GPU",
