@@ -111,6 +111,8 @@ static int g_pf_force = []() { const char* e = getenv("PFLU_PF_KERNEL"); return 
 // rank owns EVERY panel (the per-step critical path: TU_L + PF) but only 1/P of each trailing update
 static int g_emu_ranks = []() { const char* e = getenv("PFLU_EMU_RANKS"); return e ? atoi(e) : 0; }();
 // look-ahead-1 schedule with the swap+TRSM of every step overlapped with the previous GEMM
+// DMMA swap+TRSM strip width for blocks of <= 256 rows (32 or 16 columns per CTA)
+static int g_swap_bn = []() { const char* e = getenv("PFLU_SWAP_BN"); return e ? atoi(e) : 16; }();  // C4: 16 -> 764.5, 32 -> 769.2 ms
 static int g_tur_split = []() { const char* e = getenv("PFLU_TUR_SPLIT"); return e ? atoi(e) : 0; }();
 
 // Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.
@@ -233,6 +235,7 @@ static int ctx_get(DevCtx** out) {
       }
     CK(allow((const void*)swap_trsm_kernel<8>));
     CK(allow((const void*)swap_trsm_dmma_kernel<256, 32>));
+    CK(allow((const void*)swap_trsm_dmma_kernel<256, 16>));
     CK(allow((const void*)swap_trsm_dmma_kernel<512, 16>));
     CK(allow((const void*)swap_trsm_kernel<16>));
     CK(allow((const void*)swap_trsm_kernel<32>));
@@ -453,7 +456,10 @@ static int launch_swap(double* a, int64_t lda, int64_t d, int np, const int64_t*
                        const double* L, int64_t ldl, bool do_trsm, cudaStream_t st, const double* inv = nullptr) {
   if (c1 <= c0 || np <= 0) return PFLU_OK;
   const int t = do_trsm ? 1 : 0;
-  if (do_trsm && inv && np <= 256) {
+  if (do_trsm && inv && np <= 256 && g_swap_bn == 16) {
+    swap_trsm_dmma_kernel<256, 16><<<(unsigned)((c1 - c0 + 15) / 16), 256, SdCfg<256, 16>::SMEM, st>>>(
+        a, lda, d, np, plan, c0, c1, L, ldl, inv);
+  } else if (do_trsm && inv && np <= 256) {
     swap_trsm_dmma_kernel<256, 32><<<(unsigned)((c1 - c0 + 31) / 32), 256, SdCfg<256, 32>::SMEM, st>>>(
         a, lda, d, np, plan, c0, c1, L, ldl, inv);
   } else if (do_trsm && inv && np <= 512) {
