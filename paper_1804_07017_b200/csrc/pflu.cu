@@ -113,6 +113,8 @@ static int g_emu_ranks = []() { const char* e = getenv("PFLU_EMU_RANKS"); return
 // look-ahead-1 schedule with the swap+TRSM of every step overlapped with the previous GEMM
 // DMMA swap+TRSM strip width for blocks of <= 256 rows (32 or 16 columns per CTA)
 static int g_swap_bn = []() { const char* e = getenv("PFLU_SWAP_BN"); return e ? atoi(e) : 16; }();  // C4: 16 -> 764.5, 32 -> 769.2 ms
+// strip width of the pure row-permutation kernel (deferred left swaps): 16 or 32 columns
+static int g_lswap_tw = []() { const char* e = getenv("PFLU_LSWAP_TW"); return e ? atoi(e) : 16; }();
 static int g_tur_split = []() { const char* e = getenv("PFLU_TUR_SPLIT"); return e ? atoi(e) : 0; }();
 
 // Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.
@@ -465,6 +467,14 @@ static int launch_swap(double* a, int64_t lda, int64_t d, int np, const int64_t*
   } else if (do_trsm && inv && np <= 512) {
     swap_trsm_dmma_kernel<512, 16><<<(unsigned)((c1 - c0 + 15) / 16), 256, SdCfg<512, 16>::SMEM, st>>>(
         a, lda, d, np, plan, c0, c1, L, ldl, inv);
+  } else if (!do_trsm && np <= 256 && g_lswap_tw == 8) {
+    size_t smem = (size_t)(np * 8 + std::max(np * 8, 1024)) * 8;
+    swap_trsm_kernel<8><<<(unsigned)((c1 - c0 + 7) / 8), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl, t);
+  } else if (!do_trsm && np <= 256 && g_lswap_tw == 16) {
+    // pure row permutation (the deferred left swaps, concurrent with the trailing GEMM): 16-column
+    // strips (one 128-byte line per row), 64 KB of staging -> 3 CTAs per SM, twice the CTAs
+    size_t smem = (size_t)(np * 16 + std::max(np * 16, 1024)) * 8;
+    swap_trsm_kernel<16><<<(unsigned)((c1 - c0 + 15) / 16), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl, t);
   } else if (np <= 256) {
     size_t smem = (size_t)(np * 32 + std::max(np * 32, 1024)) * 8;
     swap_trsm_kernel<32><<<(unsigned)((c1 - c0 + 31) / 32), 256, smem, st>>>(a, lda, d, np, plan, c0, c1, L, ldl, t);
