@@ -887,7 +887,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     return ch;
   };
   const size_t nev = 2 + (size_t)count * (nch + 2);
-  CKR(ctx_events(c, nev + nch));
+  CKR(ctx_events(c, nev + nch + 1));
   cudaEvent_t ev_start = c.ev[0];
   auto ev_pf = [&](int k) { return c.ev[2 + (size_t)k * (nch + 2)]; };
   auto ev_tul = [&](int k) { return c.ev[3 + (size_t)k * (nch + 2)]; };
@@ -897,14 +897,20 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   CK(cudaStreamWaitEvent(c.sL, ev_start, 0));
   for (int ch = 0; ch < nch; ++ch) CK(cudaStreamWaitEvent(c.sC[ch], ev_start, 0));
   if (hin) {  // per-chunk H2D on `user`, in column order
+    // the first two block columns go first, on their own: PF(0), TU_L(0) and PF(1) touch only them,
+    // so the panel chain starts while the rest of the first chunk is still in flight
+    const int64_t head = std::min<int64_t>(n, 2 * b);
+    CK(cudaMemcpy2DAsync(a, lda * 8, hin->a, hin->lda * 8, head * 8, m, cudaMemcpyHostToDevice, user));
+    CK(cudaEventRecord(c.ev[nev + nch], user));
+    CK(cudaStreamWaitEvent(c.sP, c.ev[nev + nch], 0));
     for (int ch = 0; ch < nch; ++ch) {
-      const int64_t lo = (int64_t)chunk_blk[ch] * b, hi = std::min<int64_t>(n, (int64_t)chunk_blk[ch + 1] * b);
+      const int64_t lo = std::max<int64_t>(head, (int64_t)chunk_blk[ch] * b);
+      const int64_t hi = std::min<int64_t>(n, (int64_t)chunk_blk[ch + 1] * b);
       if (hi > lo)
         CK(cudaMemcpy2DAsync(a + lo, lda * 8, hin->a + lo, hin->lda * 8, (hi - lo) * 8, m, cudaMemcpyHostToDevice, user));
       cudaEvent_t e = c.ev[nev + ch];
       CK(cudaEventRecord(e, user));
       CK(cudaStreamWaitEvent(c.sC[ch], e, 0));
-      if (ch == 0 || ch == chunk_of_block(std::min(1, count - 1))) CK(cudaStreamWaitEvent(c.sP, e, 0));
     }
   }
   CKR(pf(0, c.sP));
