@@ -115,6 +115,7 @@ static int g_emu_ranks = []() { const char* e = getenv("PFLU_EMU_RANKS"); return
 static int g_swap_bn = []() { const char* e = getenv("PFLU_SWAP_BN"); return e ? atoi(e) : 16; }();  // C4: 16 -> 764.5, 32 -> 769.2 ms
 // strip width of the pure row-permutation kernel (deferred left swaps): 16 or 32 columns
 static int g_lswap_tw = []() { const char* e = getenv("PFLU_LSWAP_TW"); return e ? atoi(e) : 16; }();
+static int g_emu_grid_ranks = []() { const char* e = getenv("PFLU_EMU_GRID_RANKS"); return e ? atoi(e) : 8; }();
 static int g_tur_split = []() { const char* e = getenv("PFLU_TUR_SPLIT"); return e ? atoi(e) : 0; }();
 
 // Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.
@@ -746,7 +747,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     pflu_options popt = opt;
     if (lookahead == 0 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;
     // = dist.py: the owner's tall panels on the grid kernel from 8 ranks up (chain-bound there)
-    if (g_emu_ranks >= 8 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;
+    if (g_emu_ranks >= g_emu_grid_ranks && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;
     if (g_pf_force >= 0 && opt.panel_kernel == 0) popt.panel_kernel = g_pf_force;
     CKR(panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, popt, st));
     const int np = (int)std::min(s.bw, m - s.col0);
