@@ -12,3 +12,8 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:pane
 tail -2 gpurun_out/ncu_panel_full.log
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_dmma -s 2 -c 1 -o gpurun_out/gemm_full_$R python tools/gemm_once.py 32512 32512 256 1 > gpurun_out/ncu_gemm_full.log 2>&1
 tail -2 gpurun_out/ncu_gemm_full.log
+# TRSM (FP64 pipe) and laswp (HBM) evidence: one launch each, tools/swap_dmma_once.py
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:swap_trsm_dmma -s 2 -c 1 -o gpurun_out/trsm_full_$R python tools/swap_dmma_once.py > gpurun_out/ncu_trsm_full.log 2>&1
+tail -2 gpurun_out/ncu_trsm_full.log
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:swap_trsm_kernel -s 2 -c 1 -o gpurun_out/lswap_full_$R python tools/swap_dmma_once.py > gpurun_out/ncu_lswap_full.log 2>&1
+tail -2 gpurun_out/ncu_lswap_full.log
