@@ -56,6 +56,14 @@ def lib():
         L.orc_getrf.argtypes = [_d, _I64, _I64, _I64, _I64, _i]
         L.orc_getrf_steps.restype = _I64
         L.orc_getrf_steps.argtypes = [_d, _I64, _I64, _I64, _I64, _i, _I64]
+        L.orc_qr_unb.restype = None
+        L.orc_qr_unb.argtypes = [_d, _I64, _I64, _I64, _d]
+        L.orc_larft.restype = None
+        L.orc_larft.argtypes = [_d, _I64, _I64, _I64, _d, _d]
+        L.orc_apply_block_reflector.restype = None
+        L.orc_apply_block_reflector.argtypes = [_d, _I64, _I64, _I64, _d, _d, _I64, _I64]
+        L.orc_geqrf_steps.restype = None
+        L.orc_geqrf_steps.argtypes = [_d, _I64, _I64, _I64, _I64, _d, _I64]
         L.orc_set_threads.restype = None
         L.orc_set_threads.argtypes = [ctypes.c_int]
         _LIB = L
@@ -201,3 +209,99 @@ def max_rel_diff(lu_a, lu_b, a0) -> float:
     """max |LU_a - LU_b| / ||A||_max (north_star's second parity measure)."""
     amax = float(np.max(np.abs(a0)))
     return float(np.max(np.abs(np.asarray(lu_a) - np.asarray(lu_b)))) / (amax if amax else 1.0)
+
+
+# ---------------------------------------------------------------------------------------
+# Householder QR (Kind.QR; reference factor.py:147-205, _jit.py:190-218, oracle.py:90-127)
+
+def qr_unb(a):
+    """In place unblocked Householder QR of a row-major m x w panel (m >= w) (reference
+    _jit.py:190-218, bitwise).  Returns (a, tau)."""
+    a = _rowmajor(a)
+    m, w = a.shape
+    tau = np.zeros(w)
+    lib().orc_qr_unb(_dp(a), m, w, w, _dp(tau))
+    return a, tau
+
+
+def larft(v, tau):
+    """T (k x k upper) with I - V T V^T = H_1 ... H_k for the reflectors stored in v
+    (reference factor.py:174-189, same loop order; the reference's products use BLAS)."""
+    v = _rowmajor(v)
+    tau = np.ascontiguousarray(tau, dtype=np.float64)
+    m, k = v.shape
+    t = np.zeros((k, k))
+    lib().orc_larft(_dp(v), m, k, k, _dp(tau), _dp(t))
+    return t
+
+
+def geqrf(a, b: int, nsteps: int = -1):
+    """Blocked Householder QR (reference dmf_mtb / dmf_la with Kind.QR) on a COPY of `a`.
+    Returns (factors row-major: R on/above the diagonal, reflectors below; tau float64[n])."""
+    a = np.array(a, dtype=np.float64, order="C", copy=True)
+    m, n = a.shape
+    if m < n or n < 1:
+        raise ValueError("factorizations require a square or tall, non-empty matrix")
+    tau = np.zeros(n)
+    lib().orc_geqrf_steps(_dp(a), m, n, n, int(b), _dp(tau), int(nsteps))
+    return a, tau
+
+
+def apply_qt(f, tau, c, block: int = 256):
+    """Q^T c for the stored reflectors (f, tau), reflector by reflector in blocks (numpy)."""
+    f = np.asarray(f, dtype=np.float64)
+    c = np.array(c, dtype=np.float64, copy=True)
+    m = f.shape[0]
+    for j0 in range(0, len(tau), block):
+        j1 = min(len(tau), j0 + block)
+        for j in range(j0, j1):
+            t = tau[j]
+            if t == 0.0:
+                continue
+            v = np.empty(m - j)
+            v[0] = 1.0
+            v[1:] = f[j + 1:, j]
+            w = v @ c[j:]
+            c[j:] -= t * np.outer(v, w)
+    return c
+
+
+def form_q(f, tau) -> np.ndarray:
+    """m x m orthogonal factor H_1 ... H_k (reference oracle.py:90-110)."""
+    f = np.asarray(f, dtype=np.float64)
+    m = f.shape[0]
+    q = np.eye(m)
+    for j in range(len(tau) - 1, -1, -1):
+        t = tau[j]
+        if t == 0.0:
+            continue
+        v = np.zeros(m - j)
+        v[0] = 1.0
+        v[1:] = f[j + 1:, j]
+        w = q[j:, :].T @ v
+        q[j:, :] -= t * np.outer(v, w)
+    return q
+
+
+def qr_residual(a0, f, tau):
+    """(||A - Q R||_F / (n u ||A||_F), ||Q^T Q - I||_F / (n u)) (reference oracle.py:113-127)."""
+    a0 = np.asarray(a0, dtype=np.float64)
+    f = np.asarray(f, dtype=np.float64)
+    n = max(a0.shape[1], 1)
+    q = form_q(f, tau)
+    r = np.triu(f)
+    norm_a = np.linalg.norm(a0)
+    err = np.linalg.norm(a0 - q @ r)
+    factor = err / (n * UNIT_ROUNDOFF * norm_a) if norm_a else err
+    ortho = np.linalg.norm(q.T @ q - np.eye(q.shape[0])) / (n * UNIT_ROUNDOFF)
+    return float(factor), float(ortho)
+
+
+def qr_backward_error(a0, f, tau) -> float:
+    """||Q^T A - R||_F / (n u ||A||_F) without forming Q (large sizes)."""
+    a0 = np.asarray(a0, dtype=np.float64)
+    n = max(a0.shape[1], 1)
+    d = apply_qt(f, tau, a0) - np.triu(np.asarray(f))
+    norm_a = np.linalg.norm(a0)
+    err = np.linalg.norm(d)
+    return float(err / (n * UNIT_ROUNDOFF * norm_a)) if norm_a else float(err)

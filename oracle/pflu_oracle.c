@@ -27,6 +27,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 #include <omp.h>
 
@@ -182,4 +183,118 @@ int64_t orc_getrf(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, int64
  * of a factorization too large to run completely on the host (C4/C5). */
 int64_t orc_lu_prefix(double *a, int64_t m, int64_t n, int64_t lda, int64_t *piv, int64_t steps) {
   return orc_lu_unb(a, m, n, lda, piv, steps);
+}
+
+/* ==========================================================================================
+ * Householder QR (Kind.QR), SURVEY.md §8(f) row 4.  Same storage conventions (row-major).
+ *   orc_qr_unb    <- _jit.py:190-218 (qr_unb_run: beta opposite in sign to the leading entry,
+ *                    tau = (beta - alpha) / beta, v scaled by 1 / (alpha - beta), each reflector
+ *                    applied to the panel's later columns as s = a_jc + sum v_i a_ic (i
+ *                    ascending), s *= tau, a -= s v).  Pinned bitwise to the reference.
+ *   orc_larft     <- factor.py:174-189 (larft_forward_columnwise: T[j,j] = tau_j,
+ *                    T[:j,j] = -tau_j T[:j,:j] (V[:,:j]^T v_j)).  The reference evaluates the two
+ *                    products with numpy/BLAS, so this loop order matches it only to rounding.
+ *   orc_apply_block_reflector <- factor.py:192-205 + kernels.py:249-270 + _jit.py:54-80 and
+ *                    the trmm_upper_run loop (W = 0 + V^T C p ascending; W = T^T W zero-seeded,
+ *                    l ascending; C += V (-W) p ascending, multiply then add).
+ *   orc_geqrf     <- dmf_mtb (factor.py:382-412) with kind=Kind.QR: per panel qr_unb + larft,
+ *                    then the block reflector on the columns to the right.
+ */
+void orc_qr_unb(double *a, int64_t m, int64_t w, int64_t lda, double *tau) {
+  for (int64_t j = 0; j < w; ++j) {
+    const double alpha = a[IDX(j, j, lda)];
+    double sq = 0.0;
+    for (int64_t i = j + 1; i < m; ++i) { double v = a[IDX(i, j, lda)]; double t = v * v; sq = sq + t; }
+    if (sq == 0.0) { tau[j] = 0.0; continue; }
+    double aa = alpha * alpha;
+    const double norm = sqrt(aa + sq);
+    const double beta = alpha >= 0.0 ? -norm : norm;
+    tau[j] = (beta - alpha) / beta;
+    const double scale = 1.0 / (alpha - beta);
+    for (int64_t i = j + 1; i < m; ++i) a[IDX(i, j, lda)] *= scale;
+    a[IDX(j, j, lda)] = beta;
+    for (int64_t c = j + 1; c < w; ++c) {
+      double s = a[IDX(j, c, lda)];
+      for (int64_t i = j + 1; i < m; ++i) { double t = a[IDX(i, j, lda)] * a[IDX(i, c, lda)]; s = s + t; }
+      s = s * tau[j];
+      a[IDX(j, c, lda)] -= s;
+      for (int64_t i = j + 1; i < m; ++i) { double t = s * a[IDX(i, j, lda)]; a[IDX(i, c, lda)] -= t; }
+    }
+  }
+}
+
+/* v(i, j) of the stored reflectors: unit diagonal, zero above, the panel below. */
+static inline double vref(const double *v, int64_t ldv, int64_t i, int64_t j) {
+  return i > j ? v[IDX(i, j, ldv)] : (i == j ? 1.0 : 0.0);
+}
+
+/* T (k x k row-major, upper) from the reflectors stored in the m x k panel v and tau. */
+void orc_larft(const double *v, int64_t m, int64_t k, int64_t ldv, const double *tau, double *t) {
+  for (int64_t i = 0; i < k * k; ++i) t[i] = 0.0;
+  double *wv = (double *)calloc((size_t)(k > 0 ? k : 1), sizeof(double));
+  for (int64_t j = 0; j < k; ++j) {
+    t[IDX(j, j, k)] = tau[j];
+    if (!j) continue;
+    for (int64_t l = 0; l < j; ++l) {
+      double s = 0.0;
+      for (int64_t i = 0; i < m; ++i) { double p = vref(v, ldv, i, l) * vref(v, ldv, i, j); s = s + p; }
+      wv[l] = s;
+    }
+    for (int64_t i = 0; i < j; ++i) {
+      double s = 0.0;
+      for (int64_t l = i; l < j; ++l) { double p = t[IDX(i, l, k)] * wv[l]; s = s + p; }
+      t[IDX(i, j, k)] = -tau[j] * s;
+    }
+  }
+  free(wv);
+}
+
+/* c (m x nc) <- (I - V T V^T)^T c = c - V (T^T (V^T c)). */
+void orc_apply_block_reflector(const double *v, int64_t m, int64_t k, int64_t ldv, const double *t,
+                               double *c, int64_t nc, int64_t ldc) {
+  if (m <= 0 || nc <= 0 || k <= 0) return;
+  double *w = (double *)calloc((size_t)(k * nc), sizeof(double));
+  double *z = (double *)calloc((size_t)(k * nc), sizeof(double));
+  int nt = nthreads();
+#pragma omp parallel for num_threads(nt) schedule(static) if (m * nc * k > 1000000)
+  for (int64_t j = 0; j < nc; ++j) {
+    for (int64_t r = 0; r < k; ++r) {          /* W = 0 + V^T C */
+      double acc = 0.0;
+      for (int64_t p = 0; p < m; ++p) { double q = vref(v, ldv, p, r) * c[IDX(p, j, ldc)]; acc = acc + q; }
+      w[IDX(r, j, nc)] = acc;
+    }
+    for (int64_t l = 0; l < k; ++l) {          /* Z = T^T W, zero-seeded, l ascending */
+      const double xv = w[IDX(l, j, nc)];
+      for (int64_t i = l; i < k; ++i) { double q = t[IDX(l, i, k)] * xv; z[IDX(i, j, nc)] = z[IDX(i, j, nc)] + q; }
+    }
+    for (int64_t i = 0; i < k; ++i) z[IDX(i, j, nc)] = -z[IDX(i, j, nc)];
+    for (int64_t i = 0; i < m; ++i) {          /* C += V (-Z), p ascending */
+      double acc = c[IDX(i, j, ldc)];
+      for (int64_t p = 0; p < k; ++p) { double q = vref(v, ldv, i, p) * z[IDX(p, j, nc)]; acc = acc + q; }
+      c[IDX(i, j, ldc)] = acc;
+    }
+  }
+  free(w);
+  free(z);
+}
+
+/* Blocked Householder QR, dmf_mtb order.  m >= n >= 1.  tau: double[n]. */
+void orc_geqrf_steps(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, double *tau, int64_t nsteps) {
+  int64_t step = 0;
+  for (int64_t col0 = 0; col0 < n && (nsteps < 0 || step < nsteps); col0 += b, ++step) {
+    const int64_t bw = n - col0 < b ? n - col0 : b;
+    double *panel = a + IDX(col0, col0, lda);
+    orc_qr_unb(panel, m - col0, bw, lda, tau + col0);
+    const int64_t lo = col0 + bw;
+    if (lo < n) {
+      double *t = (double *)malloc((size_t)(bw * bw) * sizeof(double));
+      orc_larft(panel, m - col0, bw, lda, tau + col0, t);
+      orc_apply_block_reflector(panel, m - col0, bw, lda, t, a + IDX(col0, lo, lda), n - lo, lda);
+      free(t);
+    }
+  }
+}
+
+void orc_geqrf(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, double *tau) {
+  orc_geqrf_steps(a, m, n, lda, b, tau, -1);
 }
