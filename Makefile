@@ -2,7 +2,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 NVFLAGS = -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -std=c++17 --shared -Xcompiler -fPIC
 SRC = paper_1804_07017_b200/csrc/pflu.cu
-HDR = paper_1804_07017_b200/csrc/pflu_kernels.cuh paper_1804_07017_b200/csrc/pflu_panel.cuh paper_1804_07017_b200/csrc/pflu_gemm.cuh include/pflu.h
+HDR = paper_1804_07017_b200/csrc/pflu_kernels.cuh paper_1804_07017_b200/csrc/pflu_panel.cuh paper_1804_07017_b200/csrc/pflu_gemm.cuh paper_1804_07017_b200/csrc/pflu_qr.cuh include/pflu.h
 
 all: paper_1804_07017_b200/libpflu.so oracle/liboracle.so
 

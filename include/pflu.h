@@ -146,6 +146,46 @@ int pflu_trsm(const double* d_l, int64_t ldl, int64_t nb, double* d_x, int64_t l
 int pflu_gemm_update(double* d_c, int64_t ldc, const double* d_a, int64_t lda, const double* d_b,
                      int64_t ldb, int64_t m, int64_t n, int64_t k, int exact, void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Householder QR (Kind.QR of dmf_mtb / dmf_la).  Same row-major storage;
+ * the factors overwrite a in place: R on and above the diagonal, the Householder vectors' tails
+ * below it (unit heads implicit), tau[j] the scalar of reflector j (H_j = I - tau_j v_j v_j^T;
+ * tau_j = 0 is a null reflector for a column that is already zero below the diagonal).
+ * Reference interfaces replaced (pkg/src/panelforge/...):
+ *   pflu_geqrf / pflu_geqrf_device  <- dmf_mtb (factor.py:382-412, lookahead=0) and dmf_la
+ *                                      (factor.py:455-515, lookahead=1) with kind=Kind.QR,
+ *                                      returning QrOutput (factor.py:65-72)
+ *   pflu_qr_panel                   <- qr_unb + _jit.qr_unb_run (factor.py:147-161; _jit.py:190-218)
+ *   pflu_larft                      <- larft_forward_columnwise (factor.py:174-189)
+ *   pflu_apply_block_reflector      <- apply_block_reflector (factor.py:192-205)
+ * Block sizes up to 1024.  Results agree with the reference to rounding (the reference's own T is
+ * formed with numpy/BLAS products), not bitwise. */
+
+/* Whole factorization, HOST buffers (H2D, factorization, D2H).  a: m x n row-major (m >= n >= 1,
+ * lda >= n), overwritten in place; tau: double[n] host. */
+int pflu_geqrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, double* tau);
+
+/* Whole factorization, DEVICE buffers on the current device, ordered on `stream`; blocks until done.
+ * d_tau: double[n] device. */
+int pflu_geqrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, double* d_tau,
+                      void* stream);
+
+/* Householder factorization of the panel rows [d, m) x columns [col, col + w) (the diagonal of
+ * panel column j is row d + j; w <= m - d), in place; d_tau[0 .. w) receives the scalars.
+ * Asynchronous on `stream`. */
+int pflu_qr_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w, double* d_tau,
+                  void* stream);
+
+/* T (k x k, upper, ld ldt, device) with H_1 ... H_k = I - V T V^T for the reflectors stored in the
+ * mp x k panel d_v (ld ldv; unit diagonal implied, upper part ignored) and d_tau[0 .. k).  Blocks. */
+int pflu_larft(const double* d_v, int64_t ldv, int64_t mp, int64_t k, const double* d_tau, double* d_t,
+               int64_t ldt, void* stream);
+
+/* C (mp x nc, ld ldc, device) := (H_1 ... H_k)^T C = C - V (T^T (V^T C)) for the reflectors stored in
+ * the mp x k panel d_v with scalars d_tau.  Asynchronous on `stream`. */
+int pflu_apply_block_reflector(const double* d_v, int64_t ldv, int64_t mp, int64_t k, const double* d_tau,
+                               double* d_c, int64_t ldc, int64_t nc, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

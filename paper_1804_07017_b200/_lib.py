@@ -25,6 +25,7 @@ EXPORTS = (
     "pflu_getrf", "pflu_getrf_device", "pflu_panel", "pflu_laswp", "pflu_swap_trsm",
     "pflu_trsm", "pflu_gemm_update", "pflu_info_reset", "pflu_info_read", "pflu_pivot_plan",
     "pflu_swap_trsm_plan", "pflu_copy2d", "pflu_release_workspace", "pflu_diag_inv", "pflu_swap_trsm_inv",
+    "pflu_geqrf", "pflu_geqrf_device", "pflu_qr_panel", "pflu_larft", "pflu_apply_block_reflector",
 )
 
 
@@ -99,6 +100,17 @@ def load():
         L.pflu_diag_inv.argtypes = [_vp, _i64, _i64, _vp, _vp]
         L.pflu_swap_trsm_inv.restype = ctypes.c_int
         L.pflu_swap_trsm_inv.argtypes = [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _vp]
+        _pd = ctypes.c_void_p
+        L.pflu_geqrf.restype = ctypes.c_int
+        L.pflu_geqrf.argtypes = [_vp, _i64, _i64, _i64, _i64, ctypes.c_int, _pd]
+        L.pflu_geqrf_device.restype = ctypes.c_int
+        L.pflu_geqrf_device.argtypes = [_vp, _i64, _i64, _i64, _i64, ctypes.c_int, _pd, _vp]
+        L.pflu_qr_panel.restype = ctypes.c_int
+        L.pflu_qr_panel.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, _pd, _vp]
+        L.pflu_larft.restype = ctypes.c_int
+        L.pflu_larft.argtypes = [_vp, _i64, _i64, _i64, _pd, _pd, _i64, _vp]
+        L.pflu_apply_block_reflector.restype = ctypes.c_int
+        L.pflu_apply_block_reflector.argtypes = [_vp, _i64, _i64, _i64, _pd, _vp, _i64, _i64, _vp]
         _lib = L
         return L
 

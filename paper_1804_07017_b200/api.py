@@ -106,6 +106,16 @@ class LuOutput:
     info: int = 0
 
 
+@dataclass
+class QrOutput:
+    """In-place QR factors: R in the upper triangle, Householder vectors (unit head, stored below
+    the diagonal) and their tau scalars (reference factor.py:65-72)."""
+
+    matrix: Matrix
+    tau: np.ndarray
+    strategy: Strategy
+
+
 @dataclass(frozen=True)
 class TraceEvent:
     """One timed task (reference factor.py:104-113); times are seconds from the start."""
@@ -238,9 +248,69 @@ def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a:
     return (work, piv, info) if return_info else (work, piv)
 
 
+def geqrf_host(a: np.ndarray, b: int, lookahead: int) -> np.ndarray:
+    """Householder QR of a row-major C-contiguous float64 host array in place through pflu_geqrf.
+    Returns tau float64[n]."""
+    L = _lib.load()
+    m, n = a.shape
+    tau = np.zeros(n)
+    rc = L.pflu_geqrf(a.ctypes.data, m, n, a.strides[0] // 8, int(b), int(lookahead), tau.ctypes.data)
+    _lib.check(rc, "pflu_geqrf")
+    return tau
+
+
+def geqrf_device(a, b: int, lookahead: int, tau=None):
+    """Householder QR of a row-major CUDA float64 torch tensor in place through pflu_geqrf_device
+    on the current torch stream.  Returns tau (float64 CUDA tensor of length n)."""
+    import torch
+
+    L = _lib.load()
+    m, n = a.shape
+    if tau is None:
+        tau = torch.zeros(n, dtype=torch.float64, device=a.device)
+    stream = torch.cuda.current_stream(a.device).cuda_stream
+    with torch.cuda.device(a.device):
+        rc = L.pflu_geqrf_device(a.data_ptr(), m, n, a.stride(0), int(b), int(lookahead), tau.data_ptr(), stream)
+    _lib.check(rc, "pflu_geqrf_device")
+    return tau
+
+
+def qr_factor(a, b: int = 256, lookahead: int = 1, overwrite_a: bool = True):
+    """Blocked Householder QR on the B200 (the reference's Kind.QR of dmf_la / dmf_mtb).
+
+    ``a``: float64 m x n (m >= n) row-major -- a numpy array (host buffers, pflu_geqrf) or a CUDA
+    torch tensor (device buffers, current stream).  Returns ``(f, tau)``: R on and above the
+    diagonal of ``f``, the Householder vectors' tails below it (unit heads implicit), and the
+    reflector scalars (H_j = I - tau_j v_j v_j^T, Q = H_1 ... H_n).
+    """
+    if lookahead not in (0, 1):
+        raise ValueError("lookahead must be 0 or 1 (the reference defines depth 0 and 1)")
+    if b < 1:
+        raise ValueError("block size must be >= 1")
+    if _is_torch(a):
+        import torch
+
+        if a.dtype != torch.float64 or a.dim() != 2:
+            raise ValueError("expected a 2-D float64 tensor")
+        _validate_shape(*a.shape)
+        if not a.is_cuda:
+            raise ValueError("torch input must be a CUDA tensor (use a numpy array for host buffers)")
+        work = a if (overwrite_a and a.stride(1) == 1) else a.contiguous().clone()
+        return work, geqrf_device(work, b, lookahead)
+    arr = np.asarray(a)
+    if arr.dtype != np.float64 or arr.ndim != 2:
+        arr = np.asarray(arr, dtype=np.float64)
+        if arr.ndim != 2:
+            raise ValueError("expected a 2-D array")
+    _validate_shape(*arr.shape)
+    if overwrite_a and arr is a and arr.flags.c_contiguous and arr.flags.writeable:
+        work = arr
+    else:
+        work = np.array(arr, dtype=np.float64, order="C", copy=True)
+    return work, geqrf_host(work, b, lookahead)
+
+
 def _factor_matrix(a, cfg: CacheConfig, kind: Kind, lookahead: int, strategy: Strategy, trace):
-    if kind is not Kind.LU:
-        raise NotImplementedError("only Kind.LU is implemented on the B200 (QR is out of scope, SURVEY.md §2)")
     if isinstance(a, Matrix):
         mat = a
     else:
@@ -250,6 +320,10 @@ def _factor_matrix(a, cfg: CacheConfig, kind: Kind, lookahead: int, strategy: St
     # row-major copy and write the factors back into the caller's buffer (in place, like the
     # reference, factor.py:300-302)
     work = np.ascontiguousarray(mat.array)
+    if kind is Kind.QR:
+        tau = geqrf_host(work, cfg.b, lookahead)
+        mat.array[...] = work
+        return QrOutput(mat, tau, strategy)
     piv0, info = getrf_host(work, cfg.b, lookahead)
     mat.array[...] = work
     if trace is not None:

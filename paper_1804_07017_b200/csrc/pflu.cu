@@ -980,6 +980,8 @@ static int finish_info(DevCtx& c, cudaStream_t st, int64_t* info) {
 
 }  // namespace pflu
 
+#include "pflu_qr.cuh"
+
 using namespace pflu;
 
 // ==========================================================================================
@@ -1330,6 +1332,140 @@ int pflu_gemm_update(double* d_c, int64_t ldc, const double* d_a, int64_t lda, c
   DevCtx* c = nullptr;
   CKR(ctx_get(&c));
   return launch_gemm(d_c, ldc, d_a, lda, d_b, ldb, m, n, k, exact != 0, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Householder QR (Kind.QR)
+
+static int check_qr_dims(int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead) {
+  if (m < 1) return -2;
+  if (n < 1 || n > m) return -3;
+  if (lda < n) return -4;
+  if (b < 1) return -5;
+  if (lookahead != 0 && lookahead != 1) return -6;
+  if (std::min(b, n) > 1024) return set_err(PFLU_ERR_UNSUPPORTED, "QR block size %lld > 1024", (long long)b);
+  return PFLU_OK;
+}
+
+int pflu_geqrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, double* d_tau,
+                      void* stream) {
+  if (!d_a) return -1;
+  CKR(check_qr_dims(m, n, lda, b, lookahead));
+  if (!d_tau) return -7;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  cudaStream_t st = (cudaStream_t)stream;
+  CKR(geqrf_async(*c, d_a, m, n, lda, std::min(b, n), lookahead, d_tau, st));
+  CK(cudaStreamSynchronize(st));
+  return PFLU_OK;
+}
+
+int pflu_geqrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, double* tau) {
+  if (!a) return -1;
+  CKR(check_qr_dims(m, n, lda, b, lookahead));
+  if (!tau) return -7;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  const int64_t ld = qr_even(n);
+  double* d_a = nullptr;
+  double* d_tau = nullptr;
+  if (cudaMalloc(&d_a, sizeof(double) * (size_t)(m * ld)) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(PFLU_ERR_NOMEM, "pflu_geqrf: device copy of %lld x %lld", (long long)m, (long long)n);
+  }
+  if (cudaMalloc(&d_tau, sizeof(double) * (size_t)n) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(d_a);
+    return set_err(PFLU_ERR_NOMEM, "pflu_geqrf: tau");
+  }
+  cudaStream_t st = c->sH;
+  int rc = PFLU_OK;
+  do {
+    if (cudaMemcpy2DAsync(d_a, ld * 8, a, lda * 8, n * 8, m, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+      rc = set_err(PFLU_ERR_CUDA, "pflu_geqrf: H2D failed");
+      break;
+    }
+    rc = geqrf_async(*c, d_a, m, n, ld, std::min(b, n), lookahead, d_tau, st);
+    if (rc != PFLU_OK) break;
+    if (cudaMemcpy2DAsync(a, lda * 8, d_a, ld * 8, n * 8, m, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(tau, d_tau, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+      rc = set_err(PFLU_ERR_CUDA, "pflu_geqrf: D2H failed");
+      break;
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) rc = set_err(PFLU_ERR_CUDA, "pflu_geqrf: %s", cudaGetErrorString(cudaGetLastError()));
+  } while (0);
+  cudaStreamSynchronize(st);
+  cudaFree(d_a);
+  cudaFree(d_tau);
+  return rc;
+}
+
+int pflu_qr_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w, double* d_tau, void* stream) {
+  if (!d_a) return -1;
+  if (lda < col + w || col < 0) return -2;
+  if (m < 1) return -3;
+  if (d < 0 || d >= m) return -4;
+  if (w < 1 || w > m - d) return -6;
+  if (!d_tau) return -7;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  QrCtx* q = nullptr;
+  CKR(qr_ctx(*c, &q));
+  CKR(qr_panel(*c, *q, d_a, lda, m, d, col, w, d_tau, (cudaStream_t)stream));
+  return PFLU_OK;
+}
+
+int pflu_larft(const double* d_v, int64_t ldv, int64_t mp, int64_t k, const double* d_tau, double* d_t, int64_t ldt,
+               void* stream) {
+  if (!d_v) return -1;
+  if (ldv < k) return -2;
+  if (mp < k) return -3;
+  if (k < 1 || k > 1024) return -4;
+  if (!d_tau) return -5;
+  if (!d_t) return -6;
+  if (ldt < k) return -7;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  QrCtx* q = nullptr;
+  CKR(qr_ctx(*c, &q));
+  cudaStream_t st = (cudaStream_t)stream;
+  // the panel view: rows [0, mp) of columns [0, k) at d_v
+  CKR(qr_build(*c, q->ws[0], q->leaf, d_v, ldv, 0, mp, 0, (int)k, d_tau, st));
+  // T = (T^T)^T into the caller's upper-triangular layout
+  std::vector<double> tt((size_t)(k * q->leaf.ldt)), t((size_t)(k * ldt), 0.0);
+  CK(cudaMemcpyAsync(tt.data(), q->leaf.tt.p, sizeof(double) * tt.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(t.data(), d_t, sizeof(double) * t.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < k; ++i)
+    for (int64_t j = 0; j < k; ++j) t[(size_t)(i * ldt + j)] = j >= i ? tt[(size_t)(j * q->leaf.ldt + i)] : 0.0;
+  CK(cudaMemcpyAsync(d_t, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  return PFLU_OK;
+}
+
+int pflu_apply_block_reflector(const double* d_v, int64_t ldv, int64_t mp, int64_t k, const double* d_tau, double* d_c,
+                               int64_t ldc, int64_t nc, void* stream) {
+  if (!d_v) return -1;
+  if (ldv < k) return -2;
+  if (mp < k) return -3;
+  if (k < 1 || k > 1024) return -4;
+  if (!d_tau) return -5;
+  if (!d_c) return -6;
+  if (ldc < nc) return -7;
+  if (nc < 0) return -8;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCtx* c = nullptr;
+  CKR(ctx_get(&c));
+  QrCtx* q = nullptr;
+  CKR(qr_ctx(*c, &q));
+  cudaStream_t st = (cudaStream_t)stream;
+  CKR(qr_build(*c, q->ws[0], q->leaf, d_v, ldv, 0, mp, 0, (int)k, d_tau, st));
+  CKR(qr_apply(*c, q->ws[0], q->leaf, d_c, ldc, nc, st));
+  return PFLU_OK;
 }
 
 }  // extern "C"

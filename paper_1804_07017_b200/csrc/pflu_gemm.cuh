@@ -112,8 +112,18 @@ struct FastLoader {
   }
 };
 
-template <class C, int VEC>
+// SPLIT (QR's tall-skinny products V^T C): blockIdx.y selects a K slice of p.kslice columns of A /
+// rows of B and its own output slice p.c + blockIdx.y * p.cslice; accumulators start from zero, so
+// slice s holds -(A_s B_s) and the caller sums the slices in a fixed order (deterministic).
+template <class C, int VEC, bool SPLIT = false>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_t(GemmArgs p) {
+  if constexpr (SPLIT) {
+    const int64_t ks = (int64_t)blockIdx.y * p.kslice;
+    p.a += ks;
+    p.b += ks * p.ldb;
+    p.c += (int64_t)blockIdx.y * p.cslice;
+    p.K = min(p.kslice, p.K - ks);
+  }
   extern __shared__ __align__(128) double gm_smem[];
   double* sA = gm_smem;
   double* sB = gm_smem + C::ST * C::BM * C::BK;
@@ -147,7 +157,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_t(GemmArgs p) {
     for (int j = 0; j < C::FN; ++j) {
       const int64_t col = n0 + wn * C::TN + j * 8 + 2 * t;
       const double* cp = p.c + row * p.ldc + col;
-      if (VEC == 2 && row < p.M && col + 1 < p.N) {
+      if (SPLIT) {
+        acc[i][j][0] = 0.0;
+        acc[i][j][1] = 0.0;
+      } else if (VEC == 2 && row < p.M && col + 1 < p.N) {
         const double2 v = *reinterpret_cast<const double2*>(cp);
         acc[i][j][0] = v.x;
         acc[i][j][1] = v.y;

@@ -374,6 +374,7 @@ struct GemmArgs {
   const double* b;
   int64_t ldc, lda, ldb, M, N, K;
   int tiles_m, tiles_n;
+  int64_t kslice, cslice;  // split-K GEMM (QR): K per blockIdx.y slice, C elements between slices
 };
 
 __device__ __forceinline__ void tile_coords(int lin, int tiles_m, int tiles_n, int& tm, int& tn) {

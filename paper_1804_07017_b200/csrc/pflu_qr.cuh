@@ -1,0 +1,479 @@
+// pflu_qr.cuh -- blocked Householder QR (Kind.QR) on the B200, SURVEY.md §8(f) row 4.
+//
+// Included by pflu.cu inside namespace pflu (after the GEMM launchers).  Same storage as the LU
+// path: float64 m x n row-major, factored in place (R on/above the diagonal, the reflectors' tails
+// below it, unit heads implicit), tau[n] out.  Reference (pkg/src/panelforge/...):
+//   qr_leaf_kernel            <- qr_unb / _jit.qr_unb_run (factor.py:147-161, _jit.py:190-218),
+//                                32 columns at a time
+//   qr_larft_kernel           <- larft_forward_columnwise (factor.py:174-189)
+//   qr_apply (3 DMMA GEMMs)   <- apply_block_reflector (factor.py:192-205): C - V (T^T (V^T C))
+//   geqrf_async               <- dmf_mtb (factor.py:382-412, depth 0) / dmf_la (factor.py:455-515,
+//                                depth 1) with kind=Kind.QR
+//
+// B200 mapping.  The panel (m_p x b) is factored in 32-column leaves by ONE cooperative kernel per
+// leaf: every CTA keeps its contiguous row chunk of the leaf in shared memory for all 32 columns,
+// and each column costs two grid-wide exchanges (the column norm's partial sums, then the partial
+// dot products v^T a_c of the leaf's later columns), each reduced by every CTA in the same fixed
+// order so all CTAs hold bit-identical tau / s_c.  Between leaves, and for the trailing matrix,
+// the reflectors are applied as a block reflector on the FP64 tensor cores: V^T C and V^T V are
+// tall-skinny products (K = panel height) run as split-K DMMA GEMMs whose slices are summed in a
+// fixed order (deterministic), T^T W and C -= V Z are the ordinary DMMA GEMM.
+#pragma once
+
+namespace pflu {
+
+constexpr int QR_THREADS = 256;
+constexpr int QR_LW = 32;   // leaf width
+constexpr int QR_LDT = 33;  // leaf tile row stride (doubles)
+constexpr int QR_MAXG = 256;
+
+static int g_qr_rows = []() { const char* e = getenv("PFLU_QR_ROWS"); return e ? atoi(e) : 512; }();
+
+struct QrLeafArgs {
+  double* a;
+  int64_t lda;
+  int64_t r0, m;   // panel rows [r0, m); the diagonal of leaf column j is row r0 + j
+  int64_t c0;      // leaf columns [c0, c0 + w)
+  int w;
+  int G, R;        // CTAs, rows per CTA
+  double* tau;     // tau of leaf column j at tau[j]
+  double* part;    // [2][G] sum-of-squares partials (column parity)
+  double* dots;    // [2][G][32] partial v^T a_c
+  double* drow;    // [2][32] diagonal row, [64 + parity] alpha
+  unsigned* bar;   // grid barrier counter, zeroed before the launch
+};
+
+__device__ __forceinline__ double qr_warp_sum(double v) {
+  // xor butterfly: every lane ends with the bit-identical sum
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void qr_grid_sync(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// Sum of the G partials at src[0..G) (L2 reads), same order on every CTA.
+__device__ __forceinline__ double qr_sum_partials(const double* src, int G, int stride, int lane) {
+  double t = 0.0;
+  for (int i = lane; i < G; i += 32) t += __ldcg(src + (int64_t)i * stride);
+  return qr_warp_sum(t);
+}
+
+__global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
+  extern __shared__ __align__(16) double qr_smem[];
+  double* tile = qr_smem;  // R x QR_LDT
+  __shared__ double red[QR_THREADS / 32];
+  __shared__ double sc[QR_LW];
+  __shared__ double bc[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q = blockIdx.x;
+  const int64_t rbeg = p.r0 + (int64_t)q * p.R;
+  const int64_t rend = min(p.m, rbeg + p.R);
+  const int nrows = (int)max((int64_t)0, rend - rbeg);
+  const int w = p.w;
+  for (int idx = tid; idx < nrows * w; idx += QR_THREADS) {
+    const int r = idx / w, c = idx - r * w;
+    tile[r * QR_LDT + c] = p.a[(rbeg + r) * p.lda + p.c0 + c];
+  }
+  __syncthreads();
+  unsigned nbar = 0;
+  for (int j = 0; j < w; ++j) {
+    const int64_t d = p.r0 + j;
+    const int par = j & 1;
+    const bool own_d = d >= rbeg && d < rend;
+    const int dl = (int)(d - rbeg);
+    const int rfirst = (int)min((int64_t)nrows, max((int64_t)0, d + 1 - rbeg));
+    // (A) partial sum of squares below the diagonal (_jit.py:199-202)
+    double s = 0.0;
+    for (int r = rfirst + tid; r < nrows; r += QR_THREADS) {
+      const double x = tile[r * QR_LDT + j];
+      s += x * x;
+    }
+    s = qr_warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (warp == 0) {
+      const double t = qr_warp_sum(lane < QR_THREADS / 32 ? red[lane] : 0.0);
+      if (lane == 0) {
+        p.part[par * p.G + q] = t;
+        if (own_d) p.drow[64 + par] = tile[dl * QR_LDT + j];
+      }
+    }
+    qr_grid_sync(p.bar, (++nbar) * (unsigned)p.G);
+    // (B) reflector of column j (_jit.py:203-212), identical on every CTA
+    if (warp == 0) {
+      const double t = qr_sum_partials(p.part + par * p.G, p.G, 1, lane);
+      if (lane == 0) {
+        bc[0] = t;
+        bc[1] = __ldcg(p.drow + 64 + par);
+      }
+    }
+    __syncthreads();
+    const double sq = bc[0], alpha = bc[1];
+    if (sq == 0.0) {  // null reflector, column unchanged (uniform over the grid)
+      if (q == 0 && tid == 0) p.tau[j] = 0.0;
+      continue;
+    }
+    const double norm = sqrt(alpha * alpha + sq);
+    const double beta = alpha >= 0.0 ? -norm : norm;
+    const double tj = (beta - alpha) / beta;
+    const double scale = 1.0 / (alpha - beta);
+    if (q == 0 && tid == 0) p.tau[j] = tj;
+    for (int r = rfirst + tid; r < nrows; r += QR_THREADS) tile[r * QR_LDT + j] *= scale;
+    __syncthreads();
+    // partial s_c = v^T a_c over this CTA's rows, one warp per column (_jit.py:213-216)
+    for (int c = j + 1 + warp; c < w; c += QR_THREADS / 32) {
+      double t = 0.0;
+      for (int r = rfirst + lane; r < nrows; r += 32) t += tile[r * QR_LDT + j] * tile[r * QR_LDT + c];
+      t = qr_warp_sum(t);
+      if (lane == 0) {
+        p.dots[((int64_t)par * p.G + q) * QR_LW + c] = t;
+        if (own_d) p.drow[par * 32 + c] = tile[dl * QR_LDT + c];
+      }
+    }
+    if (own_d && tid == 0) tile[dl * QR_LDT + j] = beta;
+    qr_grid_sync(p.bar, (++nbar) * (unsigned)p.G);
+    // (C) s_c = (a_jc + sum) * tau; a_jc -= s_c; a_ic -= s_c v_i (_jit.py:213-218)
+    for (int c = j + 1 + warp; c < w; c += QR_THREADS / 32) {
+      const double t = qr_sum_partials(p.dots + (int64_t)par * p.G * QR_LW + c, p.G, QR_LW, lane);
+      if (lane == 0) sc[c] = (__ldcg(p.drow + par * 32 + c) + t) * tj;
+    }
+    __syncthreads();
+    if (own_d)
+      for (int c = j + 1 + tid; c < w; c += QR_THREADS) tile[dl * QR_LDT + c] -= sc[c];
+    for (int r = rfirst + tid; r < nrows; r += QR_THREADS) {
+      double* tr = tile + r * QR_LDT;
+      const double v = tr[j];
+      for (int c = j + 1; c < w; ++c) tr[c] -= sc[c] * v;
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < nrows * w; idx += QR_THREADS) {
+    const int r = idx / w, c = idx - r * w;
+    p.a[(rbeg + r) * p.lda + p.c0 + c] = tile[r * QR_LDT + c];
+  }
+}
+
+// Dense reflector block of the panel rows [d, d + mp), columns [cv, cv + k): unit diagonal, zeros
+// above.  vd: mp x k (ld ldv), vt = vd^T: k x mp (ld ldvt).  32x32 tiles through shared memory.
+__global__ void qr_make_v_kernel(const double* __restrict__ a, int64_t lda, int64_t d, int64_t cv, int64_t mp,
+                                 int k, double* __restrict__ vd, int64_t ldv, double* __restrict__ vt,
+                                 int64_t ldvt) {
+  __shared__ double t[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = i0 + r;
+    const int c = c0 + tx;
+    double v = 0.0;
+    if (i < mp && c < k) v = i > c ? a[(d + i) * lda + cv + c] : (i == c ? 1.0 : 0.0);
+    t[r][tx] = v;
+    if (i < mp && c < k) vd[i * ldv + c] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int c = c0 + r;
+    const int64_t i = i0 + tx;
+    if (c < k && i < mp) vt[(int64_t)c * ldvt + i] = t[tx][r];
+  }
+}
+
+// out (rows x cols, ld ldo) = sum over s of part[s] (slices cslice apart, ld ldp), s ascending.
+__global__ void qr_split_reduce_kernel(const double* __restrict__ part, int64_t ldp, int64_t cslice, int S,
+                                       int64_t rows, int64_t cols, double* __restrict__ out, int64_t ldo) {
+  const int64_t n = rows * cols;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / cols, c = idx - r * cols;
+    const double* src = part + r * ldp + c;
+    double acc = src[0];
+    for (int s = 1; s < S; ++s) acc += src[(int64_t)s * cslice];
+    out[r * ldo + c] = acc;
+  }
+}
+
+// larft (factor.py:174-189): T[j][j] = tau_j, T[:j, j] = -tau_j T[:j, :j] (V^T v_j), from
+// gneg = -(V^T V).  Writes tt = T^T (k x k, ld ldt) including the zero upper part.  One CTA,
+// thread i owns row i of T (column i of tt: coalesced reads of tt rows).
+__global__ void qr_larft_kernel(const double* __restrict__ gneg, int64_t ldg, const double* __restrict__ tau, int k,
+                                double* tt, int64_t ldt) {
+  extern __shared__ double qr_y[];
+  for (int64_t idx = threadIdx.x; idx < (int64_t)k * k; idx += blockDim.x) {
+    const int r = (int)(idx / k), c = (int)(idx - (int64_t)r * k);
+    if (c > r) tt[(int64_t)r * ldt + c] = 0.0;
+  }
+  const int i = threadIdx.x;
+  for (int j = 0; j < k; ++j) {
+    if (i < j) qr_y[i] = -gneg[(int64_t)i * ldg + j];
+    __syncthreads();
+    const double tj = tau[j];
+    if (i < j) {
+      double acc = 0.0;
+      for (int l = i; l < j; ++l) acc += tt[(int64_t)l * ldt + i] * qr_y[l];
+      tt[(int64_t)j * ldt + i] = -tj * acc;
+    } else if (i == j) {
+      tt[(int64_t)j * ldt + j] = tj;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+
+static inline int64_t qr_even(int64_t x) { return (x + 1) & ~(int64_t)1; }
+
+struct QrBuf {
+  double* p = nullptr;
+  size_t cap = 0;  // doubles
+  int need(size_t n) {
+    if (n <= cap) return PFLU_OK;
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    if (cudaMalloc(&p, n * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(PFLU_ERR_NOMEM, "QR workspace: cudaMalloc(%zu bytes) failed", n * sizeof(double));
+    }
+    cap = n;
+    return PFLU_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// One block reflector: dense V, V^T and T^T.
+struct QrRefl {
+  QrBuf vd, vt, tt;
+  int64_t mp = 0, ldv = 0, ldvt = 0, ldt = 0;
+  int k = 0;
+};
+
+// Scratch of one stream: products W / Z / Gram and split-K slices.
+struct QrScratch {
+  QrBuf w, z, g, part;
+};
+
+struct QrCtx {
+  QrRefl refl[2];     // outer step reflectors, by step parity
+  QrRefl leaf;        // in-panel leaf reflector
+  QrScratch ws[2];    // 0: panel stream (leaves, TU_L), 1: trailing stream (TU_R)
+  double* leafx = nullptr;  // leaf kernel exchange: part, dots, drow
+  unsigned* bar = nullptr;
+  bool ready = false;
+  void release() {
+    for (auto& r : refl) { r.vd.release(); r.vt.release(); r.tt.release(); }
+    leaf.vd.release(); leaf.vt.release(); leaf.tt.release();
+    for (auto& s : ws) { s.w.release(); s.z.release(); s.g.release(); s.part.release(); }
+  }
+};
+static QrCtx g_qr[64];
+
+static int qr_ctx(DevCtx& c, QrCtx** out) {
+  QrCtx& q = g_qr[c.dev];
+  if (!q.ready) {
+    CK(cudaMalloc(&q.leafx, sizeof(double) * (2 * QR_MAXG + 2 * QR_MAXG * QR_LW + 128)));
+    CK(cudaMalloc(&q.bar, 64));
+    CK(cudaFuncSetAttribute(qr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)std::min<size_t>(c.smem_optin, 227 * 1024) - 1024));
+    q.ready = true;
+  }
+  *out = &q;
+  return PFLU_OK;
+}
+
+// Split-K DMMA product: out (M x N, ld ldo) = -(A B), A: M x K (ld lda), B: K x N (ld ldb).
+static int qr_gemm_neg(DevCtx& c, QrScratch& ws, double* out, int64_t ldo, const double* a, int64_t lda,
+                       const double* b, int64_t ldb, int64_t M, int64_t N, int64_t K, cudaStream_t st) {
+  using C = GV6;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(gemm_dmma_t<C, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    CK(cudaFuncSetAttribute(gemm_dmma_t<C, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  if (M <= 0 || N <= 0) return PFLU_OK;
+  const int64_t tm = (M + C::BM - 1) / C::BM, tn = (N + C::BN - 1) / C::BN;
+  if (tm * tn > INT_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "gemm grid too large");
+  const int64_t want = std::max<int64_t>(1, (2 * c.sms + tm * tn - 1) / (tm * tn));
+  int64_t S = std::max<int64_t>(1, std::min<int64_t>(want, (K + 255) / 256));
+  S = std::min<int64_t>(S, 65535);
+  int64_t ks = ((K + S - 1) / S + C::BK - 1) / C::BK * C::BK;
+  if (K <= 0) ks = 0;
+  S = K <= 0 ? 1 : (K + ks - 1) / ks;
+  GemmArgs p;
+  p.a = a; p.b = b; p.lda = lda; p.ldb = ldb;
+  p.M = M; p.N = N; p.K = std::max<int64_t>(K, 0);
+  p.tiles_m = (int)tm; p.tiles_n = (int)tn;
+  p.kslice = std::max<int64_t>(ks, 1);
+  if (S == 1) {
+    p.c = out; p.ldc = ldo; p.cslice = 0;
+  } else {
+    const int64_t ldp = qr_even(N);
+    CKR(ws.part.need((size_t)(S * M * ldp)));
+    p.c = ws.part.p; p.ldc = ldp; p.cslice = M * ldp;
+  }
+  const bool v2 = aligned16(p.c) && aligned16(a) && aligned16(b) && (p.ldc % 2 == 0) && (lda % 2 == 0) &&
+                  (ldb % 2 == 0);
+  dim3 grid((unsigned)(tm * tn), (unsigned)S);
+  if (v2) gemm_dmma_t<C, 2, true><<<grid, C::THREADS, C::SMEM, st>>>(p);
+  else gemm_dmma_t<C, 1, true><<<grid, C::THREADS, C::SMEM, st>>>(p);
+  CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (S > 1) {
+    const int64_t n = M * N;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * c.sms);
+    qr_split_reduce_kernel<<<blocks, 256, 0, st>>>(p.c, p.ldc, p.cslice, (int)S, M, N, out, ldo);
+    CK(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  return PFLU_OK;
+}
+
+// V, V^T and T^T of the reflectors stored at rows [d, m), columns [cv, cv + k).
+static int qr_build(DevCtx& c, QrScratch& ws, QrRefl& R, const double* a, int64_t lda, int64_t d, int64_t m,
+                    int64_t cv, int k, const double* d_tau, cudaStream_t st) {
+  R.mp = m - d;
+  R.k = k;
+  R.ldv = qr_even(k);
+  R.ldvt = qr_even(R.mp);
+  R.ldt = qr_even(k);
+  CKR(R.vd.need((size_t)(R.mp * R.ldv)));
+  CKR(R.vt.need((size_t)(k * R.ldvt)));
+  CKR(R.tt.need((size_t)(k * R.ldt)));
+  dim3 g((unsigned)((R.mp + 31) / 32), (unsigned)((k + 31) / 32));
+  qr_make_v_kernel<<<g, dim3(32, 8), 0, st>>>(a, lda, d, cv, R.mp, k, R.vd.p, R.ldv, R.vt.p, R.ldvt);
+  CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CKR(ws.g.need((size_t)(k * R.ldt)));
+  CKR(qr_gemm_neg(c, ws, ws.g.p, R.ldt, R.vt.p, R.ldvt, R.vd.p, R.ldv, k, k, R.mp, st));
+  const int thr = std::max(32, (k + 31) / 32 * 32);
+  if (thr > 1024) return set_err(PFLU_ERR_UNSUPPORTED, "QR block size %d > 1024", k);
+  qr_larft_kernel<<<1, thr, sizeof(double) * k, st>>>(ws.g.p, R.ldt, d_tau, k, R.tt.p, R.ldt);
+  CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return PFLU_OK;
+}
+
+// C (rows [d, m) of columns [lo, lo + nc)) := C - V (T^T (V^T C))   (factor.py:192-205)
+static int qr_apply(DevCtx& c, QrScratch& ws, const QrRefl& R, double* cp, int64_t ldc, int64_t nc, cudaStream_t st) {
+  if (nc <= 0 || R.k <= 0 || R.mp <= 0) return PFLU_OK;
+  const int64_t ldw = qr_even(nc);
+  CKR(ws.w.need((size_t)(R.k * ldw)));
+  CKR(ws.z.need((size_t)(R.k * ldw)));
+  // W = -(V^T C), Z = -(T^T W) = T^T V^T C, C -= V Z
+  CKR(qr_gemm_neg(c, ws, ws.w.p, ldw, R.vt.p, R.ldvt, cp, ldc, R.k, nc, R.mp, st));
+  CKR(qr_gemm_neg(c, ws, ws.z.p, ldw, R.tt.p, R.ldt, ws.w.p, ldw, R.k, nc, R.k, st));
+  CKR(launch_gemm(cp, ldc, R.vd.p, R.ldv, ws.z.p, ldw, R.mp, nc, R.k, false, st));
+  return PFLU_OK;
+}
+
+// Householder factorization of the panel rows [d, m), columns [col, col + w): 32-column leaves,
+// each followed by its block reflector on the panel's remaining columns.
+static int qr_panel(DevCtx& c, QrCtx& q, double* a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w,
+                    double* d_tau, cudaStream_t st) {
+  for (int64_t p0 = 0; p0 < w; p0 += QR_LW) {
+    const int lw = (int)std::min<int64_t>(QR_LW, w - p0);
+    const int64_t r0 = d + p0, mp = m - r0;
+    int R = std::max<int64_t>(g_qr_rows > 0 ? g_qr_rows : 512, (mp + c.sms - 1) / c.sms);
+    const int64_t smax = (int64_t)std::min<size_t>(c.smem_optin, 227 * 1024) - 1024;
+    if ((int64_t)R * QR_LDT * 8 > smax) return set_err(PFLU_ERR_UNSUPPORTED, "QR panel of %lld rows too tall", (long long)mp);
+    int G = (int)((mp + R - 1) / R);
+    if (G > QR_MAXG || G > c.sms) return set_err(PFLU_ERR_UNSUPPORTED, "QR panel grid %d too large", G);
+    R = (int)((mp + G - 1) / G);
+    QrLeafArgs la;
+    la.a = a; la.lda = lda; la.r0 = r0; la.m = m; la.c0 = col + p0; la.w = lw;
+    la.G = G; la.R = R;
+    la.tau = d_tau + p0;
+    la.part = q.leafx;
+    la.dots = q.leafx + 2 * QR_MAXG;
+    la.drow = q.leafx + 2 * QR_MAXG + 2 * QR_MAXG * QR_LW;
+    la.bar = q.bar;
+    CK(cudaMemsetAsync(q.bar, 0, sizeof(unsigned), st));
+    void* args[] = {&la};
+    CK(cudaLaunchCooperativeKernel((void*)qr_leaf_kernel, dim3(G), dim3(QR_THREADS), args,
+                                   (size_t)R * QR_LDT * 8, st));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const int64_t rest = w - p0 - lw;
+    if (rest > 0) {
+      CKR(qr_build(c, q.ws[0], q.leaf, a, lda, r0, m, col + p0, lw, d_tau + p0, st));
+      CKR(qr_apply(c, q.ws[0], q.leaf, a + r0 * lda + col + p0 + lw, lda, rest, st));
+    }
+  }
+  return PFLU_OK;
+}
+
+// Blocked QR, depth 0 (dmf_mtb order) or 1 (dmf_la: TU_L(k) + PF(k+1) on the panel stream while
+// TU_R(k) runs on the trailing stream), asynchronous; the caller's stream `st` is joined at the end.
+static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
+                       double* d_tau, cudaStream_t st) {
+  QrCtx* qp = nullptr;
+  CKR(qr_ctx(c, &qp));
+  QrCtx& q = *qp;
+  const int64_t steps = (n + b - 1) / b;
+  cudaStream_t sP = c.sP, sU = c.sU;
+  CKR(ctx_events(c, 4));
+  cudaEvent_t e_in = c.ev[0], e_pf = c.ev[1], e_tu = c.ev[2], e_out = c.ev[3];
+  CK(cudaEventRecord(e_in, st));
+  CK(cudaStreamWaitEvent(sP, e_in, 0));
+  CK(cudaStreamWaitEvent(sU, e_in, 0));
+  auto bw_of = [&](int64_t k) { return std::min(b, n - k * b); };
+  if (lookahead == 0) {
+    for (int64_t k = 0; k < steps; ++k) {
+      const int64_t col0 = k * b, bw = bw_of(k), lo = col0 + bw;
+      CKR(qr_panel(c, q, a, lda, m, col0, col0, bw, d_tau + col0, sP));
+      if (lo < n) {
+        QrRefl& R = q.refl[k & 1];
+        CKR(qr_build(c, q.ws[0], R, a, lda, col0, m, col0, (int)bw, d_tau + col0, sP));
+        CKR(qr_apply(c, q.ws[0], R, a + col0 * lda + lo, lda, n - lo, sP));
+      }
+    }
+    CK(cudaEventRecord(e_out, sP));
+    CK(cudaStreamWaitEvent(st, e_out, 0));
+    return PFLU_OK;
+  }
+  // look-ahead 1
+  CKR(qr_panel(c, q, a, lda, m, 0, 0, bw_of(0), d_tau, sP));
+  for (int64_t k = 0; k < steps; ++k) {
+    const int64_t col0 = k * b, bw = bw_of(k), lo = col0 + bw;
+    if (lo >= n) break;
+    QrRefl& R = q.refl[k & 1];
+    CKR(qr_build(c, q.ws[0], R, a, lda, col0, m, col0, (int)bw, d_tau + col0, sP));
+    CK(cudaEventRecord(e_pf, sP));
+    // TU_R(k): columns beyond block k+1, on the trailing stream
+    const int64_t lo2 = lo + bw_of(k + 1);
+    if (lo2 < n) {
+      CK(cudaStreamWaitEvent(sU, e_pf, 0));
+      CKR(qr_apply(c, q.ws[1], R, a + col0 * lda + lo2, lda, n - lo2, sU));
+    }
+    // TU_L(k) + PF(k+1) on the panel stream; TU_R(k-1) (recorded before e_tu is re-recorded
+    // below) finished updating block k+1
+    CKR(qr_apply(c, q.ws[0], R, a + col0 * lda + lo, lda, bw_of(k + 1), sP));
+    CKR(qr_panel(c, q, a, lda, m, lo, lo, bw_of(k + 1), d_tau + lo, sP));
+    // the next TU_L / build (which rewrites refl[(k+1)&1] ... refl[k&1] at step k+2) must follow TU_R(k)
+    if (lo2 < n) {
+      CK(cudaEventRecord(e_tu, sU));
+      CK(cudaStreamWaitEvent(sP, e_tu, 0));
+    }
+  }
+  CK(cudaEventRecord(e_out, sU));
+  CK(cudaStreamWaitEvent(st, e_out, 0));
+  CK(cudaEventRecord(e_out, sP));
+  CK(cudaStreamWaitEvent(st, e_out, 0));
+  return PFLU_OK;
+}
+
+}  // namespace pflu

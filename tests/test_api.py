@@ -33,9 +33,15 @@ def test_bad_arguments():
         CacheConfig(b=0)
 
 
-def test_qr_is_out_of_scope():
-    with pytest.raises(NotImplementedError):
-        dmf_la(Matrix.zeros(4, 4), CacheConfig(b=2), None, Kind.QR)
+def test_qr_bad_arguments():
+    from paper_1804_07017_b200 import qr_factor
+
+    with pytest.raises(ValueError):
+        qr_factor(np.eye(4), lookahead=2)
+    with pytest.raises(ValueError):
+        qr_factor(np.eye(4), b=0)
+    with pytest.raises(ValueError):
+        qr_factor(np.zeros((3, 5)))   # wide: the reference rejects it (factor.py:293-297)
 
 
 def test_matrix_container_is_column_major():

@@ -55,6 +55,13 @@ def test_argument_validation_codes_without_gpu():
     assert L.pflu_getrf(None, 8, 8, 8, 2, 1, piv.ctypes.data, ctypes.byref(info), None) == -1
     assert L.pflu_gemm_update(None, 1, None, 1, None, 1, 1, 1, 1, 0, None) == -1
     assert L.pflu_laswp(b.ctypes.data, 8, 5, 3, piv.ctypes.data, 0, 1, None) == -4
+    tau = np.zeros(8)
+    assert L.pflu_geqrf(a.ctypes.data, 4, 8, 8, 2, 1, tau.ctypes.data) == -3
+    assert L.pflu_geqrf(b.ctypes.data, 8, 8, 4, 2, 1, tau.ctypes.data) == -4
+    assert L.pflu_geqrf(b.ctypes.data, 8, 8, 8, 0, 1, tau.ctypes.data) == -5
+    assert L.pflu_geqrf(b.ctypes.data, 8, 8, 8, 2, 2, tau.ctypes.data) == -6
+    assert L.pflu_geqrf(b.ctypes.data, 8, 8, 8, 2, 1, None) == -7
+    assert L.pflu_geqrf_device(None, 8, 8, 8, 2, 1, None, None) == -1
 
 
 def test_no_device_fails_loudly():
@@ -66,3 +73,9 @@ def test_no_device_fails_loudly():
         pytest.skip("a GPU is visible")
     with pytest.raises(RuntimeError):
         lu_factor(np.eye(8), b=4)
+    from paper_1804_07017_b200 import Kind, Matrix, CacheConfig, dmf_la, qr_factor
+
+    with pytest.raises(RuntimeError):
+        qr_factor(np.eye(8), b=4)
+    with pytest.raises(RuntimeError):
+        dmf_la(Matrix.zeros(8, 8), CacheConfig(b=4), None, Kind.QR)
