@@ -70,13 +70,18 @@ __device__ __forceinline__ double qr_sum_partials(const double* src, int G, int 
   return qr_warp_sum(t);
 }
 
+// One grid exchange per column: with x the column below the diagonal and v = x * scale, the
+// reflector's products s_c = a_jc + v^T a_c equal a_jc + scale * (x^T a_c), so the squared norm
+// (c = j) and every raw dot x^T a_c (c > j) are reduced together BEFORE the norm is known; every
+// CTA then derives beta, tau, scale and s_c from the same sums (same order, same bits) and updates
+// its rows.  Rounding differs from the reference's sequential order (parity is to tolerance).
 __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
   extern __shared__ __align__(16) double qr_smem[];
   double* tile = qr_smem;  // R x QR_LDT
-  __shared__ double red[QR_THREADS / 32];
-  __shared__ double sc[QR_LW];
-  __shared__ double bc[2];
+  __shared__ double sc[QR_LW];   // column sums, then s_c
+  __shared__ double dr[QR_LW];   // diagonal row
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q = blockIdx.x;
+  constexpr int NW = QR_THREADS / 32;
   const int64_t rbeg = p.r0 + (int64_t)q * p.R;
   const int64_t rend = min(p.m, rbeg + p.R);
   const int nrows = (int)max((int64_t)0, rend - rbeg);
@@ -86,42 +91,51 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
     tile[r * QR_LDT + c] = p.a[(rbeg + r) * p.lda + p.c0 + c];
   }
   __syncthreads();
-  unsigned nbar = 0;
   for (int j = 0; j < w; ++j) {
     const int64_t d = p.r0 + j;
     const int par = j & 1;
     const bool own_d = d >= rbeg && d < rend;
     const int dl = (int)(d - rbeg);
     const int rfirst = (int)min((int64_t)nrows, max((int64_t)0, d + 1 - rbeg));
-    // (A) partial sum of squares below the diagonal (_jit.py:199-202)
-    double s = 0.0;
-    for (int r = rfirst + tid; r < nrows; r += QR_THREADS) {
-      const double x = tile[r * QR_LDT + j];
-      s += x * x;
-    }
-    s = qr_warp_sum(s);
-    if (lane == 0) red[warp] = s;
-    __syncthreads();
-    if (warp == 0) {
-      const double t = qr_warp_sum(lane < QR_THREADS / 32 ? red[lane] : 0.0);
+    double* dots = p.dots + (int64_t)par * p.G * QR_LW;
+    // (A) partial x^T a_c for c in [j, w) over this CTA's rows below the diagonal, one warp per column
+    for (int c = j + warp; c < w; c += NW) {
+      double t = 0.0;
+      for (int r = rfirst + lane; r < nrows; r += 32) t += tile[r * QR_LDT + j] * tile[r * QR_LDT + c];
+      t = qr_warp_sum(t);
       if (lane == 0) {
-        p.part[par * p.G + q] = t;
-        if (own_d) p.drow[64 + par] = tile[dl * QR_LDT + j];
+        dots[(int64_t)q * QR_LW + c] = t;
+        if (own_d) p.drow[par * 32 + c] = tile[dl * QR_LDT + c];
       }
     }
-    qr_grid_sync(p.bar, (++nbar) * (unsigned)p.G);
-    // (B) reflector of column j (_jit.py:203-212), identical on every CTA
-    if (warp == 0) {
-      const double t = qr_sum_partials(p.part + par * p.G, p.G, 1, lane);
-      if (lane == 0) {
-        bc[0] = t;
-        bc[1] = __ldcg(p.drow + 64 + par);
+    qr_grid_sync(p.bar, (unsigned)(j + 1) * (unsigned)p.G);
+    // (B) the same fixed-order sums on every CTA; all loads of a warp's columns in flight together
+    {
+      double acc[(QR_LW + NW - 1) / NW];
+#pragma unroll
+      for (int u = 0; u < (QR_LW + NW - 1) / NW; ++u) acc[u] = 0.0;
+      for (int i = lane; i < p.G; i += 32) {
+#pragma unroll
+        for (int u = 0; u < (QR_LW + NW - 1) / NW; ++u) {
+          const int c = j + warp + u * NW;
+          if (c < w) acc[u] += __ldcg(dots + (int64_t)i * QR_LW + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < (QR_LW + NW - 1) / NW; ++u) {
+        const int c = j + warp + u * NW;
+        const double t = qr_warp_sum(acc[u]);
+        if (lane == 0 && c < w) {
+          sc[c] = t;
+          dr[c] = __ldcg(p.drow + par * 32 + c);
+        }
       }
     }
     __syncthreads();
-    const double sq = bc[0], alpha = bc[1];
-    if (sq == 0.0) {  // null reflector, column unchanged (uniform over the grid)
+    const double sq = sc[j], alpha = dr[j];
+    if (sq == 0.0) {  // null reflector, column unchanged (uniform over the grid; _jit.py:203-205)
       if (q == 0 && tid == 0) p.tau[j] = 0.0;
+      __syncthreads();
       continue;
     }
     const double norm = sqrt(alpha * alpha + sq);
@@ -129,32 +143,19 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
     const double tj = (beta - alpha) / beta;
     const double scale = 1.0 / (alpha - beta);
     if (q == 0 && tid == 0) p.tau[j] = tj;
-    for (int r = rfirst + tid; r < nrows; r += QR_THREADS) tile[r * QR_LDT + j] *= scale;
+    __syncthreads();  // every thread read sc[j] before it is overwritten below
+    if (tid < w && tid > j) sc[tid] = (dr[tid] + scale * sc[tid]) * tj;
     __syncthreads();
-    // partial s_c = v^T a_c over this CTA's rows, one warp per column (_jit.py:213-216)
-    for (int c = j + 1 + warp; c < w; c += QR_THREADS / 32) {
-      double t = 0.0;
-      for (int r = rfirst + lane; r < nrows; r += 32) t += tile[r * QR_LDT + j] * tile[r * QR_LDT + c];
-      t = qr_warp_sum(t);
-      if (lane == 0) {
-        p.dots[((int64_t)par * p.G + q) * QR_LW + c] = t;
-        if (own_d) p.drow[par * 32 + c] = tile[dl * QR_LDT + c];
-      }
-    }
-    if (own_d && tid == 0) tile[dl * QR_LDT + j] = beta;
-    qr_grid_sync(p.bar, (++nbar) * (unsigned)p.G);
-    // (C) s_c = (a_jc + sum) * tau; a_jc -= s_c; a_ic -= s_c v_i (_jit.py:213-218)
-    for (int c = j + 1 + warp; c < w; c += QR_THREADS / 32) {
-      const double t = qr_sum_partials(p.dots + (int64_t)par * p.G * QR_LW + c, p.G, QR_LW, lane);
-      if (lane == 0) sc[c] = (__ldcg(p.drow + par * 32 + c) + t) * tj;
-    }
-    __syncthreads();
-    if (own_d)
-      for (int c = j + 1 + tid; c < w; c += QR_THREADS) tile[dl * QR_LDT + c] -= sc[c];
+    // (C) v = x * scale; a_ic -= s_c v_i; a_jj = beta; a_jc -= s_c (_jit.py:206-218)
     for (int r = rfirst + tid; r < nrows; r += QR_THREADS) {
       double* tr = tile + r * QR_LDT;
-      const double v = tr[j];
+      const double v = tr[j] * scale;
+      tr[j] = v;
       for (int c = j + 1; c < w; ++c) tr[c] -= sc[c] * v;
+    }
+    if (own_d) {
+      if (tid == 0) tile[dl * QR_LDT + j] = beta;
+      for (int c = j + 1 + tid; c < w; c += QR_THREADS) tile[dl * QR_LDT + c] -= sc[c];
     }
     __syncthreads();
   }
@@ -203,10 +204,64 @@ __global__ void qr_split_reduce_kernel(const double* __restrict__ part, int64_t 
 }
 
 // larft (factor.py:174-189): T[j][j] = tau_j, T[:j, j] = -tau_j T[:j, :j] (V^T v_j), from
-// gneg = -(V^T V).  Writes tt = T^T (k x k, ld ldt) including the zero upper part.  One CTA,
-// thread i owns row i of T (column i of tt: coalesced reads of tt rows).
-__global__ void qr_larft_kernel(const double* __restrict__ gneg, int64_t ldg, const double* __restrict__ tau, int k,
-                                double* tt, int64_t ldt) {
+// gneg = -(V^T V).  Writes tt = T^T (k x k, ld ldt) including the zero upper part.
+// Blocked over 32-column blocks (one CTA of 1024 threads, k <= 512): every diagonal block by its own
+// warp with the column recurrence, then block column J from the merge rule of two compact-WY
+// factors, T[0:J0, J] = -T[0:J0, 0:J0] (G[0:J0, J] T_JJ) -- the same T, rounded differently.
+constexpr int QR_LARFT_THREADS = 1024;
+constexpr int QR_LARFT_MAXK = 512;
+__global__ void __launch_bounds__(QR_LARFT_THREADS, 1)
+qr_larft_kernel(const double* __restrict__ gneg, int64_t ldg, const double* __restrict__ tau, int k, double* tt,
+                int64_t ldt) {
+  extern __shared__ double qr_x[];  // (ceil(k/32) - 1) * 32 x 32: G[0:J0, J] T_JJ
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t idx = tid; idx < (int64_t)k * k; idx += QR_LARFT_THREADS) {
+    const int r = (int)(idx / k), c = (int)(idx - (int64_t)r * k);
+    if (c > r) tt[(int64_t)r * ldt + c] = 0.0;
+  }
+  const int nb = (k + 31) / 32;
+  // diagonal blocks: lane i owns row i of T_II; T[i][l] lives at tt[l][i]
+  for (int bI = warp; bI < nb; bI += QR_LARFT_THREADS / 32) {
+    const int I0 = bI * 32, bs = min(32, k - I0);
+    for (int j = 0; j < bs; ++j) {
+      const double tj = tau[I0 + j];
+      const int i = lane;
+      double acc = 0.0;
+      if (i < j)
+        for (int l = i; l < j; ++l) acc += tt[(int64_t)(I0 + l) * ldt + I0 + i] * -gneg[(int64_t)(I0 + l) * ldg + I0 + j];
+      __syncwarp();
+      if (i < j) tt[(int64_t)(I0 + j) * ldt + I0 + i] = -tj * acc;
+      else if (i == j) tt[(int64_t)(I0 + j) * ldt + I0 + j] = tj;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int bJ = 1; bJ < nb; ++bJ) {
+    const int J0 = bJ * 32, bs = min(32, k - J0);
+    // X[r][c] = sum_{l <= c} G[r][J0 + l] T_JJ[l][c]
+    for (int idx = tid; idx < J0 * 32; idx += QR_LARFT_THREADS) {
+      const int r = idx >> 5, c = idx & 31;
+      double acc = 0.0;
+      if (c < bs)
+        for (int l = 0; l <= c; ++l) acc += -gneg[(int64_t)r * ldg + J0 + l] * tt[(int64_t)(J0 + c) * ldt + J0 + l];
+      qr_x[idx] = acc;
+    }
+    __syncthreads();
+    // T[r][J0 + c] = -sum_{l = r}^{J0 - 1} T[r][l] X[l][c]   (T[r][l] = tt[l][r])
+    for (int idx = tid; idx < J0 * 32; idx += QR_LARFT_THREADS) {
+      const int r = idx >> 5, c = idx & 31;
+      if (c >= bs) continue;
+      double acc = 0.0;
+      for (int l = r; l < J0; ++l) acc += tt[(int64_t)l * ldt + r] * qr_x[l * 32 + c];
+      tt[(int64_t)(J0 + c) * ldt + r] = -acc;
+    }
+    __syncthreads();
+  }
+}
+
+// Column recurrence in one CTA (any k <= 1024; used above QR_LARFT_MAXK).
+__global__ void qr_larft_seq_kernel(const double* __restrict__ gneg, int64_t ldg, const double* __restrict__ tau,
+                                    int k, double* tt, int64_t ldt) {
   extern __shared__ double qr_y[];
   for (int64_t idx = threadIdx.x; idx < (int64_t)k * k; idx += blockDim.x) {
     const int r = (int)(idx / k), c = (int)(idx - (int64_t)r * k);
@@ -287,6 +342,8 @@ static int qr_ctx(DevCtx& c, QrCtx** out) {
   if (!q.ready) {
     CK(cudaMalloc(&q.leafx, sizeof(double) * (2 * QR_MAXG + 2 * QR_MAXG * QR_LW + 128)));
     CK(cudaMalloc(&q.bar, 64));
+    CK(cudaFuncSetAttribute(qr_larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double) * 32 * (QR_LARFT_MAXK - 32))));
     CK(cudaFuncSetAttribute(qr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)std::min<size_t>(c.smem_optin, 227 * 1024) - 1024));
     q.ready = true;
@@ -360,9 +417,14 @@ static int qr_build(DevCtx& c, QrScratch& ws, QrRefl& R, const double* a, int64_
   g_launches.fetch_add(1, std::memory_order_relaxed);
   CKR(ws.g.need((size_t)(k * R.ldt)));
   CKR(qr_gemm_neg(c, ws, ws.g.p, R.ldt, R.vt.p, R.ldvt, R.vd.p, R.ldv, k, k, R.mp, st));
-  const int thr = std::max(32, (k + 31) / 32 * 32);
-  if (thr > 1024) return set_err(PFLU_ERR_UNSUPPORTED, "QR block size %d > 1024", k);
-  qr_larft_kernel<<<1, thr, sizeof(double) * k, st>>>(ws.g.p, R.ldt, d_tau, k, R.tt.p, R.ldt);
+  if (k <= QR_LARFT_MAXK) {
+    qr_larft_kernel<<<1, QR_LARFT_THREADS, sizeof(double) * 32 * 32 * ((k + 31) / 32 - 1), st>>>(ws.g.p, R.ldt, d_tau, k,
+                                                                                        R.tt.p, R.ldt);
+  } else {
+    const int thr = std::max(32, (k + 31) / 32 * 32);
+    if (thr > 1024) return set_err(PFLU_ERR_UNSUPPORTED, "QR block size %d > 1024", k);
+    qr_larft_seq_kernel<<<1, thr, sizeof(double) * k, st>>>(ws.g.p, R.ldt, d_tau, k, R.tt.p, R.ldt);
+  }
   CK(cudaGetLastError());
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return PFLU_OK;
