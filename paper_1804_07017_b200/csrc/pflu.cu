@@ -1414,7 +1414,7 @@ int pflu_qr_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, i
   CKR(ctx_get(&c));
   QrCtx* q = nullptr;
   CKR(qr_ctx(*c, &q));
-  CKR(qr_panel(*c, *q, d_a, lda, m, d, col, w, d_tau, (cudaStream_t)stream));
+  CKR(qr_panel(*c, *q, d_a, lda, m, d, col, w, d_tau, q->leaf, (cudaStream_t)stream));
   return PFLU_OK;
 }
 
@@ -1464,7 +1464,7 @@ int pflu_apply_block_reflector(const double* d_v, int64_t ldv, int64_t mp, int64
   CKR(qr_ctx(*c, &q));
   cudaStream_t st = (cudaStream_t)stream;
   CKR(qr_build(*c, q->ws[0], q->leaf, d_v, ldv, 0, mp, 0, (int)k, d_tau, st));
-  CKR(qr_apply(*c, q->ws[0], q->leaf, d_c, ldc, nc, st));
+  CKR(qr_apply(*c, q->ws[0], qr_view(q->leaf), d_c, ldc, nc, st));
   return PFLU_OK;
 }
 

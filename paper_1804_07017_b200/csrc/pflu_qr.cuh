@@ -32,15 +32,25 @@ static int g_qr_rows = []() { const char* e = getenv("PFLU_QR_ROWS"); return e ?
 struct QrLeafArgs {
   double* a;
   int64_t lda;
-  int64_t r0, m;   // panel rows [r0, m); the diagonal of leaf column j is row r0 + j
+  int64_t r0, m;   // leaf rows [r0, m); the diagonal of leaf column j is row r0 + j
   int64_t c0;      // leaf columns [c0, c0 + w)
   int w;
   int G, R;        // CTAs, rows per CTA
   double* tau;     // tau of leaf column j at tau[j]
-  double* part;    // [2][G] sum-of-squares partials (column parity)
-  double* dots;    // [2][G][32] partial v^T a_c
-  double* drow;    // [2][32] diagonal row, [64 + parity] alpha
+  double* dots;    // [2][G][32] partial x^T a_c (column parity)
+  double* drow;    // [2][32] diagonal row
+  double* gram;    // [G][32 x 32] partial V^T V of the finished leaf
   unsigned* bar;   // grid barrier counter, zeroed before the launch
+  // the enclosing panel's block reflector (rows [r0 - p0, m)): this leaf writes its columns
+  // [p0, p0 + w) of V (vd, ld ldv) and V^T (vt, ld ldvt), zeros above, and its diagonal block of
+  // T^T (tt, ld ldt)
+  double* vd;
+  int64_t ldv;
+  double* vt;
+  int64_t ldvt;
+  double* tt;
+  int64_t ldt;
+  int p0;
 };
 
 __device__ __forceinline__ double qr_warp_sum(double v) {
@@ -75,11 +85,18 @@ __device__ __forceinline__ double qr_sum_partials(const double* src, int G, int 
 // (c = j) and every raw dot x^T a_c (c > j) are reduced together BEFORE the norm is known; every
 // CTA then derives beta, tau, scale and s_c from the same sums (same order, same bits) and updates
 // its rows.  Rounding differs from the reference's sequential order (parity is to tolerance).
+// After the last column the leaf also emits its part of the panel's block reflector: V and V^T
+// (unit diagonal, zeros above) and, from one more exchange of partial Gram matrices, its 32x32
+// diagonal block of T (the column recurrence of larft, factor.py:174-189) -- so the in-panel block
+// reflector needs no separate make-V / Gram / larft launches.
+// (An NCCL-LL style variant without the grid barrier -- flagged 16-byte partials polled by every
+// CTA -- measured slower: 0.264 vs 0.214 ms per 32768 x 32 leaf, polling contention on shared lines.)
 __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
   extern __shared__ __align__(16) double qr_smem[];
   double* tile = qr_smem;  // R x QR_LDT
   __shared__ double sc[QR_LW];   // column sums, then s_c
   __shared__ double dr[QR_LW];   // diagonal row
+  __shared__ double tl[QR_LW];   // tau of the leaf's columns
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q = blockIdx.x;
   constexpr int NW = QR_THREADS / 32;
   const int64_t rbeg = p.r0 + (int64_t)q * p.R;
@@ -134,7 +151,10 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
     __syncthreads();
     const double sq = sc[j], alpha = dr[j];
     if (sq == 0.0) {  // null reflector, column unchanged (uniform over the grid; _jit.py:203-205)
-      if (q == 0 && tid == 0) p.tau[j] = 0.0;
+      if (tid == 0) {
+        tl[j] = 0.0;
+        if (q == 0) p.tau[j] = 0.0;
+      }
       __syncthreads();
       continue;
     }
@@ -142,7 +162,10 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
     const double beta = alpha >= 0.0 ? -norm : norm;
     const double tj = (beta - alpha) / beta;
     const double scale = 1.0 / (alpha - beta);
-    if (q == 0 && tid == 0) p.tau[j] = tj;
+    if (tid == 0) {
+      tl[j] = tj;
+      if (q == 0) p.tau[j] = tj;
+    }
     __syncthreads();  // every thread read sc[j] before it is overwritten below
     if (tid < w && tid > j) sc[tid] = (dr[tid] + scale * sc[tid]) * tj;
     __syncthreads();
@@ -159,9 +182,72 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
     }
     __syncthreads();
   }
+  // write back; V (row-major) and V^T of the leaf's columns into the panel's reflector block
+  const int64_t rho0 = rbeg - p.r0;  // leaf-local index of this CTA's first row
+  auto vval = [&](int r, int c) -> double {
+    const int64_t rho = rho0 + r;
+    return rho > c ? tile[r * QR_LDT + c] : (rho == c ? 1.0 : 0.0);
+  };
   for (int idx = tid; idx < nrows * w; idx += QR_THREADS) {
     const int r = idx / w, c = idx - r * w;
     p.a[(rbeg + r) * p.lda + p.c0 + c] = tile[r * QR_LDT + c];
+    p.vd[(p.p0 + rho0 + r) * p.ldv + p.p0 + c] = vval(r, c);
+  }
+  for (int idx = tid; idx < nrows * w; idx += QR_THREADS) {
+    const int c = idx / nrows, r = idx - c * nrows;
+    p.vt[(int64_t)(p.p0 + c) * p.ldvt + p.p0 + rho0 + r] = vval(r, c);
+  }
+  if (q == 0) {  // rows of the panel above this leaf: zeros in the leaf's columns
+    for (int idx = tid; idx < p.p0 * w; idx += QR_THREADS) {
+      const int r = idx / w, c = idx - r * w;
+      p.vd[(int64_t)r * p.ldv + p.p0 + c] = 0.0;
+    }
+    for (int idx = tid; idx < p.p0 * w; idx += QR_THREADS) {
+      const int c = idx / p.p0, r = idx - c * p.p0;
+      p.vt[(int64_t)(p.p0 + c) * p.ldvt + r] = 0.0;
+    }
+  }
+  // partial Gram v_x^T v_y (x < y) over this CTA's rows: rows below y contribute v_rx v_ry, row y v_yx
+  for (int e = tid; e < w * w; e += QR_THREADS) {
+    const int x = e / w, y = e - x * w;
+    if (x >= y) continue;
+    double acc = 0.0;
+    const int rs = (int)min((int64_t)nrows, max((int64_t)0, y - rho0));
+    if (rs < nrows && rho0 + rs == y) acc = tile[rs * QR_LDT + x];
+    for (int r = (rho0 + rs == y && rs < nrows) ? rs + 1 : rs; r < nrows; ++r)
+      acc += tile[r * QR_LDT + x] * tile[r * QR_LDT + y];
+    p.gram[(int64_t)q * QR_LW * QR_LW + x * QR_LW + y] = acc;
+  }
+  qr_grid_sync(p.bar, (unsigned)(w + 1) * (unsigned)p.G);
+  if (q != 0) return;
+  // CTA 0: G = sum of the partials (fixed order), T by the column recurrence, T^T block out
+  double* gs = qr_smem;                  // 32 x 33 (the tile is no longer needed)
+  double* ts = qr_smem + QR_LW * QR_LDT; // 32 x 33
+  for (int e = tid; e < w * w; e += QR_THREADS) {
+    const int x = e / w, y = e - x * w;
+    double acc = 0.0;
+    if (x < y)
+      for (int i = 0; i < p.G; ++i) acc += __ldcg(p.gram + (int64_t)i * QR_LW * QR_LW + x * QR_LW + y);
+    gs[x * QR_LDT + y] = acc;
+    ts[x * QR_LDT + y] = 0.0;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int i = lane;
+    for (int j = 0; j < w; ++j) {
+      double acc = 0.0;
+      if (i < j)
+        for (int l = i; l < j; ++l) acc += ts[i * QR_LDT + l] * gs[l * QR_LDT + j];
+      __syncwarp();
+      if (i < j) ts[i * QR_LDT + j] = -tl[j] * acc;
+      else if (i == j) ts[i * QR_LDT + j] = tl[j];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < w * w; e += QR_THREADS) {
+    const int r = e / w, c = e - r * w;  // tt[r][c] = T[c][r]
+    p.tt[(int64_t)(p.p0 + r) * p.ldt + p.p0 + c] = c <= r ? ts[c * QR_LDT + r] : 0.0;
   }
 }
 
@@ -212,16 +298,17 @@ constexpr int QR_LARFT_THREADS = 1024;
 constexpr int QR_LARFT_MAXK = 512;
 __global__ void __launch_bounds__(QR_LARFT_THREADS, 1)
 qr_larft_kernel(const double* __restrict__ gneg, int64_t ldg, const double* __restrict__ tau, int k, double* tt,
-                int64_t ldt) {
+                int64_t ldt, int diag_given) {
   extern __shared__ double qr_x[];  // (ceil(k/32) - 1) * 32 x 32: G[0:J0, J] T_JJ
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t idx = tid; idx < (int64_t)k * k; idx += QR_LARFT_THREADS) {
     const int r = (int)(idx / k), c = (int)(idx - (int64_t)r * k);
-    if (c > r) tt[(int64_t)r * ldt + c] = 0.0;
+    if (c > r && (!diag_given || (c >> 5) != (r >> 5))) tt[(int64_t)r * ldt + c] = 0.0;  // given diagonal blocks stay
   }
   const int nb = (k + 31) / 32;
-  // diagonal blocks: lane i owns row i of T_II; T[i][l] lives at tt[l][i]
-  for (int bI = warp; bI < nb; bI += QR_LARFT_THREADS / 32) {
+  // diagonal blocks (unless the leaf kernels already wrote them): lane i owns row i of T_II;
+  // T[i][l] lives at tt[l][i]
+  for (int bI = diag_given ? nb : warp; bI < nb; bI += QR_LARFT_THREADS / 32) {
     const int I0 = bI * 32, bs = min(32, k - I0);
     for (int j = 0; j < bs; ++j) {
       const double tj = tau[I0 + j];
@@ -324,23 +411,18 @@ struct QrScratch {
 
 struct QrCtx {
   QrRefl refl[2];     // outer step reflectors, by step parity
-  QrRefl leaf;        // in-panel leaf reflector
+  QrRefl leaf;        // kernel-level entry points (pflu_qr_panel / pflu_larft / pflu_apply_block_reflector)
   QrScratch ws[2];    // 0: panel stream (leaves, TU_L), 1: trailing stream (TU_R)
-  double* leafx = nullptr;  // leaf kernel exchange: part, dots, drow
+  double* leafx = nullptr;  // leaf kernel exchange: dots, drow, partial Gram matrices
   unsigned* bar = nullptr;
   bool ready = false;
-  void release() {
-    for (auto& r : refl) { r.vd.release(); r.vt.release(); r.tt.release(); }
-    leaf.vd.release(); leaf.vt.release(); leaf.tt.release();
-    for (auto& s : ws) { s.w.release(); s.z.release(); s.g.release(); s.part.release(); }
-  }
 };
 static QrCtx g_qr[64];
 
 static int qr_ctx(DevCtx& c, QrCtx** out) {
   QrCtx& q = g_qr[c.dev];
   if (!q.ready) {
-    CK(cudaMalloc(&q.leafx, sizeof(double) * (2 * QR_MAXG + 2 * QR_MAXG * QR_LW + 128)));
+    CK(cudaMalloc(&q.leafx, sizeof(double) * (2 * QR_MAXG * QR_LW + 64 + QR_MAXG * QR_LW * QR_LW)));
     CK(cudaMalloc(&q.bar, 64));
     CK(cudaFuncSetAttribute(qr_larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double) * 32 * (QR_LARFT_MAXK - 32))));
@@ -349,6 +431,46 @@ static int qr_ctx(DevCtx& c, QrCtx** out) {
     q.ready = true;
   }
   *out = &q;
+  return PFLU_OK;
+}
+
+// A block reflector as the GEMMs see it (possibly a sub-block of a QrRefl).
+struct QrView {
+  const double* vd;
+  int64_t ldv;
+  const double* vt;
+  int64_t ldvt;
+  const double* tt;
+  int64_t ldt;
+  int64_t mp;
+  int k;
+};
+static QrView qr_view(const QrRefl& R) { return {R.vd.p, R.ldv, R.vt.p, R.ldvt, R.tt.p, R.ldt, R.mp, R.k}; }
+
+static int qr_refl_alloc(QrRefl& R, int64_t mp, int k) {
+  R.mp = mp;
+  R.k = k;
+  R.ldv = qr_even(k);
+  R.ldvt = qr_even(mp);
+  R.ldt = qr_even(k);
+  CKR(R.vd.need((size_t)(R.mp * R.ldv)));
+  CKR(R.vt.need((size_t)(k * R.ldvt)));
+  CKR(R.tt.need((size_t)(k * R.ldt)));
+  return PFLU_OK;
+}
+
+static int qr_larft_launch(QrScratch& ws, QrRefl& R, const double* d_tau, int diag_given, cudaStream_t st) {
+  const int k = R.k;
+  if (k <= QR_LARFT_MAXK) {
+    qr_larft_kernel<<<1, QR_LARFT_THREADS, sizeof(double) * 32 * 32 * ((k + 31) / 32 - 1), st>>>(
+        ws.g.p, R.ldt, d_tau, k, R.tt.p, R.ldt, diag_given);
+  } else {
+    const int thr = std::max(32, (k + 31) / 32 * 32);
+    if (thr > 1024) return set_err(PFLU_ERR_UNSUPPORTED, "QR block size %d > 1024", k);
+    qr_larft_seq_kernel<<<1, thr, sizeof(double) * k, st>>>(ws.g.p, R.ldt, d_tau, k, R.tt.p, R.ldt);
+  }
+  CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return PFLU_OK;
 }
 
@@ -400,79 +522,80 @@ static int qr_gemm_neg(DevCtx& c, QrScratch& ws, double* out, int64_t ldo, const
   return PFLU_OK;
 }
 
-// V, V^T and T^T of the reflectors stored at rows [d, m), columns [cv, cv + k).
+// V, V^T and T^T of the reflectors stored at rows [d, m), columns [cv, cv + k) (kernel-level
+// entry points; the factorization gets V / V^T / T's diagonal blocks from the leaf kernels).
 static int qr_build(DevCtx& c, QrScratch& ws, QrRefl& R, const double* a, int64_t lda, int64_t d, int64_t m,
                     int64_t cv, int k, const double* d_tau, cudaStream_t st) {
-  R.mp = m - d;
-  R.k = k;
-  R.ldv = qr_even(k);
-  R.ldvt = qr_even(R.mp);
-  R.ldt = qr_even(k);
-  CKR(R.vd.need((size_t)(R.mp * R.ldv)));
-  CKR(R.vt.need((size_t)(k * R.ldvt)));
-  CKR(R.tt.need((size_t)(k * R.ldt)));
+  CKR(qr_refl_alloc(R, m - d, k));
   dim3 g((unsigned)((R.mp + 31) / 32), (unsigned)((k + 31) / 32));
   qr_make_v_kernel<<<g, dim3(32, 8), 0, st>>>(a, lda, d, cv, R.mp, k, R.vd.p, R.ldv, R.vt.p, R.ldvt);
   CK(cudaGetLastError());
   g_launches.fetch_add(1, std::memory_order_relaxed);
   CKR(ws.g.need((size_t)(k * R.ldt)));
   CKR(qr_gemm_neg(c, ws, ws.g.p, R.ldt, R.vt.p, R.ldvt, R.vd.p, R.ldv, k, k, R.mp, st));
-  if (k <= QR_LARFT_MAXK) {
-    qr_larft_kernel<<<1, QR_LARFT_THREADS, sizeof(double) * 32 * 32 * ((k + 31) / 32 - 1), st>>>(ws.g.p, R.ldt, d_tau, k,
-                                                                                        R.tt.p, R.ldt);
-  } else {
-    const int thr = std::max(32, (k + 31) / 32 * 32);
-    if (thr > 1024) return set_err(PFLU_ERR_UNSUPPORTED, "QR block size %d > 1024", k);
-    qr_larft_seq_kernel<<<1, thr, sizeof(double) * k, st>>>(ws.g.p, R.ldt, d_tau, k, R.tt.p, R.ldt);
-  }
-  CK(cudaGetLastError());
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return PFLU_OK;
+  return qr_larft_launch(ws, R, d_tau, 0, st);
+}
+
+// T of a panel whose leaves already wrote V, V^T and T's 32x32 diagonal blocks: the Gram matrix
+// on the split-K DMMA GEMM, then only the off-diagonal merges of larft.
+static int qr_finish_t(DevCtx& c, QrScratch& ws, QrRefl& R, const double* d_tau, cudaStream_t st) {
+  if (R.k <= 32) return PFLU_OK;
+  CKR(ws.g.need((size_t)(R.k * R.ldt)));
+  CKR(qr_gemm_neg(c, ws, ws.g.p, R.ldt, R.vt.p, R.ldvt, R.vd.p, R.ldv, R.k, R.k, R.mp, st));
+  return qr_larft_launch(ws, R, d_tau, R.k <= QR_LARFT_MAXK ? 1 : 0, st);
 }
 
 // C (rows [d, m) of columns [lo, lo + nc)) := C - V (T^T (V^T C))   (factor.py:192-205)
-static int qr_apply(DevCtx& c, QrScratch& ws, const QrRefl& R, double* cp, int64_t ldc, int64_t nc, cudaStream_t st) {
+static int qr_apply(DevCtx& c, QrScratch& ws, const QrView& R, double* cp, int64_t ldc, int64_t nc, cudaStream_t st) {
   if (nc <= 0 || R.k <= 0 || R.mp <= 0) return PFLU_OK;
   const int64_t ldw = qr_even(nc);
   CKR(ws.w.need((size_t)(R.k * ldw)));
   CKR(ws.z.need((size_t)(R.k * ldw)));
   // W = -(V^T C), Z = -(T^T W) = T^T V^T C, C -= V Z
-  CKR(qr_gemm_neg(c, ws, ws.w.p, ldw, R.vt.p, R.ldvt, cp, ldc, R.k, nc, R.mp, st));
-  CKR(qr_gemm_neg(c, ws, ws.z.p, ldw, R.tt.p, R.ldt, ws.w.p, ldw, R.k, nc, R.k, st));
-  CKR(launch_gemm(cp, ldc, R.vd.p, R.ldv, ws.z.p, ldw, R.mp, nc, R.k, false, st));
+  CKR(qr_gemm_neg(c, ws, ws.w.p, ldw, R.vt, R.ldvt, cp, ldc, R.k, nc, R.mp, st));
+  CKR(qr_gemm_neg(c, ws, ws.z.p, ldw, R.tt, R.ldt, ws.w.p, ldw, R.k, nc, R.k, st));
+  CKR(launch_gemm(cp, ldc, R.vd, R.ldv, ws.z.p, ldw, R.mp, nc, R.k, false, st));
   return PFLU_OK;
 }
 
 // Householder factorization of the panel rows [d, m), columns [col, col + w): 32-column leaves,
-// each followed by its block reflector on the panel's remaining columns.
+// each followed by its block reflector on the panel's remaining columns.  On return R holds the
+// panel's V, V^T and the 32x32 diagonal blocks of T^T (qr_finish_t completes T).
 static int qr_panel(DevCtx& c, QrCtx& q, double* a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w,
-                    double* d_tau, cudaStream_t st) {
+                    double* d_tau, QrRefl& Rf, cudaStream_t st) {
+  CKR(qr_refl_alloc(Rf, m - d, (int)w));
+  const int64_t smax = (int64_t)std::min<size_t>(c.smem_optin, 227 * 1024) - 1024;
+  const int gcap = std::min(c.sms, QR_MAXG);
   for (int64_t p0 = 0; p0 < w; p0 += QR_LW) {
     const int lw = (int)std::min<int64_t>(QR_LW, w - p0);
     const int64_t r0 = d + p0, mp = m - r0;
-    int R = std::max<int64_t>(g_qr_rows > 0 ? g_qr_rows : 512, (mp + c.sms - 1) / c.sms);
-    const int64_t smax = (int64_t)std::min<size_t>(c.smem_optin, 227 * 1024) - 1024;
-    if ((int64_t)R * QR_LDT * 8 > smax) return set_err(PFLU_ERR_UNSUPPORTED, "QR panel of %lld rows too tall", (long long)mp);
-    int G = (int)((mp + R - 1) / R);
-    if (G > QR_MAXG || G > c.sms) return set_err(PFLU_ERR_UNSUPPORTED, "QR panel grid %d too large", G);
+    int R = (int)std::max<int64_t>(g_qr_rows > 0 ? g_qr_rows : 512, (mp + gcap - 1) / gcap);
+    const int G = (int)((mp + R - 1) / R);
     R = (int)((mp + G - 1) / G);
+    if ((int64_t)R * QR_LDT * 8 > smax) return set_err(PFLU_ERR_UNSUPPORTED, "QR panel of %lld rows too tall", (long long)mp);
+    if (G > QR_MAXG || G > c.sms) return set_err(PFLU_ERR_UNSUPPORTED, "QR panel grid %d too large", G);
     QrLeafArgs la;
     la.a = a; la.lda = lda; la.r0 = r0; la.m = m; la.c0 = col + p0; la.w = lw;
     la.G = G; la.R = R;
     la.tau = d_tau + p0;
-    la.part = q.leafx;
-    la.dots = q.leafx + 2 * QR_MAXG;
-    la.drow = q.leafx + 2 * QR_MAXG + 2 * QR_MAXG * QR_LW;
+    la.dots = q.leafx;
+    la.drow = q.leafx + 2 * QR_MAXG * QR_LW;
+    la.gram = q.leafx + 2 * QR_MAXG * QR_LW + 64;
     la.bar = q.bar;
-    CK(cudaMemsetAsync(q.bar, 0, sizeof(unsigned), st));
+    la.vd = Rf.vd.p; la.ldv = Rf.ldv;
+    la.vt = Rf.vt.p; la.ldvt = Rf.ldvt;
+    la.tt = Rf.tt.p; la.ldt = Rf.ldt;
+    la.p0 = (int)p0;
     void* args[] = {&la};
-    CK(cudaLaunchCooperativeKernel((void*)qr_leaf_kernel, dim3(G), dim3(QR_THREADS), args,
-                                   (size_t)R * QR_LDT * 8, st));
+    CK(cudaMemsetAsync(q.bar, 0, sizeof(unsigned), st));
+    const size_t smem = (size_t)std::max(R, 2 * QR_LW) * QR_LDT * 8;
+    CK(cudaLaunchCooperativeKernel((void*)qr_leaf_kernel, dim3(G), dim3(QR_THREADS), args, smem, st));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const int64_t rest = w - p0 - lw;
     if (rest > 0) {
-      CKR(qr_build(c, q.ws[0], q.leaf, a, lda, r0, m, col + p0, lw, d_tau + p0, st));
-      CKR(qr_apply(c, q.ws[0], q.leaf, a + r0 * lda + col + p0 + lw, lda, rest, st));
+      const QrView v = {Rf.vd.p + p0 * Rf.ldv + p0, Rf.ldv, Rf.vt.p + p0 * Rf.ldvt + p0, Rf.ldvt,
+                        Rf.tt.p + p0 * Rf.ldt + p0, Rf.ldt, mp, lw};
+      CKR(qr_apply(c, q.ws[0], v, a + r0 * lda + col + p0 + lw, lda, rest, st));
     }
   }
   return PFLU_OK;
@@ -496,11 +619,11 @@ static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   if (lookahead == 0) {
     for (int64_t k = 0; k < steps; ++k) {
       const int64_t col0 = k * b, bw = bw_of(k), lo = col0 + bw;
-      CKR(qr_panel(c, q, a, lda, m, col0, col0, bw, d_tau + col0, sP));
+      QrRefl& R = q.refl[k & 1];
+      CKR(qr_panel(c, q, a, lda, m, col0, col0, bw, d_tau + col0, R, sP));
       if (lo < n) {
-        QrRefl& R = q.refl[k & 1];
-        CKR(qr_build(c, q.ws[0], R, a, lda, col0, m, col0, (int)bw, d_tau + col0, sP));
-        CKR(qr_apply(c, q.ws[0], R, a + col0 * lda + lo, lda, n - lo, sP));
+        CKR(qr_finish_t(c, q.ws[0], R, d_tau + col0, sP));
+        CKR(qr_apply(c, q.ws[0], qr_view(R), a + col0 * lda + lo, lda, n - lo, sP));
       }
     }
     CK(cudaEventRecord(e_out, sP));
@@ -508,23 +631,23 @@ static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     return PFLU_OK;
   }
   // look-ahead 1
-  CKR(qr_panel(c, q, a, lda, m, 0, 0, bw_of(0), d_tau, sP));
+  CKR(qr_panel(c, q, a, lda, m, 0, 0, bw_of(0), d_tau, q.refl[0], sP));
   for (int64_t k = 0; k < steps; ++k) {
     const int64_t col0 = k * b, bw = bw_of(k), lo = col0 + bw;
     if (lo >= n) break;
     QrRefl& R = q.refl[k & 1];
-    CKR(qr_build(c, q.ws[0], R, a, lda, col0, m, col0, (int)bw, d_tau + col0, sP));
+    CKR(qr_finish_t(c, q.ws[0], R, d_tau + col0, sP));
     CK(cudaEventRecord(e_pf, sP));
     // TU_R(k): columns beyond block k+1, on the trailing stream
     const int64_t lo2 = lo + bw_of(k + 1);
     if (lo2 < n) {
       CK(cudaStreamWaitEvent(sU, e_pf, 0));
-      CKR(qr_apply(c, q.ws[1], R, a + col0 * lda + lo2, lda, n - lo2, sU));
+      CKR(qr_apply(c, q.ws[1], qr_view(R), a + col0 * lda + lo2, lda, n - lo2, sU));
     }
     // TU_L(k) + PF(k+1) on the panel stream; TU_R(k-1) (recorded before e_tu is re-recorded
     // below) finished updating block k+1
-    CKR(qr_apply(c, q.ws[0], R, a + col0 * lda + lo, lda, bw_of(k + 1), sP));
-    CKR(qr_panel(c, q, a, lda, m, lo, lo, bw_of(k + 1), d_tau + lo, sP));
+    CKR(qr_apply(c, q.ws[0], qr_view(R), a + col0 * lda + lo, lda, bw_of(k + 1), sP));
+    CKR(qr_panel(c, q, a, lda, m, lo, lo, bw_of(k + 1), d_tau + lo, q.refl[(k + 1) & 1], sP));
     // the next TU_L / build (which rewrites refl[(k+1)&1] ... refl[k&1] at step k+2) must follow TU_R(k)
     if (lo2 < n) {
       CK(cudaEventRecord(e_tu, sU));

@@ -188,3 +188,26 @@ def test_qr_device_buffers_and_lookahead_agree(cuda):
     assert float((f1 - f0).abs().max()) / float(ta.abs().max()) <= 1e-10
     back, orth = gpu_qr_residual(a, f1.cpu().numpy(), t1.cpu().numpy())
     assert back <= 10 and orth <= 10
+
+
+def test_qr_deterministic_across_processes(cuda):
+    """Every reduction (leaf exchanges, split-K slices) sums in a fixed order, so two runs in fresh
+    processes give bitwise identical factors and tau."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "from paper_1804_07017_b200 import qr_factor\n"
+        "a = np.random.default_rng(4).uniform(-1, 1, (20000, 96))\n"
+        "f, t = qr_factor(a, b=64, lookahead=1)\n"
+        "np.save(sys.argv[1], np.concatenate([f.ravel(), t]))\n")
+    outs = []
+    for rep in range(2):
+        path = os.path.join("/tmp", f"qr_det{rep}.npy")
+        r = subprocess.run([sys.executable, "-c", code, path], cwd=root, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert outs[0].tobytes() == outs[1].tobytes()
