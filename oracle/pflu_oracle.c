@@ -200,27 +200,37 @@ int64_t orc_lu_prefix(double *a, int64_t m, int64_t n, int64_t lda, int64_t *piv
  *   orc_geqrf     <- dmf_mtb (factor.py:382-412) with kind=Kind.QR: per panel qr_unb + larft,
  *                    then the block reflector on the columns to the right.
  */
-void orc_qr_unb(double *a, int64_t m, int64_t w, int64_t lda, double *tau) {
+/* The panel is staged column-major (the reference's own F-order layout) so the column loops are
+ * contiguous; the arithmetic is op for op _jit.qr_unb_run. */
+void orc_qr_unb(double *a0, int64_t m, int64_t w, int64_t lda0, double *tau) {
+  double *a = (double *)malloc((size_t)(m * w) * sizeof(double));
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < w; ++j) a[j * m + i] = a0[IDX(i, j, lda0)];
+#define A_(i, j) a[(int64_t)(j) * m + (i)]
   for (int64_t j = 0; j < w; ++j) {
-    const double alpha = a[IDX(j, j, lda)];
+    const double alpha = A_(j, j);
     double sq = 0.0;
-    for (int64_t i = j + 1; i < m; ++i) { double v = a[IDX(i, j, lda)]; double t = v * v; sq = sq + t; }
+    for (int64_t i = j + 1; i < m; ++i) { double v = A_(i, j); double t = v * v; sq = sq + t; }
     if (sq == 0.0) { tau[j] = 0.0; continue; }
     double aa = alpha * alpha;
     const double norm = sqrt(aa + sq);
     const double beta = alpha >= 0.0 ? -norm : norm;
     tau[j] = (beta - alpha) / beta;
     const double scale = 1.0 / (alpha - beta);
-    for (int64_t i = j + 1; i < m; ++i) a[IDX(i, j, lda)] *= scale;
-    a[IDX(j, j, lda)] = beta;
+    for (int64_t i = j + 1; i < m; ++i) A_(i, j) *= scale;
+    A_(j, j) = beta;
     for (int64_t c = j + 1; c < w; ++c) {
-      double s = a[IDX(j, c, lda)];
-      for (int64_t i = j + 1; i < m; ++i) { double t = a[IDX(i, j, lda)] * a[IDX(i, c, lda)]; s = s + t; }
+      double s = A_(j, c);
+      for (int64_t i = j + 1; i < m; ++i) { double t = A_(i, j) * A_(i, c); s = s + t; }
       s = s * tau[j];
-      a[IDX(j, c, lda)] -= s;
-      for (int64_t i = j + 1; i < m; ++i) { double t = s * a[IDX(i, j, lda)]; a[IDX(i, c, lda)] -= t; }
+      A_(j, c) -= s;
+      for (int64_t i = j + 1; i < m; ++i) { double t = s * A_(i, j); A_(i, c) -= t; }
     }
   }
+#undef A_
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < w; ++j) a0[IDX(i, j, lda0)] = a[j * m + i];
+  free(a);
 }
 
 /* v(i, j) of the stored reflectors: unit diagonal, zero above, the panel below. */
@@ -228,16 +238,21 @@ static inline double vref(const double *v, int64_t ldv, int64_t i, int64_t j) {
   return i > j ? v[IDX(i, j, ldv)] : (i == j ? 1.0 : 0.0);
 }
 
-/* T (k x k row-major, upper) from the reflectors stored in the m x k panel v and tau. */
+/* T (k x k row-major, upper) from the reflectors stored in the m x k panel v and tau (V staged
+ * column-major so the products V[:, :j]^T v_j run down contiguous columns). */
 void orc_larft(const double *v, int64_t m, int64_t k, int64_t ldv, const double *tau, double *t) {
   for (int64_t i = 0; i < k * k; ++i) t[i] = 0.0;
   double *wv = (double *)calloc((size_t)(k > 0 ? k : 1), sizeof(double));
+  double *vc = (double *)malloc((size_t)(m * (k > 0 ? k : 1)) * sizeof(double));
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < k; ++j) vc[j * m + i] = vref(v, ldv, i, j);
   for (int64_t j = 0; j < k; ++j) {
     t[IDX(j, j, k)] = tau[j];
     if (!j) continue;
     for (int64_t l = 0; l < j; ++l) {
       double s = 0.0;
-      for (int64_t i = 0; i < m; ++i) { double p = vref(v, ldv, i, l) * vref(v, ldv, i, j); s = s + p; }
+      const double *x = vc + l * m, *y = vc + j * m;
+      for (int64_t i = 0; i < m; ++i) { double p = x[i] * y[i]; s = s + p; }
       wv[l] = s;
     }
     for (int64_t i = 0; i < j; ++i) {
@@ -246,36 +261,56 @@ void orc_larft(const double *v, int64_t m, int64_t k, int64_t ldv, const double 
       t[IDX(i, j, k)] = -tau[j] * s;
     }
   }
+  free(vc);
   free(wv);
 }
 
-/* c (m x nc) <- (I - V T V^T)^T c = c - V (T^T (V^T c)). */
+/* c (m x nc) <- (I - V T V^T)^T c = c - V (T^T (V^T c)).  Column blocks of c in parallel; inside a
+ * block the loops run row by row (cache friendly) but every element still sees its reference
+ * operation sequence (p ascending for W and C, l ascending for Z, multiply then add). */
 void orc_apply_block_reflector(const double *v, int64_t m, int64_t k, int64_t ldv, const double *t,
                                double *c, int64_t nc, int64_t ldc) {
   if (m <= 0 || nc <= 0 || k <= 0) return;
-  double *w = (double *)calloc((size_t)(k * nc), sizeof(double));
-  double *z = (double *)calloc((size_t)(k * nc), sizeof(double));
+  const int64_t JB = 64;
+  const int64_t nblk = (nc + JB - 1) / JB;
   int nt = nthreads();
-#pragma omp parallel for num_threads(nt) schedule(static) if (m * nc * k > 1000000)
-  for (int64_t j = 0; j < nc; ++j) {
-    for (int64_t r = 0; r < k; ++r) {          /* W = 0 + V^T C */
-      double acc = 0.0;
-      for (int64_t p = 0; p < m; ++p) { double q = vref(v, ldv, p, r) * c[IDX(p, j, ldc)]; acc = acc + q; }
-      w[IDX(r, j, nc)] = acc;
+#pragma omp parallel num_threads(nt) if (m * nc * k > 1000000)
+  {
+    double *w = (double *)malloc((size_t)(k * JB) * sizeof(double));
+    double *z = (double *)malloc((size_t)(k * JB) * sizeof(double));
+    double *vr = (double *)malloc((size_t)k * sizeof(double));
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t jb = 0; jb < nblk; ++jb) {
+      const int64_t j0 = jb * JB, jw = nc - j0 < JB ? nc - j0 : JB;
+      for (int64_t i = 0; i < k * JB; ++i) { w[i] = 0.0; z[i] = 0.0; }
+      for (int64_t p = 0; p < m; ++p) {                 /* W = 0 + V^T C, p ascending */
+        for (int64_t r = 0; r < k; ++r) vr[r] = vref(v, ldv, p, r);
+        const double *cp = c + IDX(p, j0, ldc);
+        for (int64_t r = 0; r < k; ++r) {
+          const double x = vr[r];
+          double *wr = w + r * JB;
+          for (int64_t jj = 0; jj < jw; ++jj) { double q = x * cp[jj]; wr[jj] = wr[jj] + q; }
+        }
+      }
+      for (int64_t l = 0; l < k; ++l)                  /* Z = T^T W, zero-seeded, l ascending */
+        for (int64_t i = l; i < k; ++i) {
+          const double tv = t[IDX(l, i, k)];
+          for (int64_t jj = 0; jj < jw; ++jj) { double q = tv * w[l * JB + jj]; z[i * JB + jj] = z[i * JB + jj] + q; }
+        }
+      for (int64_t i = 0; i < k * JB; ++i) z[i] = -z[i];
+      for (int64_t i = 0; i < m; ++i) {                 /* C += V (-Z), p ascending */
+        double *ci = c + IDX(i, j0, ldc);
+        for (int64_t p = 0; p < k; ++p) {
+          const double x = vref(v, ldv, i, p);
+          const double *zp = z + p * JB;
+          for (int64_t jj = 0; jj < jw; ++jj) { double q = x * zp[jj]; ci[jj] = ci[jj] + q; }
+        }
+      }
     }
-    for (int64_t l = 0; l < k; ++l) {          /* Z = T^T W, zero-seeded, l ascending */
-      const double xv = w[IDX(l, j, nc)];
-      for (int64_t i = l; i < k; ++i) { double q = t[IDX(l, i, k)] * xv; z[IDX(i, j, nc)] = z[IDX(i, j, nc)] + q; }
-    }
-    for (int64_t i = 0; i < k; ++i) z[IDX(i, j, nc)] = -z[IDX(i, j, nc)];
-    for (int64_t i = 0; i < m; ++i) {          /* C += V (-Z), p ascending */
-      double acc = c[IDX(i, j, ldc)];
-      for (int64_t p = 0; p < k; ++p) { double q = vref(v, ldv, i, p) * z[IDX(p, j, nc)]; acc = acc + q; }
-      c[IDX(i, j, ldc)] = acc;
-    }
+    free(w);
+    free(z);
+    free(vr);
   }
-  free(w);
-  free(z);
 }
 
 /* Blocked Householder QR, dmf_mtb order.  m >= n >= 1.  tau: double[n]. */

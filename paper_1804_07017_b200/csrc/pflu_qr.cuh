@@ -299,7 +299,7 @@ constexpr int QR_LARFT_MAXK = 512;
 __global__ void __launch_bounds__(QR_LARFT_THREADS, 1)
 qr_larft_kernel(const double* __restrict__ gneg, int64_t ldg, const double* __restrict__ tau, int k, double* tt,
                 int64_t ldt, int diag_given) {
-  extern __shared__ double qr_x[];  // (ceil(k/32) - 1) * 32 x 32: G[0:J0, J] T_JJ
+  extern __shared__ double qr_x[];  // (QR_LARFT_MAXK - 32) x 32: G[0:J0, J] T_JJ, then T_JJ (32 x 33)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t idx = tid; idx < (int64_t)k * k; idx += QR_LARFT_THREADS) {
     const int r = (int)(idx / k), c = (int)(idx - (int64_t)r * k);
@@ -323,27 +323,58 @@ qr_larft_kernel(const double* __restrict__ gneg, int64_t ldg, const double* __re
     }
   }
   __syncthreads();
+  // block column J: warp w owns rows r = w, w + 32, ...; lane = column c of the block
+  double* tjj = qr_x + (size_t)(QR_LARFT_MAXK - 32) * 32;  // 32 x 33: T_JJ
+  constexpr int RPW = QR_LARFT_MAXK / QR_LARFT_THREADS * 32 / 32;  // rows per warp (<= 16)
   for (int bJ = 1; bJ < nb; ++bJ) {
     const int J0 = bJ * 32, bs = min(32, k - J0);
-    // X[r][c] = sum_{l <= c} G[r][J0 + l] T_JJ[l][c]
-    for (int idx = tid; idx < J0 * 32; idx += QR_LARFT_THREADS) {
-      const int r = idx >> 5, c = idx & 31;
-      double acc = 0.0;
-      if (c < bs)
-        for (int l = 0; l <= c; ++l) acc += -gneg[(int64_t)r * ldg + J0 + l] * tt[(int64_t)(J0 + c) * ldt + J0 + l];
-      qr_x[idx] = acc;
+    for (int e = tid; e < 32 * 32; e += QR_LARFT_THREADS) {
+      const int l = e >> 5, c = e & 31;  // T_JJ[l][c] = tt[J0 + c][J0 + l]
+      tjj[l * 33 + c] = (l < bs && c < bs) ? tt[(int64_t)(J0 + c) * ldt + J0 + l] : 0.0;
     }
     __syncthreads();
-    // T[r][J0 + c] = -sum_{l = r}^{J0 - 1} T[r][l] X[l][c]   (T[r][l] = tt[l][r])
-    for (int idx = tid; idx < J0 * 32; idx += QR_LARFT_THREADS) {
-      const int r = idx >> 5, c = idx & 31;
-      if (c >= bs) continue;
+    // X[r][c] = sum_{l <= c} G[r][J0 + l] T_JJ[l][c]: the warp's G rows prefetched, then shuffles
+    {
+      double g[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int r = warp + 32 * t;
+        g[t] = (r < J0 && lane < bs) ? -gneg[(int64_t)r * ldg + J0 + lane] : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int r = warp + 32 * t;
+        if (r >= J0) break;
+        double acc = 0.0;
+        for (int l = 0; l < 32; ++l) {
+          const double gl = __shfl_sync(0xffffffffu, g[t], l);
+          if (l <= lane) acc += gl * tjj[l * 33 + lane];
+        }
+        qr_x[r * 32 + lane] = acc;
+      }
+    }
+    __syncthreads();
+    // T[r][J0 + c] = -sum_{l = r}^{J0 - 1} T[r][l] X[l][c]; T[r][l] = tt[l][r], 32 l per load round
+    for (int r = warp; r < J0; r += QR_LARFT_THREADS / 32) {
+      double tv[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int l = r + 32 * t + lane;
+        tv[t] = l < J0 ? tt[(int64_t)l * ldt + r] : 0.0;
+      }
       double acc = 0.0;
-      for (int l = r; l < J0; ++l) acc += tt[(int64_t)l * ldt + r] * qr_x[l * 32 + c];
-      tt[(int64_t)(J0 + c) * ldt + r] = -acc;
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int l0 = r + 32 * t;
+        if (l0 >= J0) break;
+        const int cnt = min(32, J0 - l0);
+        for (int i = 0; i < cnt; ++i) acc += __shfl_sync(0xffffffffu, tv[t], i) * qr_x[(l0 + i) * 32 + lane];
+      }
+      if (lane < bs) tt[(int64_t)(J0 + lane) * ldt + r] = -acc;
     }
     __syncthreads();
   }
+  (void)RPW;
 }
 
 // Column recurrence in one CTA (any k <= 1024; used above QR_LARFT_MAXK).
@@ -425,7 +456,7 @@ static int qr_ctx(DevCtx& c, QrCtx** out) {
     CK(cudaMalloc(&q.leafx, sizeof(double) * (2 * QR_MAXG * QR_LW + 64 + QR_MAXG * QR_LW * QR_LW)));
     CK(cudaMalloc(&q.bar, 64));
     CK(cudaFuncSetAttribute(qr_larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(sizeof(double) * 32 * (QR_LARFT_MAXK - 32))));
+                            (int)(sizeof(double) * ((QR_LARFT_MAXK - 32) * 32 + 32 * 33))));
     CK(cudaFuncSetAttribute(qr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)std::min<size_t>(c.smem_optin, 227 * 1024) - 1024));
     q.ready = true;
@@ -462,7 +493,7 @@ static int qr_refl_alloc(QrRefl& R, int64_t mp, int k) {
 static int qr_larft_launch(QrScratch& ws, QrRefl& R, const double* d_tau, int diag_given, cudaStream_t st) {
   const int k = R.k;
   if (k <= QR_LARFT_MAXK) {
-    qr_larft_kernel<<<1, QR_LARFT_THREADS, sizeof(double) * 32 * 32 * ((k + 31) / 32 - 1), st>>>(
+    qr_larft_kernel<<<1, QR_LARFT_THREADS, sizeof(double) * ((QR_LARFT_MAXK - 32) * 32 + 32 * 33), st>>>(
         ws.g.p, R.ldt, d_tau, k, R.tt.p, R.ldt, diag_given);
   } else {
     const int thr = std::max(32, (k + 31) / 32 * 32);
