@@ -1154,6 +1154,7 @@ int pflu_release_workspace(void) {
   c->hbuf = nullptr;
   c->hpiv = nullptr;
   c->hbuf_cap = c->hpiv_cap = 0;
+  g_qr[c->dev].release();
   return PFLU_OK;
 }
 
@@ -1361,6 +1362,8 @@ int pflu_geqrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b,
   return PFLU_OK;
 }
 
+// Host buffers: H2D into the grow-only device copy shared with pflu_getrf, the factorization, and a
+// D2H that streams every row block as soon as it is final (overlapping the rest of the run).
 int pflu_geqrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, double* tau) {
   if (!a) return -1;
   CKR(check_qr_dims(m, n, lda, b, lookahead));
@@ -1368,38 +1371,58 @@ int pflu_geqrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int look
   std::lock_guard<std::mutex> lk(g_mu);
   DevCtx* c = nullptr;
   CKR(ctx_get(&c));
-  const int64_t ld = qr_even(n);
-  double* d_a = nullptr;
-  double* d_tau = nullptr;
-  if (cudaMalloc(&d_a, sizeof(double) * (size_t)(m * ld)) != cudaSuccess) {
-    cudaGetLastError();
-    return set_err(PFLU_ERR_NOMEM, "pflu_geqrf: device copy of %lld x %lld", (long long)m, (long long)n);
-  }
-  if (cudaMalloc(&d_tau, sizeof(double) * (size_t)n) != cudaSuccess) {
-    cudaGetLastError();
-    cudaFree(d_a);
-    return set_err(PFLU_ERR_NOMEM, "pflu_geqrf: tau");
-  }
-  cudaStream_t st = c->sH;
-  int rc = PFLU_OK;
-  do {
-    if (cudaMemcpy2DAsync(d_a, ld * 8, a, lda * 8, n * 8, m, cudaMemcpyHostToDevice, st) != cudaSuccess) {
-      rc = set_err(PFLU_ERR_CUDA, "pflu_geqrf: H2D failed");
-      break;
+  QrCtx* q = nullptr;
+  CKR(qr_ctx(*c, &q));
+  const int64_t ldd = qr_even(n);
+  const size_t need = (size_t)m * ldd;
+  if (c->hbuf_cap < need) {
+    if (c->hbuf) CK(cudaFree(c->hbuf));
+    c->hbuf = nullptr;
+    c->hbuf_cap = 0;
+    if (cudaMalloc(&c->hbuf, sizeof(double) * need) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(PFLU_ERR_NOMEM, "pflu_geqrf: device copy of %lld x %lld", (long long)m, (long long)n);
     }
-    rc = geqrf_async(*c, d_a, m, n, ld, std::min(b, n), lookahead, d_tau, st);
-    if (rc != PFLU_OK) break;
-    if (cudaMemcpy2DAsync(a, lda * 8, d_a, ld * 8, n * 8, m, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaMemcpyAsync(tau, d_tau, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
-      rc = set_err(PFLU_ERR_CUDA, "pflu_geqrf: D2H failed");
-      break;
+    c->hbuf_cap = need;
+  }
+  CKR(q->htau.need((size_t)n));
+  double* d_a = c->hbuf;
+  double* d_tau = q->htau.p;
+  cudaStream_t st = c->sH, sD = c->sD;
+  if (cudaMemcpy2DAsync(d_a, ldd * 8, a, lda * 8, n * 8, m, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return set_err(PFLU_ERR_CUDA, "pflu_geqrf: H2D failed");
+  int64_t sent = 0;
+  size_t nev = 0;
+  auto next_event = [&](cudaEvent_t* e) -> int {
+    while (c->rev.size() <= nev) {
+      cudaEvent_t x;
+      CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+      c->rev.push_back(x);
     }
-    if (cudaStreamSynchronize(st) != cudaSuccess) rc = set_err(PFLU_ERR_CUDA, "pflu_geqrf: %s", cudaGetErrorString(cudaGetLastError()));
-  } while (0);
-  cudaStreamSynchronize(st);
-  cudaFree(d_a);
-  cudaFree(d_tau);
-  return rc;
+    *e = c->rev[nev++];
+    return PFLU_OK;
+  };
+  RowSink sink = [&](int64_t r0, int64_t r1, cudaStream_t after) -> int {
+    if (r0 != sent || r1 <= r0) return PFLU_OK;
+    cudaEvent_t e;
+    CKR(next_event(&e));
+    CK(cudaEventRecord(e, after));
+    CK(cudaStreamWaitEvent(sD, e, 0));
+    CK(cudaMemcpy2DAsync(a + r0 * lda, lda * 8, d_a + r0 * ldd, ldd * 8, n * 8, r1 - r0, cudaMemcpyDeviceToHost, sD));
+    sent = r1;
+    return PFLU_OK;
+  };
+  CKR(geqrf_async(*c, d_a, m, n, ldd, std::min(b, n), lookahead, d_tau, st, &sink));
+  cudaEvent_t e;
+  CKR(next_event(&e));
+  CK(cudaEventRecord(e, st));
+  CK(cudaStreamWaitEvent(sD, e, 0));
+  if (sent < m)
+    CK(cudaMemcpy2DAsync(a + sent * lda, lda * 8, d_a + sent * ldd, ldd * 8, n * 8, m - sent, cudaMemcpyDeviceToHost, sD));
+  CK(cudaMemcpyAsync(tau, d_tau, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, sD));
+  CK(cudaStreamSynchronize(sD));
+  CK(cudaStreamSynchronize(st));
+  return PFLU_OK;
 }
 
 int pflu_qr_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w, double* d_tau, void* stream) {

@@ -444,9 +444,15 @@ struct QrCtx {
   QrRefl refl[2];     // outer step reflectors, by step parity
   QrRefl leaf;        // kernel-level entry points (pflu_qr_panel / pflu_larft / pflu_apply_block_reflector)
   QrScratch ws[2];    // 0: panel stream (leaves, TU_L), 1: trailing stream (TU_R)
+  QrBuf htau;         // pflu_geqrf: device tau (grow-only)
   double* leafx = nullptr;  // leaf kernel exchange: dots, drow, partial Gram matrices
   unsigned* bar = nullptr;
   bool ready = false;
+  void release() {
+    for (QrRefl* r : {&refl[0], &refl[1], &leaf}) { r->vd.release(); r->vt.release(); r->tt.release(); }
+    for (auto& w : ws) { w.w.release(); w.z.release(); w.g.release(); w.part.release(); }
+    htau.release();
+  }
 };
 static QrCtx g_qr[64];
 
@@ -634,15 +640,17 @@ static int qr_panel(DevCtx& c, QrCtx& q, double* a, int64_t lda, int64_t m, int6
 
 // Blocked QR, depth 0 (dmf_mtb order) or 1 (dmf_la: TU_L(k) + PF(k+1) on the panel stream while
 // TU_R(k) runs on the trailing stream), asynchronous; the caller's stream `st` is joined at the end.
+// `sink` (optional, host-buffer calls): row block k is final once step k's updates (TU_R(k) and
+// TU_L(k)) are done -- later steps only touch rows >= (k+1) b -- and is handed to the sink then.
 static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
-                       double* d_tau, cudaStream_t st) {
+                       double* d_tau, cudaStream_t st, const RowSink* sink = nullptr) {
   QrCtx* qp = nullptr;
   CKR(qr_ctx(c, &qp));
   QrCtx& q = *qp;
   const int64_t steps = (n + b - 1) / b;
   cudaStream_t sP = c.sP, sU = c.sU;
-  CKR(ctx_events(c, 4));
-  cudaEvent_t e_in = c.ev[0], e_pf = c.ev[1], e_tu = c.ev[2], e_out = c.ev[3];
+  CKR(ctx_events(c, 5));
+  cudaEvent_t e_in = c.ev[0], e_pf = c.ev[1], e_tu = c.ev[2], e_out = c.ev[3], e_tl = c.ev[4];
   CK(cudaEventRecord(e_in, st));
   CK(cudaStreamWaitEvent(sP, e_in, 0));
   CK(cudaStreamWaitEvent(sU, e_in, 0));
@@ -656,6 +664,7 @@ static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
         CKR(qr_finish_t(c, q.ws[0], R, d_tau + col0, sP));
         CKR(qr_apply(c, q.ws[0], qr_view(R), a + col0 * lda + lo, lda, n - lo, sP));
       }
+      if (sink) CKR((*sink)(col0, col0 + bw, sP));
     }
     CK(cudaEventRecord(e_out, sP));
     CK(cudaStreamWaitEvent(st, e_out, 0));
@@ -678,6 +687,11 @@ static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     // TU_L(k) + PF(k+1) on the panel stream; TU_R(k-1) (recorded before e_tu is re-recorded
     // below) finished updating block k+1
     CKR(qr_apply(c, q.ws[0], qr_view(R), a + col0 * lda + lo, lda, bw_of(k + 1), sP));
+    if (sink) {  // row block k: final after TU_L(k) (panel stream) and TU_R(k) (trailing stream)
+      CK(cudaEventRecord(e_tl, sP));
+      CK(cudaStreamWaitEvent(sU, e_tl, 0));
+      CKR((*sink)(col0, col0 + bw, sU));
+    }
     CKR(qr_panel(c, q, a, lda, m, lo, lo, bw_of(k + 1), d_tau + lo, q.refl[(k + 1) & 1], sP));
     // the next TU_L / build (which rewrites refl[(k+1)&1] ... refl[k&1] at step k+2) must follow TU_R(k)
     if (lo2 < n) {
