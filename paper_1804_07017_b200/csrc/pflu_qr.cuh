@@ -28,6 +28,7 @@ constexpr int QR_LDT = 33;  // leaf tile row stride (doubles)
 constexpr int QR_MAXG = 256;
 
 static int g_qr_rows = []() { const char* e = getenv("PFLU_QR_ROWS"); return e ? atoi(e) : 512; }();
+static int g_qr_cluster = []() { const char* e = getenv("PFLU_QR_CLUSTER"); return e ? atoi(e) : 1; }();
 
 struct QrLeafArgs {
   double* a;
@@ -91,9 +92,18 @@ __device__ __forceinline__ double qr_sum_partials(const double* src, int G, int 
 // reflector needs no separate make-V / Gram / larft launches.
 // (An NCCL-LL style variant without the grid barrier -- flagged 16-byte partials polled by every
 // CTA -- measured slower: 0.264 vs 0.214 ms per 32768 x 32 leaf, polling contention on shared lines.)
+//
+// CL = true (panels of <= ~13500 rows): the CTAs form ONE thread-block cluster and the exchange goes
+// through distributed shared memory -- every CTA stores its partials straight into each peer's
+// shared memory and a cluster barrier (release/acquire) replaces the global grid barrier and the
+// L2 round trip of the reads.
+constexpr int QR_CL_MAX = 16;
+template <bool CL>
 __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
   extern __shared__ __align__(16) double qr_smem[];
   double* tile = qr_smem;  // R x QR_LDT
+  double* xs = qr_smem + p.R * QR_LDT;   // CL: [2][QR_CL_MAX][32] peers' partials
+  double* xd = xs + 2 * QR_CL_MAX * QR_LW;  // CL: [2][32] diagonal row
   __shared__ double sc[QR_LW];   // column sums, then s_c
   __shared__ double dr[QR_LW];   // diagonal row
   __shared__ double tl[QR_LW];   // tau of the leaf's columns
@@ -107,7 +117,8 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
     const int r = idx / w, c = idx - r * w;
     tile[r * QR_LDT + c] = p.a[(rbeg + r) * p.lda + p.c0 + c];
   }
-  __syncthreads();
+  if constexpr (CL) cl_sync();  // every peer is running before the first DSMEM store
+  else __syncthreads();
   for (int j = 0; j < w; ++j) {
     const int64_t d = p.r0 + j;
     const int par = j & 1;
@@ -120,12 +131,23 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
       double t = 0.0;
       for (int r = rfirst + lane; r < nrows; r += 32) t += tile[r * QR_LDT + j] * tile[r * QR_LDT + c];
       t = qr_warp_sum(t);
-      if (lane == 0) {
+      if constexpr (CL) {
+        if (lane < p.G) {
+          const uint32_t xa = smem_addr(xs + (par * QR_CL_MAX + q) * QR_LW + c);
+          asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(cl_map(xa, lane)), "d"(t) : "memory");
+          if (own_d) {
+            const uint32_t da = smem_addr(xd + par * QR_LW + c);
+            asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(cl_map(da, lane)), "d"(tile[dl * QR_LDT + c])
+                         : "memory");
+          }
+        }
+      } else if (lane == 0) {
         dots[(int64_t)q * QR_LW + c] = t;
         if (own_d) p.drow[par * 32 + c] = tile[dl * QR_LDT + c];
       }
     }
-    qr_grid_sync(p.bar, (unsigned)(j + 1) * (unsigned)p.G);
+    if constexpr (CL) cl_sync();
+    else qr_grid_sync(p.bar, (unsigned)(j + 1) * (unsigned)p.G);
     // (B) the same fixed-order sums on every CTA; all loads of a warp's columns in flight together
     {
       double acc[(QR_LW + NW - 1) / NW];
@@ -135,7 +157,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
 #pragma unroll
         for (int u = 0; u < (QR_LW + NW - 1) / NW; ++u) {
           const int c = j + warp + u * NW;
-          if (c < w) acc[u] += __ldcg(dots + (int64_t)i * QR_LW + c);
+          if (c < w) acc[u] += CL ? xs[(par * QR_CL_MAX + i) * QR_LW + c] : __ldcg(dots + (int64_t)i * QR_LW + c);
         }
       }
 #pragma unroll
@@ -144,7 +166,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
         const double t = qr_warp_sum(acc[u]);
         if (lane == 0 && c < w) {
           sc[c] = t;
-          dr[c] = __ldcg(p.drow + par * 32 + c);
+          dr[c] = CL ? xd[par * QR_LW + c] : __ldcg(p.drow + par * 32 + c);
         }
       }
     }
@@ -218,7 +240,8 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
       acc += tile[r * QR_LDT + x] * tile[r * QR_LDT + y];
     p.gram[(int64_t)q * QR_LW * QR_LW + x * QR_LW + y] = acc;
   }
-  qr_grid_sync(p.bar, (unsigned)(w + 1) * (unsigned)p.G);
+  if constexpr (CL) cl_sync();  // release/acquire at cluster scope covers the global partials
+  else qr_grid_sync(p.bar, (unsigned)(w + 1) * (unsigned)p.G);
   if (q != 0) return;
   // CTA 0: G = sum of the partials (fixed order), T by the column recurrence, T^T block out
   double* gs = qr_smem;                  // 32 x 33 (the tile is no longer needed)
@@ -463,8 +486,11 @@ static int qr_ctx(DevCtx& c, QrCtx** out) {
     CK(cudaMalloc(&q.bar, 64));
     CK(cudaFuncSetAttribute(qr_larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double) * ((QR_LARFT_MAXK - 32) * 32 + 32 * 33))));
-    CK(cudaFuncSetAttribute(qr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(qr_leaf_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)std::min<size_t>(c.smem_optin, 227 * 1024) - 1024));
+    CK(cudaFuncSetAttribute(qr_leaf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)std::min<size_t>(c.smem_optin, 227 * 1024) - 1024));
+    CK(cudaFuncSetAttribute(qr_leaf_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     q.ready = true;
   }
   *out = &q;
@@ -607,8 +633,21 @@ static int qr_panel(DevCtx& c, QrCtx& q, double* a, int64_t lda, int64_t m, int6
     const int lw = (int)std::min<int64_t>(QR_LW, w - p0);
     const int64_t r0 = d + p0, mp = m - r0;
     int R = (int)std::max<int64_t>(g_qr_rows > 0 ? g_qr_rows : 512, (mp + gcap - 1) / gcap);
-    const int G = (int)((mp + R - 1) / R);
+    int G = (int)((mp + R - 1) / R);
     R = (int)((mp + G - 1) / G);
+    // one thread-block cluster when the leaf fits 16 CTAs' shared memory
+    const int64_t clx = (int64_t)(2 * QR_CL_MAX * QR_LW + 2 * QR_LW) * 8;
+    bool cl = false;
+    if (g_qr_cluster) {
+      int Rc = (int)std::max<int64_t>(g_qr_rows > 0 ? g_qr_rows : 512, (mp + QR_CL_MAX - 1) / QR_CL_MAX);
+      const int Gc = (int)((mp + Rc - 1) / Rc);
+      Rc = (int)((mp + Gc - 1) / Gc);
+      if (Gc <= QR_CL_MAX && (int64_t)std::max(Rc, 2 * QR_LW) * QR_LDT * 8 + clx <= smax) {
+        cl = true;
+        R = Rc;
+        G = Gc;
+      }
+    }
     if ((int64_t)R * QR_LDT * 8 > smax) return set_err(PFLU_ERR_UNSUPPORTED, "QR panel of %lld rows too tall", (long long)mp);
     if (G > QR_MAXG || G > c.sms) return set_err(PFLU_ERR_UNSUPPORTED, "QR panel grid %d too large", G);
     QrLeafArgs la;
@@ -624,9 +663,26 @@ static int qr_panel(DevCtx& c, QrCtx& q, double* a, int64_t lda, int64_t m, int6
     la.tt = Rf.tt.p; la.ldt = Rf.ldt;
     la.p0 = (int)p0;
     void* args[] = {&la};
-    CK(cudaMemsetAsync(q.bar, 0, sizeof(unsigned), st));
-    const size_t smem = (size_t)std::max(R, 2 * QR_LW) * QR_LDT * 8;
-    CK(cudaLaunchCooperativeKernel((void*)qr_leaf_kernel, dim3(G), dim3(QR_THREADS), args, smem, st));
+    if (cl) {
+      const size_t smem = (size_t)std::max(R, 2 * QR_LW) * QR_LDT * 8 + (size_t)clx;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(QR_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelExC(&cfg, (const void*)qr_leaf_kernel<true>, args));
+    } else {
+      CK(cudaMemsetAsync(q.bar, 0, sizeof(unsigned), st));
+      const size_t smem = (size_t)std::max(R, 2 * QR_LW) * QR_LDT * 8;
+      CK(cudaLaunchCooperativeKernel((void*)qr_leaf_kernel<false>, dim3(G), dim3(QR_THREADS), args, smem, st));
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const int64_t rest = w - p0 - lw;
     if (rest > 0) {

@@ -211,3 +211,30 @@ def test_qr_deterministic_across_processes(cuda):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(path))
     assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_qr_cluster_and_grid_leaf_agree_bitwise(cuda):
+    """PFLU_QR_CLUSTER=0 forces the cooperative-grid leaf kernel (global barrier + L2 exchange); the
+    default uses one thread-block cluster (DSMEM exchange) for panels that fit.  With the same row
+    split (panels <= 8192 rows: 512 rows per CTA in both) the sums run in the same order, so the
+    factors must be bitwise identical."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "from paper_1804_07017_b200 import qr_factor\n"
+        "a = np.random.default_rng(6).uniform(-1, 1, (6000, 300))\n"
+        "f, t = qr_factor(a, b=96, lookahead=1)\n"
+        "np.save(sys.argv[1], np.concatenate([f.ravel(), t]))\n")
+    outs = []
+    for cl in ("0", "1"):
+        path = os.path.join("/tmp", f"qr_cl{cl}.npy")
+        env = dict(os.environ, PFLU_QR_CLUSTER=cl)
+        r = subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert outs[0].tobytes() == outs[1].tobytes()
