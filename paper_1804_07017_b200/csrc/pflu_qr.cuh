@@ -128,9 +128,14 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
     double* dots = p.dots + (int64_t)par * p.G * QR_LW;
     // (A) partial x^T a_c for c in [j, w) over this CTA's rows below the diagonal, one warp per column
     for (int c = j + warp; c < w; c += NW) {
-      double t = 0.0;
-      for (int r = rfirst + lane; r < nrows; r += 32) t += tile[r * QR_LDT + j] * tile[r * QR_LDT + c];
-      t = qr_warp_sum(t);
+      double t = 0.0, t1 = 0.0;
+      int r = rfirst + lane;
+      for (; r + 32 < nrows; r += 64) {
+        t += tile[r * QR_LDT + j] * tile[r * QR_LDT + c];
+        t1 += tile[(r + 32) * QR_LDT + j] * tile[(r + 32) * QR_LDT + c];
+      }
+      if (r < nrows) t += tile[r * QR_LDT + j] * tile[r * QR_LDT + c];
+      t = qr_warp_sum(t + t1);
       if constexpr (CL) {
         if (lane < p.G) {
           const uint32_t xa = smem_addr(xs + (par * QR_CL_MAX + q) * QR_LW + c);
@@ -153,12 +158,28 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
       double acc[(QR_LW + NW - 1) / NW];
 #pragma unroll
       for (int u = 0; u < (QR_LW + NW - 1) / NW; ++u) acc[u] = 0.0;
-      for (int i = lane; i < p.G; i += 32) {
+      if constexpr (CL) {
+        if (lane < p.G) {
 #pragma unroll
-        for (int u = 0; u < (QR_LW + NW - 1) / NW; ++u) {
-          const int c = j + warp + u * NW;
-          if (c < w) acc[u] += CL ? xs[(par * QR_CL_MAX + i) * QR_LW + c] : __ldcg(dots + (int64_t)i * QR_LW + c);
+          for (int u = 0; u < (QR_LW + NW - 1) / NW; ++u) {
+            const int c = j + warp + u * NW;
+            if (c < w) acc[u] = xs[(par * QR_CL_MAX + lane) * QR_LW + c];
+          }
         }
+      } else {
+        // every load of the warp's columns issued before the first add (G <= QR_MAXG)
+        double v[QR_MAXG / 32][(QR_LW + NW - 1) / NW];
+#pragma unroll
+        for (int t = 0; t < QR_MAXG / 32; ++t)
+#pragma unroll
+          for (int u = 0; u < (QR_LW + NW - 1) / NW; ++u) {
+            const int i = lane + 32 * t, c = j + warp + u * NW;
+            v[t][u] = (i < p.G && c < w) ? __ldcg(dots + (int64_t)i * QR_LW + c) : 0.0;
+          }
+#pragma unroll
+        for (int t = 0; t < QR_MAXG / 32; ++t)
+#pragma unroll
+          for (int u = 0; u < (QR_LW + NW - 1) / NW; ++u) acc[u] += v[t][u];
       }
 #pragma unroll
       for (int u = 0; u < (QR_LW + NW - 1) / NW; ++u) {
@@ -233,12 +254,18 @@ __global__ void __launch_bounds__(QR_THREADS, 1) qr_leaf_kernel(QrLeafArgs p) {
   for (int e = tid; e < w * w; e += QR_THREADS) {
     const int x = e / w, y = e - x * w;
     if (x >= y) continue;
-    double acc = 0.0;
+    double acc = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // four chains: latency, not throughput, bound
     const int rs = (int)min((int64_t)nrows, max((int64_t)0, y - rho0));
     if (rs < nrows && rho0 + rs == y) acc = tile[rs * QR_LDT + x];
-    for (int r = (rho0 + rs == y && rs < nrows) ? rs + 1 : rs; r < nrows; ++r)
+    int r = (rho0 + rs == y && rs < nrows) ? rs + 1 : rs;
+    for (; r + 3 < nrows; r += 4) {
       acc += tile[r * QR_LDT + x] * tile[r * QR_LDT + y];
-    p.gram[(int64_t)q * QR_LW * QR_LW + x * QR_LW + y] = acc;
+      a1 += tile[(r + 1) * QR_LDT + x] * tile[(r + 1) * QR_LDT + y];
+      a2 += tile[(r + 2) * QR_LDT + x] * tile[(r + 2) * QR_LDT + y];
+      a3 += tile[(r + 3) * QR_LDT + x] * tile[(r + 3) * QR_LDT + y];
+    }
+    for (; r < nrows; ++r) acc += tile[r * QR_LDT + x] * tile[r * QR_LDT + y];
+    p.gram[(int64_t)q * QR_LW * QR_LW + x * QR_LW + y] = (acc + a1) + (a2 + a3);
   }
   if constexpr (CL) cl_sync();  // release/acquire at cluster scope covers the global partials
   else qr_grid_sync(p.bar, (unsigned)(w + 1) * (unsigned)p.G);
