@@ -1,4 +1,4 @@
-"""Benchmark CLI mirroring the reference's ``python -m panelforge.bench`` for Kind.LU
+"""Benchmark CLI mirroring the reference's ``python -m panelforge.bench`` for Kind.LU and Kind.QR
 (pkg/src/panelforge/bench.py): sweep n, time each strategy, emit the same CSV schema.
 
     python -m paper_1804_07017_b200.cli --kind lu --strategy la --n-min 2048 --n-max 8192 --check
@@ -8,7 +8,8 @@
 * Timing covers only the library call (the matrix is already on the device; generation, copies and
   checking are excluded), best of ``--reps`` after one warm-up (bench.py:120-145); CUDA events.
 * ``--check`` reports ||PA - LU||_F / (n u ||A||_F) (oracle.py:78-89) computed on the GPU in row
-  blocks, so it also works at C5 sizes (n = 65536) where the host residual needs ~240 GB.
+  blocks, so it also works at C5 sizes (n = 65536) where the host residual needs ~240 GB; for QR
+  ||A - QR||_F / (n u ||A||_F) (oracle.py:113-127, Q formed on the GPU by torch as the checker).
 * CSV: ``kind,strategy,n,b,threads,seconds,gflops,residual`` (bench.py:32, 219-234); the
   ``threads`` column carries the GPU count.
 * Strategies: mtb (look-ahead 0), la (look-ahead 1), la-mb (look-ahead 1: the hardware block scheduler
@@ -100,22 +101,64 @@ def time_factor(a_host: np.ndarray, b: int, lookahead: int, reps: int, check: bo
     return best, residual
 
 
+def qr_residual_gpu(a0, f, tau) -> float:
+    """||A - Q R||_F / (n u ||A||_F) on the GPU, Q = H_1 ... H_n formed by torch (checker only)."""
+    import torch
+
+    m, n = a0.shape
+    v = torch.tril(f, -1) + torch.eye(m, n, device=f.device, dtype=f.dtype)
+    q = torch.linalg.householder_product(v, tau)
+    norm_a = float(torch.linalg.norm(a0))
+    err = float(torch.linalg.norm(a0 - q @ torch.triu(f[:n])))
+    return err if norm_a == 0.0 else err / (max(n, 1) * UNIT_ROUNDOFF * norm_a)
+
+
+def time_factor_qr(a_host: np.ndarray, b: int, lookahead: int, reps: int, check: bool):
+    import torch
+
+    from .api import geqrf_device
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pristine = torch.from_numpy(np.ascontiguousarray(a_host)).to(dev)
+    work = torch.empty_like(pristine)
+    tau = torch.zeros(pristine.shape[1], dtype=torch.float64, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def once():
+        work.copy_(pristine)
+        torch.cuda.synchronize()
+        e0.record()
+        geqrf_device(work, b, lookahead, tau=tau)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e-3
+
+    once()
+    best = min(once() for _ in range(max(1, reps)))
+    residual = qr_residual_gpu(pristine, work, tau) if check else None
+    return best, residual
+
+
 def run_sweep(kind: str, strategies, sizes, b: int, reps: int, seed: int, check: bool):
     import torch
 
     from .api import Kind, flops
 
-    if kind != "lu":
-        raise ValueError(f"--kind {kind}: only lu is implemented on the B200 (QR/GEMM studies are out of scope)")
+    if kind not in ("lu", "qr"):
+        raise ValueError(f"--kind {kind}: only lu and qr are implemented on the B200 (GEMM studies are out of scope)")
     gpus = 1 if torch.cuda.is_available() else 0
     records = []
     for n in sizes:
         a = make_instance(seed, kind, n)
         for s in strategies:
             label, la = _STRATEGIES[s]
-            seconds, residual = time_factor(a, b, la, reps, check)
-            fl = flops(Kind.LU, n)
-            records.append(BenchRecord("LU", label, n, b, gpus, seconds, fl / seconds / 1e9, residual))
+            if kind == "qr":
+                seconds, residual = time_factor_qr(a, b, la, reps, check)
+                fl = flops(Kind.QR, n)
+            else:
+                seconds, residual = time_factor(a, b, la, reps, check)
+                fl = flops(Kind.LU, n)
+            records.append(BenchRecord(kind.upper(), label, n, b, gpus, seconds, fl / seconds / 1e9, residual))
     return records
 
 

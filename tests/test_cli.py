@@ -40,4 +40,4 @@ def test_parser_and_scope():
     with pytest.raises(SystemExit):
         cli.build_parser().parse_args(["--strategy", "rtm"])
     with pytest.raises(ValueError):
-        cli.run_sweep("qr", ["la"], [64], 16, 1, 0, False)
+        cli.run_sweep("gemm", ["la"], [64], 16, 1, 0, False)

@@ -238,3 +238,18 @@ def test_qr_cluster_and_grid_leaf_agree_bitwise(cuda):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(path))
     assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_cli_qr_sweep_csv(cuda):
+    """The reference-style bench CLI (python -m panelforge.bench --kind qr) on the B200: same CSV schema,
+    backward error checked on the GPU."""
+    import io
+
+    from paper_1804_07017_b200 import cli
+
+    recs = cli.run_sweep("qr", ["mtb", "la"], [256, 512], 64, 1, 0, True)
+    assert [r.kind for r in recs] == ["QR"] * 4
+    assert all(r.gflops > 0 and r.residual is not None and r.residual <= 10 for r in recs)
+    buf = io.StringIO()
+    cli.emit_csv(recs, buf)
+    assert cli.parse_csv(buf.getvalue()) == recs
