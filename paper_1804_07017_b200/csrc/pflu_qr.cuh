@@ -461,6 +461,9 @@ struct QrBuf {
   size_t cap = 0;  // doubles
   int need(size_t n) {
     if (n <= cap) return PFLU_OK;
+    // growing frees the old buffer: queued kernels may still use it (geqrf_async reserves every
+    // buffer at its maximum before its first launch, so this only happens between calls)
+    if (p) CK(cudaDeviceSynchronize());
     if (p) CK(cudaFree(p));
     p = nullptr;
     cap = 0;
@@ -731,6 +734,20 @@ static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   CKR(qr_ctx(c, &qp));
   QrCtx& q = *qp;
   const int64_t steps = (n + b - 1) / b;
+  {  // every workspace at its maximum size before the first launch (see QrBuf::need)
+    const int64_t bb = std::min(b, n);
+    for (QrRefl* R : {&q.refl[0], &q.refl[1]}) {
+      CKR(R->vd.need((size_t)(m * qr_even(bb))));
+      CKR(R->vt.need((size_t)(bb * qr_even(m))));
+      CKR(R->tt.need((size_t)(bb * qr_even(bb))));
+    }
+    for (auto& w : q.ws) {
+      CKR(w.w.need((size_t)(bb * qr_even(n))));
+      CKR(w.z.need((size_t)(bb * qr_even(n))));
+      CKR(w.g.need((size_t)(bb * qr_even(bb))));
+      CKR(w.part.need((size_t)4 * c.sms * 128 * 65));  // split-K slices: S * M * ldp <= 4 sms * 128 * 65
+    }
+  }
   cudaStream_t sP = c.sP, sU = c.sU;
   CKR(ctx_events(c, 5));
   cudaEvent_t e_in = c.ev[0], e_pf = c.ev[1], e_tu = c.ev[2], e_out = c.ev[3], e_tl = c.ev[4];

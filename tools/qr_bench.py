@@ -12,7 +12,11 @@ from paper_1804_07017_b200 import qr_factor  # noqa: E402
 
 
 def run(n, b, la, reps=2):
-    a0 = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, (n, n))).cuda()
+    if n > 32768:  # generated on the device (the host generator takes minutes at this size)
+        g = torch.Generator(device="cuda").manual_seed(4)
+        a0 = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    else:
+        a0 = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, (n, n))).cuda()
     w = a0.clone()
     qr_factor(w, b=b, lookahead=la)  # warm-up (workspaces)
     best = 1e30
