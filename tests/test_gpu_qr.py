@@ -216,7 +216,7 @@ def test_qr_deterministic_across_processes(cuda):
 def test_qr_cluster_and_grid_leaf_agree_bitwise(cuda):
     """PFLU_QR_CLUSTER=0 forces the cooperative-grid leaf kernel (global barrier + L2 exchange); the
     default uses one thread-block cluster (DSMEM exchange) for panels that fit.  With the same row
-    split (panels <= 8192 rows: 512 rows per CTA in both) the sums run in the same order, so the
+    split (panels <= 4096 rows: 256 rows per CTA in both) the sums run in the same order, so the
     factors must be bitwise identical."""
     import subprocess
     import sys
@@ -226,7 +226,7 @@ def test_qr_cluster_and_grid_leaf_agree_bitwise(cuda):
         "import numpy as np, sys\n"
         "sys.path.insert(0, '.')\n"
         "from paper_1804_07017_b200 import qr_factor\n"
-        "a = np.random.default_rng(6).uniform(-1, 1, (6000, 300))\n"
+        "a = np.random.default_rng(6).uniform(-1, 1, (4000, 300))\n"
         "f, t = qr_factor(a, b=96, lookahead=1)\n"
         "np.save(sys.argv[1], np.concatenate([f.ravel(), t]))\n")
     outs = []
