@@ -162,7 +162,10 @@ def test_larft_and_block_reflector(cuda):
 
 
 @pytest.mark.parametrize("m,n,b,lookahead", [(2048, 2048, 128, 1), (2048, 2048, 128, 0), (3000, 1000, 256, 1),
-                                             (1100, 1000, 100, 1), (777, 513, 64, 0)])
+                                             (1100, 1000, 100, 1), (777, 513, 64, 0),
+                                             # edge shapes: one column, b = 1, b > n, 1 x 1, odd b
+                                             (5, 1, 4, 1), (20, 20, 1, 1), (33, 33, 64, 0), (1, 1, 1, 1),
+                                             (100, 37, 7, 1), (64, 64, 64, 1)])
 def test_qr_matches_oracle_medium(cuda, m, n, b, lookahead):
     from paper_1804_07017_b200 import qr_factor
 
