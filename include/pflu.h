@@ -172,7 +172,8 @@ int pflu_geqrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b,
 
 /* Householder factorization of the panel rows [d, m) x columns [col, col + w) (the diagonal of
  * panel column j is row d + j; w <= m - d), in place; d_tau[0 .. w) receives the scalars.
- * Asynchronous on `stream`. */
+ * Asynchronous on `stream`; one panel at a time per device (the leaf kernels' exchange buffers are
+ * per device). */
 int pflu_qr_panel(double* d_a, int64_t lda, int64_t m, int64_t d, int64_t col, int64_t w, double* d_tau,
                   void* stream);
 
@@ -182,7 +183,8 @@ int pflu_larft(const double* d_v, int64_t ldv, int64_t mp, int64_t k, const doub
                int64_t ldt, void* stream);
 
 /* C (mp x nc, ld ldc, device) := (H_1 ... H_k)^T C = C - V (T^T (V^T C)) for the reflectors stored in
- * the mp x k panel d_v with scalars d_tau.  Asynchronous on `stream`. */
+ * the mp x k panel d_v with scalars d_tau.  Asynchronous on `stream`; workspaces are per stream, so
+ * calls on different streams may run concurrently (the multi-GPU driver's TU_L / TU_R). */
 int pflu_apply_block_reflector(const double* d_v, int64_t ldv, int64_t mp, int64_t k, const double* d_tau,
                                double* d_c, int64_t ldc, int64_t nc, void* stream);
 

@@ -275,18 +275,24 @@ def geqrf_device(a, b: int, lookahead: int, tau=None):
     return tau
 
 
-def qr_factor(a, b: int = 256, lookahead: int = 1, overwrite_a: bool = True):
+def qr_factor(a, b: int = 256, lookahead: int = 1, overwrite_a: bool = True, n_gpus: int = 1):
     """Blocked Householder QR on the B200 (the reference's Kind.QR of dmf_la / dmf_mtb).
 
     ``a``: float64 m x n (m >= n) row-major -- a numpy array (host buffers, pflu_geqrf) or a CUDA
     torch tensor (device buffers, current stream).  Returns ``(f, tau)``: R on and above the
     diagonal of ``f``, the Householder vectors' tails below it (unit heads implicit), and the
-    reflector scalars (H_j = I - tau_j v_j v_j^T, Q = H_1 ... H_n).
+    reflector scalars (H_j = I - tau_j v_j v_j^T, Q = H_1 ... H_n).  ``n_gpus > 1`` runs the 1-D
+    block-cyclic multi-GPU driver (dist.geqrf_block_cyclic; an initialised torch.distributed group
+    with one rank per GPU); every rank gets the full factors.
     """
     if lookahead not in (0, 1):
         raise ValueError("lookahead must be 0 or 1 (the reference defines depth 0 and 1)")
     if b < 1:
         raise ValueError("block size must be >= 1")
+    if n_gpus > 1:
+        from .dist import qr_factor_dist
+
+        return qr_factor_dist(a, b=b, lookahead=lookahead)
     if _is_torch(a):
         import torch
 

@@ -1456,15 +1456,16 @@ int pflu_larft(const double* d_v, int64_t ldv, int64_t mp, int64_t k, const doub
   QrCtx* q = nullptr;
   CKR(qr_ctx(*c, &q));
   cudaStream_t st = (cudaStream_t)stream;
+  QrSlot& sl = q->slot(st);
   // the panel view: rows [0, mp) of columns [0, k) at d_v
-  CKR(qr_build(*c, q->ws[0], q->leaf, d_v, ldv, 0, mp, 0, (int)k, d_tau, st));
+  CKR(qr_build(*c, sl.ws, sl.refl, d_v, ldv, 0, mp, 0, (int)k, d_tau, st));
   // T = (T^T)^T into the caller's upper-triangular layout
-  std::vector<double> tt((size_t)(k * q->leaf.ldt)), t((size_t)(k * ldt), 0.0);
-  CK(cudaMemcpyAsync(tt.data(), q->leaf.tt.p, sizeof(double) * tt.size(), cudaMemcpyDeviceToHost, st));
+  std::vector<double> tt((size_t)(k * sl.refl.ldt)), t((size_t)(k * ldt), 0.0);
+  CK(cudaMemcpyAsync(tt.data(), sl.refl.tt.p, sizeof(double) * tt.size(), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(t.data(), d_t, sizeof(double) * t.size(), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int64_t i = 0; i < k; ++i)
-    for (int64_t j = 0; j < k; ++j) t[(size_t)(i * ldt + j)] = j >= i ? tt[(size_t)(j * q->leaf.ldt + i)] : 0.0;
+    for (int64_t j = 0; j < k; ++j) t[(size_t)(i * ldt + j)] = j >= i ? tt[(size_t)(j * sl.refl.ldt + i)] : 0.0;
   CK(cudaMemcpyAsync(d_t, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
   return PFLU_OK;
@@ -1486,8 +1487,9 @@ int pflu_apply_block_reflector(const double* d_v, int64_t ldv, int64_t mp, int64
   QrCtx* q = nullptr;
   CKR(qr_ctx(*c, &q));
   cudaStream_t st = (cudaStream_t)stream;
-  CKR(qr_build(*c, q->ws[0], q->leaf, d_v, ldv, 0, mp, 0, (int)k, d_tau, st));
-  CKR(qr_apply(*c, q->ws[0], qr_view(q->leaf), d_c, ldc, nc, st));
+  QrSlot& sl = q->slot(st);
+  CKR(qr_build(*c, sl.ws, sl.refl, d_v, ldv, 0, mp, 0, (int)k, d_tau, st));
+  CKR(qr_apply(*c, sl.ws, qr_view(sl.refl), d_c, ldc, nc, st));
   return PFLU_OK;
 }
 

@@ -491,9 +491,18 @@ struct QrScratch {
   QrBuf w, z, g, part;
 };
 
+// Workspace of the kernel-level entry points on one stream (the multi-GPU driver applies block
+// reflectors on two streams at once).
+struct QrSlot {
+  cudaStream_t st = nullptr;
+  QrRefl refl;
+  QrScratch ws;
+};
+
 struct QrCtx {
   QrRefl refl[2];     // outer step reflectors, by step parity
-  QrRefl leaf;        // kernel-level entry points (pflu_qr_panel / pflu_larft / pflu_apply_block_reflector)
+  QrRefl leaf;        // pflu_qr_panel's reflector block
+  std::vector<QrSlot*> slots;  // pflu_larft / pflu_apply_block_reflector, one per stream
   QrScratch ws[2];    // 0: panel stream (leaves, TU_L), 1: trailing stream (TU_R)
   QrBuf htau;         // pflu_geqrf: device tau (grow-only)
   double* leafx = nullptr;  // leaf kernel exchange: dots, drow, partial Gram matrices
@@ -503,6 +512,19 @@ struct QrCtx {
     for (QrRefl* r : {&refl[0], &refl[1], &leaf}) { r->vd.release(); r->vt.release(); r->tt.release(); }
     for (auto& w : ws) { w.w.release(); w.z.release(); w.g.release(); w.part.release(); }
     htau.release();
+    for (QrSlot* sl : slots) {
+      sl->refl.vd.release(); sl->refl.vt.release(); sl->refl.tt.release();
+      sl->ws.w.release(); sl->ws.z.release(); sl->ws.g.release(); sl->ws.part.release();
+      delete sl;
+    }
+    slots.clear();
+  }
+  QrSlot& slot(cudaStream_t st) {
+    for (QrSlot* sl : slots)
+      if (sl->st == st) return *sl;
+    slots.push_back(new QrSlot());
+    slots.back()->st = st;
+    return *slots.back();
   }
 };
 static QrCtx g_qr[64];

@@ -187,6 +187,20 @@ class CudaKernels:
                                      b.stride(0), m, n, k, int(self.exact), self._st())
         _lib.check(rc, "pflu_gemm_update")
 
+    # Householder QR (Kind.QR)
+    def qr_panel(self, a, m: int, d: int, col: int, w: int, tau):
+        rc = self.L.pflu_qr_panel(a.data_ptr(), a.stride(0), m, d, col, w, tau.data_ptr(), self._st())
+        _lib.check(rc, "pflu_qr_panel")
+
+    def qr_apply(self, v, tau, c):
+        mp, k = v.shape
+        nc = c.shape[1]
+        if nc == 0 or mp == 0:
+            return
+        rc = self.L.pflu_apply_block_reflector(v.data_ptr(), v.stride(0), mp, k, tau.data_ptr(), c.data_ptr(),
+                                               c.stride(0), nc, self._st())
+        _lib.check(rc, "pflu_apply_block_reflector")
+
 
 # ---------------------------------------------------------------------------------------------
 # the distributed driver
@@ -325,6 +339,115 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
         info = int(t.item())
         info = 0 if info >= 2 ** 62 else info
     return piv, info
+
+
+def geqrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, kernels=None, group=None,
+                       tau: torch.Tensor | None = None):
+    """Householder QR (Kind.QR) of the block-cyclic distributed n x n matrix, in place.
+
+    Same distribution and schedule as getrf_block_cyclic: the owner of block k factors it
+    (pflu_qr_panel) and broadcasts ONE message -- the (n - kb) x bw panel (R on top, the reflectors
+    below) followed by its bw tau -- and every rank applies the block reflector to its local
+    trailing columns (pflu_apply_block_reflector, which forms V and T from the message).  Look-ahead
+    1: the owner of block k+1 updates it first, factors it and broadcasts it while every rank runs
+    the rest of step k's update.  Returns tau (the full n-vector, identical on every rank)."""
+    P = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    if kernels is None:
+        kernels = CudaKernels(a_loc.device)
+    dev = a_loc.device
+    if a_loc.shape[0] != n or a_loc.shape[1] != local_cols(n, b, P, r) or a_loc.stride(1) != 1:
+        raise ValueError("a_loc must be the row-major local block-cyclic columns (n x local_cols)")
+    nblk = num_blocks(n, b)
+    if tau is None:
+        tau = torch.zeros(n, dtype=torch.float64, device=dev)
+    pbuf = [torch.empty(n * b + b, dtype=torch.float64, device=dev) for _ in range(2)]
+    ev_bc = [kernels.event() for _ in range(2)]
+    ev_tu = [kernels.event() for _ in range(2)]
+    kernels.begin()
+
+    def cols_before(k):
+        return local_cols_before(k, n, b, P, r)
+
+    def pf_pack_bcast(k):
+        col0 = k * b
+        bw = min(b, n - col0)
+        rows = n - col0
+        o = k % P
+        msg = pbuf[k % 2][: rows * bw + bw]
+        buf = msg[: rows * bw].view(rows, bw)
+        tv = msg[rows * bw:]
+        if r == o:
+            lc = local_col_of_block(k, b, P)
+            kernels.qr_panel(a_loc, n, col0, lc, bw, tau[col0: col0 + bw])
+            buf.copy_(a_loc[col0:, lc: lc + bw])
+            tv.copy_(tau[col0: col0 + bw])
+        if P > 1:
+            dist.broadcast(msg, src=o, group=group)  # one message per step: panel + tau
+            if r != o:
+                tau[col0: col0 + bw].copy_(tv)
+        return buf, tv
+
+    def update(k, bt, c0, c1):
+        if c1 <= c0:
+            return
+        buf, tv = bt
+        kernels.qr_apply(buf, tv, a_loc[k * b:, c0:c1])
+
+    ncl = a_loc.shape[1]
+    if lookahead == 0:
+        for k in range(nblk):
+            with kernels.stream("P"):
+                bt = pf_pack_bcast(k)
+                update(k, bt, cols_before(k + 1), ncl)
+    else:
+        bufs = {}
+        with kernels.stream("P"):
+            bufs[0] = pf_pack_bcast(0)
+            kernels.record(ev_bc[0], "P")
+        for k in range(nblk):
+            nxt = k + 1 < nblk
+            own_next = nxt and (k + 1) % P == r
+            lo_r = cols_before(k + 2) if own_next else cols_before(k + 1)
+            with kernels.stream("U"):
+                kernels.wait(ev_bc[k % 2], "U")
+                update(k, bufs[k], lo_r, ncl)
+                kernels.record(ev_tu[k % 2], "U")
+            if nxt:
+                with kernels.stream("P"):
+                    if k > 0:
+                        kernels.wait(ev_tu[(k - 1) % 2], "P")
+                    if own_next:
+                        update(k, bufs[k], cols_before(k + 1), cols_before(k + 2))
+                    bufs[k + 1] = pf_pack_bcast(k + 1)
+                    kernels.record(ev_bc[(k + 1) % 2], "P")
+            bufs.pop(k - 1, None)
+    if kernels.is_cuda:
+        kernels.join()
+    return tau
+
+
+def qr_factor_dist(a, b: int = 256, lookahead: int = 1):
+    """``qr_factor(..., n_gpus=P)``: every rank passes the same full n x n matrix; each factors its
+    block-cyclic columns on its GPU; every rank gets the full factors (all-gather) and tau."""
+    import numpy as np
+
+    if not dist.is_initialized():
+        raise RuntimeError("n_gpus > 1 needs an initialised torch.distributed process group (one rank per GPU)")
+    P, r = dist.get_world_size(), dist.get_rank()
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", r % max(1, torch.cuda.device_count()))))
+    torch.cuda.set_device(dev)
+    full = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+    if full.dim() != 2 or full.shape[0] != full.shape[1] or full.dtype != torch.float64 or full.stride(1) != 1:
+        raise ValueError("the multi-GPU path factors square row-major float64 matrices")
+    n = full.shape[1]
+    a_loc = torch.empty((n, local_cols(n, b, P, r)), dtype=torch.float64, device=dev)
+    copy_local_columns(a_loc, full, n, b, P, r, to_device=True)
+    tau = geqrf_block_cyclic(a_loc, n, b, lookahead, CudaKernels(dev))
+    f = allgather_columns(a_loc, n, b)
+    if not isinstance(a, torch.Tensor):
+        return f.cpu().numpy(), tau.cpu().numpy()
+    return (f if full.is_cuda else f.cpu()), (tau if full.is_cuda else tau.cpu())
 
 
 def copy_local_columns(dst, src, n: int, b: int, P: int, r: int, to_device: bool, stream=None):

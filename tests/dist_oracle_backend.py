@@ -84,3 +84,21 @@ class OracleKernels:
         k = a.shape[1]
         if m and n and k:
             self.L.orc_gemm_sub(_dp(c), c.stride(0), _dp(a), a.stride(0), _dp(b), b.stride(0), m, n, k)
+
+    # Householder QR: the oracle's qr_unb / larft / block reflector on the same views
+    def qr_panel(self, a, m, d, col, w, tau):
+        ld = a.stride(0)
+        tmp = torch.zeros(w, dtype=torch.float64)
+        self.L.orc_qr_unb(_dp(a, d * ld + col), m - d, w, ld, _dp(tmp))
+        tau.copy_(tmp)
+
+    def qr_apply(self, v, tau, c):
+        mp, k = v.shape
+        nc = c.shape[1]
+        if nc == 0 or mp == 0:
+            return
+        vv = v.contiguous()
+        tt = tau.contiguous()
+        t = torch.zeros((k, k), dtype=torch.float64)
+        self.L.orc_larft(_dp(vv), mp, k, vv.stride(0), _dp(tt), _dp(t))
+        self.L.orc_apply_block_reflector(_dp(vv), mp, k, vv.stride(0), _dp(t), _dp(c), nc, c.stride(0))

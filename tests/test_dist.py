@@ -109,3 +109,36 @@ def test_local_columns_seeded_match_full_matrix(dist_name, seed):
         for r in range(P):
             loc = pd.local_columns_seeded(n, b, P, r, seed, dist_name, chunk_rows=100)
             assert loc.tobytes() == pd.scatter_columns(torch.from_numpy(full), b, P, r).numpy().tobytes()
+
+
+def _qr_worker(rank, world, port, n, b, lookahead, seed, out_dir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from dist_oracle_backend import OracleKernels
+    from paper_1804_07017_b200 import dist as pd
+
+    a = np.random.default_rng(seed).uniform(-1.0, 1.0, (n, n))
+    loc = pd.scatter_columns(torch.from_numpy(a), b, world, rank)
+    tau = pd.geqrf_block_cyclic(loc, n, b, lookahead, OracleKernels())
+    f = pd.allgather_columns(loc, n, b)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "f.npy"), f.numpy())
+        np.save(os.path.join(out_dir, "tau.npy"), tau.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,b,lookahead", [(2, 96, 16, 1), (2, 100, 16, 0), (3, 101, 8, 1), (4, 150, 16, 1)])
+def test_qr_block_cyclic_matches_oracle_bitwise(tmp_path, world, n, b, lookahead):
+    """The distributed Householder QR (same schedule, oracle kernels) is bitwise the single-process
+    oracle: every column's operation sequence is independent of the column distribution."""
+    import oracle
+
+    mp.spawn(_qr_worker, args=(world, _free_port(), n, b, lookahead, 7, str(tmp_path)), nprocs=world, join=True)
+    f, tau = np.load(tmp_path / "f.npy"), np.load(tmp_path / "tau.npy")
+    a = np.random.default_rng(7).uniform(-1.0, 1.0, (n, n))
+    rf, rtau = oracle.geqrf(a, b)
+    assert f.tobytes() == rf.tobytes() and tau.tobytes() == rtau.tobytes()

@@ -145,3 +145,39 @@ def test_lu_factor_local_api(cuda, tmp_path):
         assert np.array_equal(np.load(tmp_path / f"piv{r}.npy"), rpiv)
         want = pd.scatter_columns(torch.from_numpy(ref), b, world, r).numpy()
         assert np.load(tmp_path / f"loc{r}.npy").tobytes() == want.tobytes()
+
+
+def _qr_worker(rank, world, port, backend, n, b, lookahead, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+    from paper_1804_07017_b200 import dist as pd
+
+    dev = torch.device("cuda:0")
+    a = np.random.default_rng(5).uniform(-1.0, 1.0, (n, n))
+    loc = pd.scatter_columns(torch.from_numpy(a), b, world, rank).to(dev)
+    tau = pd.geqrf_block_cyclic(loc, n, b, lookahead, pd.CudaKernels(dev))
+    f = pd.allgather_columns(loc, n, b)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "f.npy"), f.cpu().numpy())
+        np.save(os.path.join(out_dir, "tau.npy"), tau.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,backend", [(1, "nccl"), (2, "gloo")])
+@pytest.mark.parametrize("n,b,lookahead", [(700, 64, 1), (513, 128, 0), (2048, 256, 1)])
+def test_dist_cuda_qr(cuda, tmp_path, world, backend, n, b, lookahead):
+    """Block-cyclic Householder QR with the CUDA kernels: factors and tau within 1e-10 of the oracle,
+    backward error / orthogonality <= 10."""
+    mp.spawn(_qr_worker, args=(world, _free_port(), backend, n, b, lookahead, str(tmp_path)), nprocs=world,
+             join=True)
+    f, tau = np.load(tmp_path / "f.npy"), np.load(tmp_path / "tau.npy")
+    a = np.random.default_rng(5).uniform(-1.0, 1.0, (n, n))
+    rf, rtau = oracle.geqrf(a, b)
+    assert np.abs(f - rf).max() / np.abs(a).max() <= 1e-10
+    assert np.abs(tau - rtau).max() <= 1e-10
+    back, orth = oracle.qr_residual(a, f, tau)
+    assert back <= 10 and orth <= 10
