@@ -425,6 +425,46 @@ qr_larft_kernel(const double* __restrict__ gneg, int64_t ldg, const double* __re
   }
 }
 
+// One block column J of T when the diagonal blocks are given (the factorization path): one launch
+// per J, CTA b owns rows 8b .. 8b + 7 of T[0:J0, J]; every CTA forms the whole X = G[0:J0, J] T_JJ in
+// shared memory (cheap) so the CTAs need no exchange.  Also zeroes tt's upper entries in block J.
+constexpr int QR_MERGE_ROWS = 8;
+__global__ void __launch_bounds__(QR_MERGE_ROWS * 32)
+qr_larft_merge_kernel(const double* __restrict__ gneg, int64_t ldg, int k, int J0, double* tt, int64_t ldt) {
+  extern __shared__ double qr_mx[];  // X: J0 x 32, then T_JJ: 32 x 33
+  double* tjj = qr_mx + (size_t)J0 * 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bs = min(32, k - J0);
+  for (int e = tid; e < 32 * 32; e += QR_MERGE_ROWS * 32) {
+    const int l = e >> 5, c = e & 31;  // T_JJ[l][c] = tt[J0 + c][J0 + l]
+    tjj[l * 33 + c] = (l < bs && c < bs) ? tt[(int64_t)(J0 + c) * ldt + J0 + l] : 0.0;
+  }
+  __syncthreads();
+  for (int r = warp; r < J0; r += QR_MERGE_ROWS) {
+    const double g = lane < bs ? -gneg[(int64_t)r * ldg + J0 + lane] : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const double gl = __shfl_sync(0xffffffffu, g, l);
+      if (l <= lane) acc += gl * tjj[l * 33 + lane];
+    }
+    qr_mx[r * 32 + lane] = acc;
+  }
+  __syncthreads();
+  const int r = blockIdx.x * QR_MERGE_ROWS + warp;
+  if (r >= J0) return;
+  double acc = 0.0;
+  for (int l0 = r; l0 < J0; l0 += 32) {
+    const double tv = l0 + lane < J0 ? tt[(int64_t)(l0 + lane) * ldt + r] : 0.0;
+    const int cnt = min(32, J0 - l0);
+    for (int i = 0; i < cnt; ++i) acc += __shfl_sync(0xffffffffu, tv, i) * qr_mx[(l0 + i) * 32 + lane];
+  }
+  if (lane < bs) {
+    tt[(int64_t)(J0 + lane) * ldt + r] = -acc;
+    tt[(int64_t)r * ldt + J0 + lane] = 0.0;
+  }
+}
+
 // Column recurrence in one CTA (any k <= 1024; used above QR_LARFT_MAXK).
 __global__ void qr_larft_seq_kernel(const double* __restrict__ gneg, int64_t ldg, const double* __restrict__ tau,
                                     int k, double* tt, int64_t ldt) {
@@ -536,6 +576,8 @@ static int qr_ctx(DevCtx& c, QrCtx** out) {
     CK(cudaMalloc(&q.bar, 64));
     CK(cudaFuncSetAttribute(qr_larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double) * ((QR_LARFT_MAXK - 32) * 32 + 32 * 33))));
+    CK(cudaFuncSetAttribute(qr_larft_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double) * ((QR_LARFT_MAXK - 32) * 32 + 32 * 33))));
     CK(cudaFuncSetAttribute(qr_leaf_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)std::min<size_t>(c.smem_optin, 227 * 1024) - 1024));
     CK(cudaFuncSetAttribute(qr_leaf_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -574,6 +616,15 @@ static int qr_refl_alloc(QrRefl& R, int64_t mp, int k) {
 
 static int qr_larft_launch(QrScratch& ws, QrRefl& R, const double* d_tau, int diag_given, cudaStream_t st) {
   const int k = R.k;
+  if (diag_given && k <= QR_LARFT_MAXK) {
+    for (int J0 = 32; J0 < k; J0 += 32) {
+      qr_larft_merge_kernel<<<(J0 + QR_MERGE_ROWS - 1) / QR_MERGE_ROWS, QR_MERGE_ROWS * 32,
+                              sizeof(double) * ((size_t)J0 * 32 + 32 * 33), st>>>(ws.g.p, R.ldt, k, J0, R.tt.p, R.ldt);
+      CK(cudaGetLastError());
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    return PFLU_OK;
+  }
   if (k <= QR_LARFT_MAXK) {
     qr_larft_kernel<<<1, QR_LARFT_THREADS, sizeof(double) * ((QR_LARFT_MAXK - 32) * 32 + 32 * 33), st>>>(
         ws.g.p, R.ldt, d_tau, k, R.tt.p, R.ldt, diag_given);
