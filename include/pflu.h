@@ -166,9 +166,10 @@ int pflu_gemm_update(double* d_c, int64_t ldc, const double* d_a, int64_t lda, c
 int pflu_geqrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, double* tau);
 
 /* Whole factorization, DEVICE buffers on the current device, ordered on `stream`; blocks until done.
- * d_tau: double[n] device. */
+ * d_tau: double[n] device.  trace (optional, may be NULL): PF / TU (look-ahead 0) or PF / TU_L / TU_R
+ * records as for pflu_getrf_device (the reference's TraceEvent labels, factor.py:104-122). */
 int pflu_geqrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, double* d_tau,
-                      void* stream);
+                      void* stream, pflu_trace_event* trace, int trace_cap, int* trace_len);
 
 /* Householder factorization of the panel rows [d, m) x columns [col, col + w) (the diagonal of
  * panel column j is row d + j; w <= m - d), in place; d_tau[0 .. w) receives the scalars.

@@ -104,7 +104,8 @@ def load():
         L.pflu_geqrf.restype = ctypes.c_int
         L.pflu_geqrf.argtypes = [_vp, _i64, _i64, _i64, _i64, ctypes.c_int, _pd]
         L.pflu_geqrf_device.restype = ctypes.c_int
-        L.pflu_geqrf_device.argtypes = [_vp, _i64, _i64, _i64, _i64, ctypes.c_int, _pd, _vp]
+        L.pflu_geqrf_device.argtypes = [_vp, _i64, _i64, _i64, _i64, ctypes.c_int, _pd, _vp,
+                                        ctypes.POINTER(TraceEvent), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         L.pflu_qr_panel.restype = ctypes.c_int
         L.pflu_qr_panel.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, _pd, _vp]
         L.pflu_larft.restype = ctypes.c_int

@@ -259,9 +259,10 @@ def geqrf_host(a: np.ndarray, b: int, lookahead: int) -> np.ndarray:
     return tau
 
 
-def geqrf_device(a, b: int, lookahead: int, tau=None):
+def geqrf_device(a, b: int, lookahead: int, tau=None, trace=None):
     """Householder QR of a row-major CUDA float64 torch tensor in place through pflu_geqrf_device
-    on the current torch stream.  Returns tau (float64 CUDA tensor of length n)."""
+    on the current torch stream.  Returns tau (float64 CUDA tensor of length n).  ``trace``: as for
+    :func:`getrf_device` (PF / TU or PF / TU_L / TU_R records)."""
     import torch
 
     L = _lib.load()
@@ -269,9 +270,21 @@ def geqrf_device(a, b: int, lookahead: int, tau=None):
     if tau is None:
         tau = torch.zeros(n, dtype=torch.float64, device=a.device)
     stream = torch.cuda.current_stream(a.device).cuda_stream
+    tbuf, tcap, tlen = None, 0, ctypes.c_int(0)
+    if trace is not None:
+        steps = -(-n // max(1, min(b, n)))
+        tcap = 8 * steps + 32
+        tbuf = (_lib.TraceEvent * tcap)()
     with torch.cuda.device(a.device):
-        rc = L.pflu_geqrf_device(a.data_ptr(), m, n, a.stride(0), int(b), int(lookahead), tau.data_ptr(), stream)
+        rc = L.pflu_geqrf_device(a.data_ptr(), m, n, a.stride(0), int(b), int(lookahead), tau.data_ptr(), stream,
+                                 tbuf, tcap, ctypes.byref(tlen))
     _lib.check(rc, "pflu_geqrf_device")
+    if trace is not None:
+        for i in range(tlen.value):
+            e = tbuf[i]
+            lab = _lib.TRACE_LABELS.get(e.label, str(e.label))
+            j = e.k + 1 if lab == "TU_L" else None
+            trace.append(TraceEvent(lab, int(e.k), j, e.start_ms * 1e-3, e.end_ms * 1e-3, None, float(e.flop)))
     return tau
 
 
@@ -326,14 +339,28 @@ def _factor_matrix(a, cfg: CacheConfig, kind: Kind, lookahead: int, strategy: St
     # row-major copy and write the factors back into the caller's buffer (in place, like the
     # reference, factor.py:300-302)
     work = np.ascontiguousarray(mat.array)
+    if trace is not None:
+        # the reference's trace hook (factor.py:104-122): run through the device-buffer entry point,
+        # which records CUDA-event timed PF / TU / TU_L / TU_R tasks into ``trace``
+        import torch
+
+        dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+        if dev is None:
+            raise RuntimeError("libpflu needs a CUDA device (there is no CPU fallback)")
+        t = torch.from_numpy(work).to(dev)
+        if kind is Kind.QR:
+            tau = geqrf_device(t, cfg.b, lookahead, trace=trace).cpu().numpy()
+            mat.array[...] = t.cpu().numpy()
+            return QrOutput(mat, tau, strategy)
+        piv, info = getrf_device(t, cfg.b, lookahead, trace=trace)
+        mat.array[...] = t.cpu().numpy()
+        return LuOutput(mat, piv.cpu().numpy() + 1, strategy, info)
     if kind is Kind.QR:
         tau = geqrf_host(work, cfg.b, lookahead)
         mat.array[...] = work
         return QrOutput(mat, tau, strategy)
     piv0, info = getrf_host(work, cfg.b, lookahead)
     mat.array[...] = work
-    if trace is not None:
-        trace.append(TraceEvent("PF" if lookahead == 0 else "TU_R", 0, None, 0.0, 0.0, None))
     return LuOutput(mat, piv0 + 1, strategy, info)
 
 

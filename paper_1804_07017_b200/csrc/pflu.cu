@@ -1349,7 +1349,7 @@ static int check_qr_dims(int64_t m, int64_t n, int64_t lda, int64_t b, int looka
 }
 
 int pflu_geqrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead, double* d_tau,
-                      void* stream) {
+                      void* stream, pflu_trace_event* trace, int trace_cap, int* trace_len) {
   if (!d_a) return -1;
   CKR(check_qr_dims(m, n, lda, b, lookahead));
   if (!d_tau) return -7;
@@ -1357,9 +1357,12 @@ int pflu_geqrf_device(double* d_a, int64_t m, int64_t n, int64_t lda, int64_t b,
   DevCtx* c = nullptr;
   CKR(ctx_get(&c));
   cudaStream_t st = (cudaStream_t)stream;
-  CKR(geqrf_async(*c, d_a, m, n, lda, std::min(b, n), lookahead, d_tau, st));
+  Tracer tr;
+  tr.c = c;
+  tr.on = trace != nullptr && trace_cap > 0;
+  CKR(geqrf_async(*c, d_a, m, n, lda, std::min(b, n), lookahead, d_tau, st, nullptr, &tr));
   CK(cudaStreamSynchronize(st));
-  return PFLU_OK;
+  return tr.collect(trace, trace_cap, trace_len);
 }
 
 // Host buffers: H2D into the grow-only device copy shared with pflu_getrf, the factorization, and a

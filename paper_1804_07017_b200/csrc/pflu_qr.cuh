@@ -800,7 +800,9 @@ static int qr_panel(DevCtx& c, QrCtx& q, double* a, int64_t lda, int64_t m, int6
 // `sink` (optional, host-buffer calls): row block k is final once step k's updates (TU_R(k) and
 // TU_L(k)) are done -- later steps only touch rows >= (k+1) b -- and is handed to the sink then.
 static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
-                       double* d_tau, cudaStream_t st, const RowSink* sink = nullptr) {
+                       double* d_tau, cudaStream_t st, const RowSink* sink = nullptr, Tracer* trp = nullptr) {
+  Tracer tr_off;
+  Tracer& tr = trp ? *trp : tr_off;
   QrCtx* qp = nullptr;
   CKR(qr_ctx(c, &qp));
   QrCtx& q = *qp;
@@ -825,15 +827,28 @@ static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   CK(cudaEventRecord(e_in, st));
   CK(cudaStreamWaitEvent(sP, e_in, 0));
   CK(cudaStreamWaitEvent(sU, e_in, 0));
+  CKR(tr.start(sP));
   auto bw_of = [&](int64_t k) { return std::min(b, n - k * b); };
+  // PF(k) on the panel stream: leaves + in-panel block reflectors (+ T when a trailing update follows)
+  auto pf = [&](int64_t k, bool with_t) -> int {
+    const int64_t col0 = k * b, bw = bw_of(k);
+    QrRefl& R = q.refl[k & 1];
+    int t_pf = -1;
+    CKR(tr.begin(PFLU_TRACE_PF, (int)k, sP, &t_pf));
+    CKR(qr_panel(c, q, a, lda, m, col0, col0, bw, d_tau + col0, R, sP));
+    if (with_t) CKR(qr_finish_t(c, q.ws[0], R, d_tau + col0, sP));
+    return tr.end(t_pf, sP);
+  };
   if (lookahead == 0) {
     for (int64_t k = 0; k < steps; ++k) {
       const int64_t col0 = k * b, bw = bw_of(k), lo = col0 + bw;
       QrRefl& R = q.refl[k & 1];
-      CKR(qr_panel(c, q, a, lda, m, col0, col0, bw, d_tau + col0, R, sP));
+      CKR(pf(k, lo < n));
       if (lo < n) {
-        CKR(qr_finish_t(c, q.ws[0], R, d_tau + col0, sP));
+        int t_tu = -1;
+        CKR(tr.begin(PFLU_TRACE_TU, (int)k, sP, &t_tu));
         CKR(qr_apply(c, q.ws[0], qr_view(R), a + col0 * lda + lo, lda, n - lo, sP));
+        CKR(tr.end(t_tu, sP));
       }
       if (sink) CKR((*sink)(col0, col0 + bw, sP));
     }
@@ -842,28 +857,33 @@ static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     return PFLU_OK;
   }
   // look-ahead 1
-  CKR(qr_panel(c, q, a, lda, m, 0, 0, bw_of(0), d_tau, q.refl[0], sP));
+  CKR(pf(0, bw_of(0) < n));
   for (int64_t k = 0; k < steps; ++k) {
     const int64_t col0 = k * b, bw = bw_of(k), lo = col0 + bw;
     if (lo >= n) break;
     QrRefl& R = q.refl[k & 1];
-    CKR(qr_finish_t(c, q.ws[0], R, d_tau + col0, sP));
     CK(cudaEventRecord(e_pf, sP));
     // TU_R(k): columns beyond block k+1, on the trailing stream
     const int64_t lo2 = lo + bw_of(k + 1);
     if (lo2 < n) {
       CK(cudaStreamWaitEvent(sU, e_pf, 0));
+      int t_r = -1;
+      CKR(tr.begin(PFLU_TRACE_TU_R, (int)k, sU, &t_r));
       CKR(qr_apply(c, q.ws[1], qr_view(R), a + col0 * lda + lo2, lda, n - lo2, sU));
+      CKR(tr.end(t_r, sU));
     }
     // TU_L(k) + PF(k+1) on the panel stream; TU_R(k-1) (recorded before e_tu is re-recorded
     // below) finished updating block k+1
+    int t_l = -1;
+    CKR(tr.begin(PFLU_TRACE_TU_L, (int)k, sP, &t_l));
     CKR(qr_apply(c, q.ws[0], qr_view(R), a + col0 * lda + lo, lda, bw_of(k + 1), sP));
+    CKR(tr.end(t_l, sP));
     if (sink) {  // row block k: final after TU_L(k) (panel stream) and TU_R(k) (trailing stream)
       CK(cudaEventRecord(e_tl, sP));
       CK(cudaStreamWaitEvent(sU, e_tl, 0));
       CKR((*sink)(col0, col0 + bw, sU));
     }
-    CKR(qr_panel(c, q, a, lda, m, lo, lo, bw_of(k + 1), d_tau + lo, q.refl[(k + 1) & 1], sP));
+    CKR(pf(k + 1, lo + bw_of(k + 1) < n));
     // the next TU_L / build (which rewrites refl[(k+1)&1] ... refl[k&1] at step k+2) must follow TU_R(k)
     if (lo2 < n) {
       CK(cudaEventRecord(e_tu, sU));

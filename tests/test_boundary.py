@@ -61,7 +61,7 @@ def test_argument_validation_codes_without_gpu():
     assert L.pflu_geqrf(b.ctypes.data, 8, 8, 8, 0, 1, tau.ctypes.data) == -5
     assert L.pflu_geqrf(b.ctypes.data, 8, 8, 8, 2, 2, tau.ctypes.data) == -6
     assert L.pflu_geqrf(b.ctypes.data, 8, 8, 8, 2, 1, None) == -7
-    assert L.pflu_geqrf_device(None, 8, 8, 8, 2, 1, None, None) == -1
+    assert L.pflu_geqrf_device(None, 8, 8, 8, 2, 1, None, None, None, 0, None) == -1
 
 
 def test_no_device_fails_loudly():

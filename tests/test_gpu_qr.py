@@ -256,3 +256,50 @@ def test_cli_qr_sweep_csv(cuda):
     buf = io.StringIO()
     cli.emit_csv(recs, buf)
     assert cli.parse_csv(buf.getvalue()) == recs
+
+
+@pytest.mark.parametrize("lookahead", [0, 1])
+def test_qr_trace_hook(cuda, lookahead):
+    """QR trace records (factor.py:104-122): a PF per step (a chain), TU (depth 0) or TU_L / TU_R (depth 1)."""
+    import torch
+    from paper_1804_07017_b200 import geqrf_device
+
+    n, b = 1000, 128
+    a = torch.from_numpy(np.random.default_rng(21).uniform(-1, 1, (n, n))).cuda()
+    tr = []
+    geqrf_device(a, b, lookahead, trace=tr)
+    steps = -(-n // b)
+    pf = {e.k: e for e in tr if e.label == "PF"}
+    assert sorted(pf) == list(range(steps))
+    for k in range(1, steps):
+        assert pf[k].start >= pf[k - 1].end - 1e-6
+    for e in tr:
+        assert 0.0 <= e.start <= e.end
+    if lookahead == 0:
+        assert sorted(e.k for e in tr if e.label == "TU") == list(range(steps - 1))
+    else:
+        assert sorted(e.k for e in tr if e.label == "TU_L") == list(range(steps - 1))
+        assert sorted(e.k for e in tr if e.label == "TU_R") == list(range(steps - 2))
+
+
+@pytest.mark.parametrize("kind_name", ["LU", "QR"])
+def test_dmf_la_trace_like_reference(cuda, kind_name):
+    """The reference's test_lookahead_overlap_instrumentation (test_factor.py:423-432) against the
+    drop-in dmf_la: {PF, TU_R} among the labels and one PF per block."""
+    from paper_1804_07017_b200 import CacheConfig, Kind, Matrix, dmf_la
+
+    cfg = CacheConfig(b=64)
+    n = 6 * cfg.b
+    a0 = np.random.default_rng(22).random((n, n))
+    m = Matrix.from_array(a0.copy())
+    trace = []
+    out = dmf_la(m, cfg, None, Kind[kind_name], malleable=True, trace=trace)
+    labels = {ev.label for ev in trace}
+    assert {"PF", "TU_R"} <= labels
+    pf = {ev.k: ev for ev in trace if ev.label == "PF"}
+    assert set(pf) == set(range(n // cfg.b))
+    if kind_name == "QR":
+        back, orth = oracle.qr_residual(a0, m.array, out.tau)
+        assert back <= 10 and orth <= 10
+    else:
+        assert oracle.lu_residual(a0, m.array, out.pivots - 1) <= 10
