@@ -562,6 +562,14 @@ struct QrCtx {
   QrSlot& slot(cudaStream_t st) {
     for (QrSlot* sl : slots)
       if (sl->st == st) return *sl;
+    if (slots.size() >= 8) {  // callers that create fresh streams per call: recycle the oldest slot
+      cudaDeviceSynchronize();
+      QrSlot* old = slots.front();
+      old->refl.vd.release(); old->refl.vt.release(); old->refl.tt.release();
+      old->ws.w.release(); old->ws.z.release(); old->ws.g.release(); old->ws.part.release();
+      delete old;
+      slots.erase(slots.begin());
+    }
     slots.push_back(new QrSlot());
     slots.back()->st = st;
     return *slots.back();
