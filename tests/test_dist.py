@@ -111,7 +111,7 @@ def test_local_columns_seeded_match_full_matrix(dist_name, seed):
             assert loc.tobytes() == pd.scatter_columns(torch.from_numpy(full), b, P, r).numpy().tobytes()
 
 
-def _qr_worker(rank, world, port, n, b, lookahead, seed, out_dir):
+def _qr_worker(rank, world, port, n, b, lookahead, seed, out_dir, zero_col=-1):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -121,6 +121,8 @@ def _qr_worker(rank, world, port, n, b, lookahead, seed, out_dir):
     from paper_1804_07017_b200 import dist as pd
 
     a = np.random.default_rng(seed).uniform(-1.0, 1.0, (n, n))
+    if zero_col >= 0:
+        a[zero_col + 1:, zero_col] = 0.0   # null reflector in that column
     loc = pd.scatter_columns(torch.from_numpy(a), b, world, rank)
     tau = pd.geqrf_block_cyclic(loc, n, b, lookahead, OracleKernels())
     f = pd.allgather_columns(loc, n, b)
@@ -131,14 +133,20 @@ def _qr_worker(rank, world, port, n, b, lookahead, seed, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,b,lookahead", [(2, 96, 16, 1), (2, 100, 16, 0), (3, 101, 8, 1), (4, 150, 16, 1)])
-def test_qr_block_cyclic_matches_oracle_bitwise(tmp_path, world, n, b, lookahead):
+@pytest.mark.parametrize("world,n,b,lookahead,zero_col", [(2, 96, 16, 1, -1), (2, 100, 16, 0, -1), (3, 101, 8, 1, -1),
+                                                          (4, 150, 16, 1, -1), (2, 64, 16, 1, 0), (3, 80, 8, 0, 21)])
+def test_qr_block_cyclic_matches_oracle_bitwise(tmp_path, world, n, b, lookahead, zero_col):
     """The distributed Householder QR (same schedule, oracle kernels) is bitwise the single-process
-    oracle: every column's operation sequence is independent of the column distribution."""
+    oracle: every column's operation sequence is independent of the column distribution (also with a
+    null reflector, tau = 0, in a column owned by a non-zero rank)."""
     import oracle
 
-    mp.spawn(_qr_worker, args=(world, _free_port(), n, b, lookahead, 7, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_qr_worker, args=(world, _free_port(), n, b, lookahead, 7, str(tmp_path), zero_col), nprocs=world,
+             join=True)
     f, tau = np.load(tmp_path / "f.npy"), np.load(tmp_path / "tau.npy")
     a = np.random.default_rng(7).uniform(-1.0, 1.0, (n, n))
+    if zero_col >= 0:
+        a[zero_col + 1:, zero_col] = 0.0
+        assert tau[zero_col] == 0.0
     rf, rtau = oracle.geqrf(a, b)
     assert f.tobytes() == rf.tobytes() and tau.tobytes() == rtau.tobytes()
