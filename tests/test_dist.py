@@ -122,7 +122,7 @@ def _qr_worker(rank, world, port, n, b, lookahead, seed, out_dir, zero_col=-1):
 
     a = np.random.default_rng(seed).uniform(-1.0, 1.0, (n, n))
     if zero_col >= 0:
-        a[zero_col + 1:, zero_col] = 0.0   # null reflector in that column
+        a[:, zero_col] = 0.0   # a zero column stays zero under every reflector: tau = 0 there
     loc = pd.scatter_columns(torch.from_numpy(a), b, world, rank)
     tau = pd.geqrf_block_cyclic(loc, n, b, lookahead, OracleKernels())
     f = pd.allgather_columns(loc, n, b)
@@ -146,7 +146,7 @@ def test_qr_block_cyclic_matches_oracle_bitwise(tmp_path, world, n, b, lookahead
     f, tau = np.load(tmp_path / "f.npy"), np.load(tmp_path / "tau.npy")
     a = np.random.default_rng(7).uniform(-1.0, 1.0, (n, n))
     if zero_col >= 0:
-        a[zero_col + 1:, zero_col] = 0.0
+        a[:, zero_col] = 0.0
         assert tau[zero_col] == 0.0
     rf, rtau = oracle.geqrf(a, b)
     assert f.tobytes() == rf.tobytes() and tau.tobytes() == rtau.tobytes()
