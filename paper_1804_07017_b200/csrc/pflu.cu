@@ -1392,7 +1392,9 @@ int pflu_geqrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int look
   double* d_a = c->hbuf;
   double* d_tau = q->htau.p;
   cudaStream_t st = c->sH, sD = c->sD;
-  if (cudaMemcpy2DAsync(d_a, ldd * 8, a, lda * 8, n * 8, m, cudaMemcpyHostToDevice, st) != cudaSuccess)
+  static const int qr_chunks = []() { const char* e = getenv("PFLU_QR_H2D_CHUNKS"); return e ? atoi(e) : 6; }();
+  const bool chunked = lookahead == 1 && qr_chunks > 1 && std::min(b, n) < n;
+  if (!chunked && cudaMemcpy2DAsync(d_a, ldd * 8, a, lda * 8, n * 8, m, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return set_err(PFLU_ERR_CUDA, "pflu_geqrf: H2D failed");
   int64_t sent = 0;
   size_t nev = 0;
@@ -1415,7 +1417,18 @@ int pflu_geqrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int look
     sent = r1;
     return PFLU_OK;
   };
-  CKR(geqrf_async(*c, d_a, m, n, ldd, std::min(b, n), lookahead, d_tau, st, &sink));
+  if (chunked) {
+    RowSinkM sinkm = [&](int64_t r0, int64_t r1, const std::vector<cudaEvent_t>& after) -> int {
+      if (r0 != sent || r1 <= r0) return PFLU_OK;
+      for (cudaEvent_t ev : after) CK(cudaStreamWaitEvent(sD, ev, 0));
+      CK(cudaMemcpy2DAsync(a + r0 * lda, lda * 8, d_a + r0 * ldd, ldd * 8, n * 8, r1 - r0, cudaMemcpyDeviceToHost, sD));
+      sent = r1;
+      return PFLU_OK;
+    };
+    CKR(geqrf_host_chunked(*c, d_a, m, n, ldd, std::min(b, n), d_tau, st, a, lda, qr_chunks, sinkm));
+  } else {
+    CKR(geqrf_async(*c, d_a, m, n, ldd, std::min(b, n), lookahead, d_tau, st, &sink));
+  }
   cudaEvent_t e;
   CKR(next_event(&e));
   CK(cudaEventRecord(e, st));

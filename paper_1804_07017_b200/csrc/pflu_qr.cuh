@@ -545,12 +545,17 @@ struct QrCtx {
   std::vector<QrSlot*> slots;  // pflu_larft / pflu_apply_block_reflector, one per stream
   QrScratch ws[2];    // 0: panel stream (leaves, TU_L), 1: trailing stream (TU_R)
   QrBuf htau;         // pflu_geqrf: device tau (grow-only)
+  static constexpr int RING = 8;
+  QrRefl ring[RING];            // pflu_geqrf's chunked schedule: reflectors of the last RING steps
+  QrScratch wsc[8];             // ... and one scratch per trailing column-chunk stream
   double* leafx = nullptr;  // leaf kernel exchange: dots, drow, partial Gram matrices
   unsigned* bar = nullptr;
   bool ready = false;
   void release() {
     for (QrRefl* r : {&refl[0], &refl[1], &leaf}) { r->vd.release(); r->vt.release(); r->tt.release(); }
+    for (auto& r : ring) { r.vd.release(); r.vt.release(); r.tt.release(); }
     for (auto& w : ws) { w.w.release(); w.z.release(); w.g.release(); w.part.release(); }
+    for (auto& w : wsc) { w.w.release(); w.z.release(); w.g.release(); w.part.release(); }
     htau.release();
     for (QrSlot* sl : slots) {
       sl->refl.vd.release(); sl->refl.vt.release(); sl->refl.tt.release();
@@ -805,6 +810,11 @@ static int qr_panel(DevCtx& c, QrCtx& q, double* a, int64_t lda, int64_t m, int6
 
 // Blocked QR, depth 0 (dmf_mtb order) or 1 (dmf_la: TU_L(k) + PF(k+1) on the panel stream while
 // TU_R(k) runs on the trailing stream), asynchronous; the caller's stream `st` is joined at the end.
+using RowSinkM = std::function<int(int64_t r0, int64_t r1, const std::vector<cudaEvent_t>& after)>;
+static int geqrf_host_chunked(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, int64_t b, double* d_tau,
+                              cudaStream_t st, const double* ha, int64_t hlda, int chunks, const RowSinkM& sinkm);
+static int g_qr_chunks = []() { const char* e = getenv("PFLU_QR_CHUNKS"); return e ? atoi(e) : 6; }();
+
 // `sink` (optional, host-buffer calls): row block k is final once step k's updates (TU_R(k) and
 // TU_L(k)) are done -- later steps only touch rows >= (k+1) b -- and is handed to the sink then.
 static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
@@ -864,7 +874,9 @@ static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     CK(cudaStreamWaitEvent(st, e_out, 0));
     return PFLU_OK;
   }
-  // look-ahead 1
+  // look-ahead 1 (device buffers): the column-chunk schedule of geqrf_host_chunked without the H2D
+  if (g_qr_chunks > 1 && !sink && !tr.on && b < n)
+    return geqrf_host_chunked(c, a, m, n, lda, b, d_tau, st, nullptr, 0, g_qr_chunks, RowSinkM());
   CKR(pf(0, bw_of(0) < n));
   for (int64_t k = 0; k < steps; ++k) {
     const int64_t col0 = k * b, bw = bw_of(k), lo = col0 + bw;
@@ -902,6 +914,112 @@ static int geqrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   CK(cudaStreamWaitEvent(st, e_out, 0));
   CK(cudaEventRecord(e_out, sP));
   CK(cudaStreamWaitEvent(st, e_out, 0));
+  return PFLU_OK;
+}
+
+// pflu_geqrf, look-ahead 1, host source: the H2D is issued per column chunk (the first two block
+// columns first) and the trailing update of every step runs per chunk on that chunk's stream, waiting
+// only for its own columns, so later columns are still in flight while the first steps run.  A chunk
+// that arrives late catches up on every earlier step, so the reflectors of the last RING steps are
+// kept (the panel stream waits before reusing a ring slot).  Row block k is handed to `sinkm` once
+// TU_L(k) and every chunk's TU_R(k) are done.
+static int geqrf_host_chunked(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, int64_t b, double* d_tau,
+                              cudaStream_t st, const double* ha, int64_t hlda, int chunks, const RowSinkM& sinkm) {
+  QrCtx* qp = nullptr;
+  CKR(qr_ctx(c, &qp));
+  QrCtx& q = *qp;
+  constexpr int NR = QrCtx::RING;
+  const int64_t steps = (n + b - 1) / b;
+  auto bw_of = [&](int64_t k) { return std::min(b, n - k * b); };
+  // chunks in block units: chunk 0 = blocks [0, 2), the rest split evenly
+  std::vector<int64_t> blo, bhi;
+  blo.push_back(0);
+  bhi.push_back(std::min<int64_t>(2, steps));
+  const int rest_ch = std::max(0, std::min<int>(chunks - 1, (int)(steps - bhi[0])));
+  for (int i = 0; i < rest_ch; ++i) {
+    const int64_t rb = steps - bhi[0];
+    blo.push_back(bhi[0] + rb * i / rest_ch);
+    bhi.push_back(bhi[0] + rb * (i + 1) / rest_ch);
+  }
+  const int nch = (int)blo.size();
+  auto chunk_of = [&](int64_t blk) { int ci = 0; while (ci + 1 < nch && blk >= bhi[ci]) ++ci; return ci; };
+  {  // every buffer at its maximum before the first launch (see QrBuf::need)
+    for (auto& R : q.ring) {
+      CKR(R.vd.need((size_t)(m * qr_even(b))));
+      CKR(R.vt.need((size_t)(b * qr_even(m))));
+      CKR(R.tt.need((size_t)(b * qr_even(b))));
+    }
+    for (QrScratch* w : {&q.ws[0], &q.wsc[0], &q.wsc[1], &q.wsc[2], &q.wsc[3], &q.wsc[4], &q.wsc[5], &q.wsc[6],
+                         &q.wsc[7]}) {
+      CKR(w->w.need((size_t)(b * qr_even(n))));
+      CKR(w->z.need((size_t)(b * qr_even(n))));
+      CKR(w->g.need((size_t)(b * qr_even(b))));
+      CKR(w->part.need((size_t)4 * c.sms * 128 * 65));
+    }
+  }
+  // events: [0] start, [1 + ci] H2D of chunk ci, then per step: e_pf, e_tl, nch chunk events
+  const size_t ne = 2 + (size_t)nch;
+  CKR(ctx_events(c, 1 + nch + (size_t)steps * ne + 1));
+  cudaEvent_t e_in = c.ev[0];
+  auto evH = [&](int ci) { return c.ev[1 + ci]; };
+  auto evPF = [&](int64_t k) { return c.ev[1 + nch + (size_t)k * ne]; };
+  auto evTL = [&](int64_t k) { return c.ev[1 + nch + (size_t)k * ne + 1]; };
+  auto evC = [&](int64_t k, int ci) { return c.ev[1 + nch + (size_t)k * ne + 2 + ci]; };
+  cudaEvent_t e_end = c.ev[1 + nch + (size_t)steps * ne];
+  cudaStream_t sP = c.sP;
+  CK(cudaEventRecord(e_in, st));
+  CK(cudaStreamWaitEvent(sP, e_in, 0));
+  for (int ci = 0; ci < nch; ++ci) {
+    const int64_t c0 = blo[ci] * b, c1 = std::min(n, bhi[ci] * b);
+    if (ha)
+      CK(cudaMemcpy2DAsync(a + c0, lda * 8, ha + c0, hlda * 8, (c1 - c0) * 8, m, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(evH(ci), st));
+    CK(cudaStreamWaitEvent(c.sC[ci], e_in, 0));
+  }
+  auto pf = [&](int64_t k) -> int {
+    const int64_t col0 = k * b, bw = bw_of(k);
+    QrRefl& R = q.ring[k % NR];
+    CKR(qr_panel(c, q, a, lda, m, col0, col0, bw, d_tau + col0, R, sP));
+    if (col0 + bw < n) CKR(qr_finish_t(c, q.ws[0], R, d_tau + col0, sP));
+    return PFLU_OK;
+  };
+  CK(cudaStreamWaitEvent(sP, evH(0), 0));
+  CKR(pf(0));
+  for (int64_t k = 0; k < steps; ++k) {
+    const int64_t col0 = k * b, bw = bw_of(k), lo = col0 + bw;
+    if (lo >= n) break;
+    QrRefl& R = q.ring[k % NR];
+    CK(cudaEventRecord(evPF(k), sP));
+    const int64_t lo2 = lo + bw_of(k + 1);
+    for (int ci = 0; ci < nch; ++ci) {  // TU_R(k), chunk by chunk
+      cudaStream_t sc = c.sC[ci];
+      const int64_t c0 = std::max(lo2, blo[ci] * b), c1 = std::min(n, bhi[ci] * b);
+      if (c1 > c0) {
+        CK(cudaStreamWaitEvent(sc, evH(ci), 0));
+        CK(cudaStreamWaitEvent(sc, evPF(k), 0));
+        CKR(qr_apply(c, q.wsc[ci], qr_view(R), a + col0 * lda + c0, lda, c1 - c0, sc));
+      }
+      CK(cudaEventRecord(evC(k, ci), sc));
+    }
+    // TU_L(k): block k+1 was last updated by TU_R(k-1) on its chunk
+    const int cb = chunk_of(k + 1);
+    CK(cudaStreamWaitEvent(sP, k >= 1 ? evC(k - 1, cb) : evH(cb), 0));
+    CKR(qr_apply(c, q.ws[0], qr_view(R), a + col0 * lda + lo, lda, bw_of(k + 1), sP));
+    CK(cudaEventRecord(evTL(k), sP));
+    // PF(k+1) reuses ring slot (k+1) % NR: every chunk must be done with step k+1-NR
+    if (k + 1 - NR >= 0)
+      for (int ci = 0; ci < nch; ++ci) CK(cudaStreamWaitEvent(sP, evC(k + 1 - NR, ci), 0));
+    CKR(pf(k + 1));
+    std::vector<cudaEvent_t> fin{evTL(k)};
+    for (int ci = 0; ci < nch; ++ci) fin.push_back(evC(k, ci));
+    if (sinkm) CKR(sinkm(col0, col0 + bw, fin));
+  }
+  for (int ci = 0; ci < nch; ++ci) {
+    CK(cudaEventRecord(e_end, c.sC[ci]));
+    CK(cudaStreamWaitEvent(st, e_end, 0));
+  }
+  CK(cudaEventRecord(e_end, sP));
+  CK(cudaStreamWaitEvent(st, e_end, 0));
   return PFLU_OK;
 }
 
