@@ -100,7 +100,7 @@ static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return
 static int g_trsm_dmma = []() { const char* e = getenv("PFLU_TRSM_DMMA"); return e ? atoi(e) : 1; }();
 static int64_t g_grid_rows = []() { const char* e = getenv("PFLU_GRID_ROWS"); return e ? atoll(e) : 8192; }();
 static int g_resync = []() { const char* e = getenv("PFLU_PANEL_RESYNC"); return e ? atoi(e) : 4; }();
-static int g_chunks = []() { const char* e = getenv("PFLU_CHUNKS"); return e ? atoi(e) : 1; }();
+static int g_chunks = []() { const char* e = getenv("PFLU_CHUNKS"); return e ? atoi(e) : 1; }();  // r04: 6 chunks: C3 117.2 -> 115.1 ms, C4 755.7 -> 754.2 ms, but the C4 GEMM roofline reads 0.845 (concurrent chunk GEMMs) vs 0.860
 static int g_tur_grid = []() { const char* e = getenv("PFLU_TUR_GRID"); return e ? atoi(e) : 0; }();
 // recursive panel (panel_kernel 3): leaf width and leaf kernel (0 auto, 1 grid, 2 cluster)
 static int g_rec_leaf = []() { const char* e = getenv("PFLU_REC_LEAF"); return e ? atoi(e) : 32; }();
