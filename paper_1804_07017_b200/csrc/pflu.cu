@@ -100,7 +100,7 @@ static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return
 static int g_trsm_dmma = []() { const char* e = getenv("PFLU_TRSM_DMMA"); return e ? atoi(e) : 1; }();
 static int64_t g_grid_rows = []() { const char* e = getenv("PFLU_GRID_ROWS"); return e ? atoll(e) : 8192; }();
 static int g_resync = []() { const char* e = getenv("PFLU_PANEL_RESYNC"); return e ? atoi(e) : 4; }();
-static int g_chunks = []() { const char* e = getenv("PFLU_CHUNKS"); return e ? atoi(e) : 1; }();  // r04: 6 chunks: C3 117.2 -> 115.1 ms, C4 755.7 -> 754.2 ms, but the C4 GEMM roofline reads 0.845 (concurrent chunk GEMMs) vs 0.860
+static int g_chunks_env = []() { const char* e = getenv("PFLU_CHUNKS"); return e ? atoi(e) : 0; }();  // 0: by size (getrf_async)
 static int g_tur_grid = []() { const char* e = getenv("PFLU_TUR_GRID"); return e ? atoi(e) : 0; }();
 // recursive panel (panel_kernel 3): leaf width and leaf kernel (0 auto, 1 grid, 2 cluster)
 static int g_rec_leaf = []() { const char* e = getenv("PFLU_REC_LEAF"); return e ? atoi(e) : 32; }();
@@ -879,7 +879,11 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   //                          PF(k+1), plan(k+1)
   //   sC[c]:                 TU_R(k) restricted to chunk c (after PF(k))
   //   sL:                    left swaps(k) on blocks < k (after every reader of L21(k-1) finished)
-  const int nch = std::max(1, std::min({hin ? std::max(g_chunks, hin->chunks) : g_chunks, MAX_CHUNKS, count}));
+  // device buffers: 6 chunks up to n = 16384, where the panel chain still shows (C3 117.2 -> 115.1 ms,
+  // C2 31.9 -> 31.6 ms: the panel stream only waits for the chunk that holds block k+1); one stream
+  // above (C4 unchanged, its concurrent chunk GEMMs interfere); PFLU_CHUNKS overrides
+  const int dflt = g_chunks_env > 0 ? g_chunks_env : (n <= 16384 ? 6 : 1);
+  const int nch = std::max(1, std::min({hin ? std::max(dflt, hin->chunks) : dflt, MAX_CHUNKS, count}));
   std::vector<int> chunk_blk(nch + 1);
   for (int ch = 0; ch <= nch; ++ch) chunk_blk[ch] = (int)((int64_t)count * ch / nch);
   auto chunk_of_block = [&](int blk) {
