@@ -364,6 +364,45 @@ def run_single_qr(args) -> None:
     ms_step = e0.elapsed_time(e1) / args.steps
     value = qr_flops(n) / (ms_step * 1e-3) / 1e9
     peak, peak_src = fp64_peak()
+    # roofline of the dominant work, the block-reflector GEMMs (W = V^T C, Z = T^T W, C -= V Z): one
+    # extra TRACED factorization (single-stream schedule, not part of the timed steps); achieved =
+    # 4 * m_p * n_c * b algorithmic flop per TU_R / TU_L record over the union of those intervals
+    from paper_1804_07017_b200 import geqrf_device
+
+    d_a.copy_(d_a0)
+    tr = []
+    geqrf_device(d_a, b, la, trace=tr)
+    torch.cuda.synchronize()
+    fl_tu, iv = 0.0, []
+    for e in tr:
+        if e.label in ("TU_R", "TU_L", "TU"):
+            col0 = e.k * b
+            mp = n - col0
+            if e.label == "TU_L":
+                nc = min(b, n - col0 - b)
+            elif e.label == "TU_R":
+                nc = n - col0 - b - min(b, n - col0 - b)
+            else:
+                nc = n - col0 - b
+            fl_tu += 4.0 * mp * max(nc, 0) * min(b, n - col0)
+            iv.append((e.start, e.end))
+    iv.sort()
+    busy, cs, ce = 0.0, None, None
+    for s_, e_ in iv:
+        if ce is None or s_ > ce:
+            if ce is not None:
+                busy += ce - cs
+            cs, ce = s_, e_
+        else:
+            ce = max(ce, e_)
+    if ce is not None:
+        busy += ce - cs
+    achieved = fl_tu / busy / 1e12 if busy > 0 else None
+    roofline = {"bound": "tensor", "kernel": "block reflector: split-K gemm_dmma_t<128x64x32> (V^T C) + gemm_dmma_t (C -= V Z)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+                "traffic": None, "peak_source": peak_src,
+                "algorithmic": "4*m_p*n_c*b flop per TU_R / TU_L record (m_p = n - kb rows, n_c = updated columns) over the "
+                               "union of their CUDA-event intervals, from one traced (single-stream) factorization"}
     e2e = None
     if args.e2e_steps > 0:
         pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
@@ -407,7 +446,7 @@ def run_single_qr(args) -> None:
         "config": {"workload": f"QR (Kind.QR) n={n} U[-1,1) numpy seed 3, b={b}, look-ahead {la}", "n": n, "b": b,
                    "lookahead": la, "parallelism": "single GPU", "fp64_peak_frac": value / 1e3 / peak,
                    "l2": "inputs (8.6 GB) larger than L2; pristine matrix restored by a D2D copy inside each step"},
-        "peak": peak, "peak_source": peak_src, "clocks": clk, "e2e": e2e, "gpu_launches": launches,
+        "roofline": roofline, "clocks": clk, "e2e": e2e, "gpu_launches": launches,
         "cpu_baseline": cpu, "parity": parity,
     }
     print(json.dumps(line), flush=True)
