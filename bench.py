@@ -56,8 +56,38 @@ def fp64_peak() -> tuple[float, str]:
     return 148 * 1.965e9 * 128 / 1e12, "nominal 148 SMs x 128 flop/clk x 1.965 GHz"
 
 
-def c4_matrix(n: int, seed: int = 3) -> np.ndarray:
-    return np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n, n))
+#: BASELINE.json configs: name -> (n, numpy seed, distribution, b, diagonal shift)
+CONFIGS = {
+    "c1": (2048, 0, "uniform", 128, 0.0),
+    "c2": (8192, 1, "uniform", 256, 0.0),
+    "c2s": (8192, 1, "uniform", 256, 8192.0),
+    "c3": (16384, 2, "normal", 256, 0.0),
+    "c4": (32768, 3, "uniform", 256, 0.0),
+    "c5": (65536, 4, "normal", 512, 0.0),
+}
+
+
+def config_matrix(name: str, n: int | None = None) -> np.ndarray:
+    """The seeded BASELINE matrix (numpy default_rng(seed), row-major draw order), generated in row
+    chunks (the same sequence as one call) so C5's 34 GB needs no second copy."""
+    n0, seed, dist_name, _, shift = CONFIGS[name]
+    n = n0 if n is None else n
+    g = np.random.default_rng(seed)
+    a = np.empty((n, n))
+    rows = max(1, (1 << 27) // n)
+    for r0 in range(0, n, rows):
+        r1 = min(n, r0 + rows)
+        a[r0:r1] = g.uniform(-1.0, 1.0, size=(r1 - r0, n)) if dist_name == "uniform" else g.standard_normal((r1 - r0, n))
+    if shift:
+        a[np.diag_indices(n)] += shift
+    return a
+
+
+def workload_name(args) -> str:
+    n0, seed, dist_name, _, shift = CONFIGS[args.config]
+    d = "U[-1,1)" if dist_name == "uniform" else "N(0,1)"
+    sh = f" + {shift:g} I" if shift else ""
+    return f"{args.config.upper()}: LUpp n={args.n} {d} numpy seed {seed}{sh}, b={args.b}, look-ahead {args.lookahead}"
 
 
 class ClockSampler:
@@ -127,7 +157,7 @@ def load_traffic() -> tuple[float | None, str | None]:
         return None, None
 
 
-def cpu_sample(n: int, b: int, threads: int | None = None):
+def cpu_sample(n: int, b: int, threads: int | None = None, cfg: str = "c4"):
     """The oracle port (bitwise the reference's arithmetic, all host threads) on the first blocked
     step of the same matrix; GFLOP/s = that step's flops / wall time.  Also returns the step's final
     outputs (pivots [0, b) and factor rows [0, b)) for the bench's parity check."""
@@ -135,7 +165,7 @@ def cpu_sample(n: int, b: int, threads: int | None = None):
 
     cores = threads or os.cpu_count() or 1
     oracle.set_threads(cores)
-    a = c4_matrix(n)
+    a = config_matrix(cfg, n)
     piv = np.zeros(n, dtype=np.int64)
     t0 = time.perf_counter()
     oracle.getrf_steps_inplace(a, b, 1, piv)
@@ -143,7 +173,7 @@ def cpu_sample(n: int, b: int, threads: int | None = None):
     fl = oracle.step_flops(n, n, b, 0)
     return ({"value": fl / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
              "sample": f"first blocked step (panel {n}x{b} + laswp + trsm + {n - b}^2x{b} gemm) of the n={n} "
-                       f"C4 matrix, {fl / 1e9:.1f} GFLOP in {dt:.2f} s, oracle/pflu_oracle.c -O3 OpenMP"},
+                       f"{cfg.upper()} matrix, {fl / 1e9:.1f} GFLOP in {dt:.2f} s, oracle/pflu_oracle.c -O3 OpenMP"},
             piv[:b].copy(), a[:b].copy())
 
 
@@ -158,7 +188,7 @@ def run_reference(args) -> None:
     n, b = args.n, args.b
     cores = os.cpu_count() or 1
     oracle.set_threads(cores)
-    pristine = c4_matrix(n)
+    pristine = config_matrix(args.config, n)
     work = np.empty_like(pristine)
     piv = np.zeros(n, dtype=np.int64)
     fl = oracle.step_flops(n, n, b, 0)
@@ -179,7 +209,7 @@ def run_reference(args) -> None:
         "config": {"workload": f"C4: LUpp n={n} U[-1,1) seed 3, b={b}, look-ahead 1",
                    "sample": "first blocked step of C4 per step"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"first blocked step of the n={n} C4 matrix ({fl / 1e9:.1f} GFLOP) per step; "
+                         "sample": f"first blocked step of the n={n} {args.config.upper()} matrix ({fl / 1e9:.1f} GFLOP) per step; "
                                    "oracle/pflu_oracle.c is op-for-op the reference (pinned bitwise, tests/test_oracle.py)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -195,7 +225,7 @@ def run_single(args) -> None:
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
     n, b, la = args.n, args.b, args.lookahead
-    a_host = c4_matrix(n)
+    a_host = config_matrix(args.config, n)
     d_a0 = torch.from_numpy(a_host).to(dev)
     d_a = torch.empty_like(d_a0)
     piv = torch.empty(n, dtype=torch.int64, device=dev)
@@ -281,7 +311,7 @@ def run_single(args) -> None:
     cpu = None
     parity = None
     if not args.no_cpu:
-        cpu, ref_piv, ref_rows = cpu_sample(n, b)
+        cpu, ref_piv, ref_rows = cpu_sample(n, b, cfg=args.config)
     if not args.no_check:
         # parity of the timed run's own output (last step): the oracle's first blocked step (pivots
         # and factor rows [0, b) are final after it) and the full backward error on the GPU
@@ -297,7 +327,7 @@ def run_single(args) -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"C4: LUpp n={n} U[-1,1) numpy seed 3, b={b}, look-ahead {la}",
+        "config": {"workload": workload_name(args),
                    "n": n, "b": b, "lookahead": la, "parallelism": "single GPU",
                    "l2": "inputs (8.6 GB) larger than L2; pristine matrix restored by a D2D copy inside each step",
                    "fp64_peak_frac": value / 1e3 / peak},
@@ -337,7 +367,7 @@ def run_single_qr(args) -> None:
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
     n, b, la = args.n, args.b, args.lookahead
-    a_host = c4_matrix(n)
+    a_host = config_matrix(args.config, n)
     d_a0 = torch.from_numpy(a_host).to(dev)
     d_a = torch.empty_like(d_a0)
     stream = torch.cuda.current_stream(dev)
@@ -452,14 +482,58 @@ def run_single_qr(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(n_gpus: int) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-launch this command under
+    torch.distributed.run with N ranks (one per GPU, rendezvous on 127.0.0.1); rank 0 prints the
+    JSON line.  Fails loudly when fewer than N GPUs are visible (never silently measures fewer)."""
+    selftest = "--selftest-launch" in sys.argv
+    if not selftest:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < n_gpus:
+            print(f"bench.py: --gpus {n_gpus} requested but only {have} CUDA device(s) are visible", file=sys.stderr)
+            return 2
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # the communicator log (nranks) stays visible on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def selftest_launch(args) -> None:
+    """--selftest-launch (CPU test of the launcher): every rank joins a gloo group and contributes
+    one to an all-reduce; rank 0 prints the JSON line with n_gpus = the number of ranks that ran."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    if dist.get_rank() == 0:
+        print(json.dumps({"metric": METRIC, "n_gpus": dist.get_world_size(), "ranks_seen": int(t.item()),
+                          "selftest": True, "argv_gpus": args.gpus}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS),
+                    help="BASELINE.json config (default C4, the one the metric's targets are quoted on)")
+    ap.add_argument("--selftest-launch", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=32768)
-    ap.add_argument("--b", type=int, default=256)
+    ap.add_argument("--n", type=int, default=None, help="override the config's n (same generator)")
+    ap.add_argument("--b", type=int, default=None, help="override the config's block size")
     ap.add_argument("--lookahead", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
@@ -469,17 +543,28 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    n0, _, _, b0, _ = CONFIGS[args.config]
+    args.n = n0 if args.n is None else args.n
+    args.b = b0 if args.b is None else args.b
+    world = int(os.environ.get("WORLD_SIZE", "0") or 0)
+    if args.gpus > 1 and world == 0 and args.impl == "ours":
+        sys.exit(spawn_ranks(args.gpus))
+    if world > 1 and args.gpus != world:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if args.selftest_launch:
+        selftest_launch(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
     if args.kind == "qr":
         run_single_qr(args)
         return
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1 or args.dist:
         from paper_1804_07017_b200.dist import bench_dist
 
-        bench_dist(args, lu_flops, METRIC, UNIT, ClockSampler, fp64_peak)
+        bench_dist(args, lu_flops, METRIC, UNIT, ClockSampler, fp64_peak, CONFIGS, workload_name(args))
         return
     run_single(args)
 

@@ -56,6 +56,8 @@ def lib():
         L.orc_getrf.argtypes = [_d, _I64, _I64, _I64, _I64, _i]
         L.orc_getrf_steps.restype = _I64
         L.orc_getrf_steps.argtypes = [_d, _I64, _I64, _I64, _I64, _i, _I64]
+        L.orc_getrf_steps_top2.restype = _I64
+        L.orc_getrf_steps_top2.argtypes = [_d, _I64, _I64, _I64, _I64, _i, _I64, _d]
         L.orc_qr_unb.restype = None
         L.orc_qr_unb.argtypes = [_d, _I64, _I64, _I64, _d]
         L.orc_larft.restype = None
@@ -119,6 +121,55 @@ def getrf_steps_inplace(a: np.ndarray, b: int, nsteps: int, piv: np.ndarray | No
     if piv is None:
         piv = np.zeros(n, dtype=np.int64)
     return int(lib().orc_getrf_steps(_dp(a), m, n, a.strides[0] // 8, int(b), _ip(piv), int(nsteps)))
+
+
+def getrf_top2_inplace(a: np.ndarray, b: int, piv: np.ndarray | None = None):
+    """The full blocked factorization in place (row-major, any size that fits in host memory), with
+    the tie classifier's record: top2[j] = (|winner|, |runner-up|, runner-up row) of column j's pivot
+    search (reference _jit.py:162-170, strict '>' so the smallest row wins).  Returns (piv, top2, info)."""
+    m, n = a.shape
+    if not a.flags.c_contiguous or a.dtype != np.float64:
+        raise ValueError("row-major float64 array required (in place)")
+    if piv is None:
+        piv = np.zeros(n, dtype=np.int64)
+    top2 = np.full((n, 3), -1.0)
+    info = int(lib().orc_getrf_steps_top2(_dp(a), m, n, n, int(b), _ip(piv), -1, _dp(top2)))
+    return piv, top2, info
+
+
+#: north_star's tie rule: a pivot may differ only where the top two magnitudes tie within this.
+TIE_RTOL = 1e-12
+
+
+def near_ties(top2: np.ndarray, rtol: float = 1e-6) -> np.ndarray:
+    """Rows (col, |winner|, |runner-up|, runner-up row) of every column whose relative top-two gap
+    (v1 - v2) / v1 is <= rtol (the columns where a correctly rounded factorization could pick another
+    pivot).  Committed per config so a GPU pivot mismatch can be classified without a host re-run."""
+    v1, v2 = top2[:, 0], top2[:, 1]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        gap = np.where(v1 > 0, (v1 - v2) / v1, np.inf)
+    cols = np.nonzero((v2 >= 0) & (gap <= rtol))[0]
+    return np.column_stack([cols.astype(np.float64), v1[cols], v2[cols], top2[cols, 2]])
+
+
+def classify_pivots(piv_gpu, piv_ref, ties: np.ndarray, rtol: float = TIE_RTOL) -> dict:
+    """North_star's pivot rule: identical, or the FIRST mismatch is a column whose top-two candidate
+    magnitudes tie within `rtol` relative and the GPU took the runner-up (everything after a legitimate
+    tie break legitimately differs).  `ties` = near_ties(top2) of the reference/oracle run."""
+    piv_gpu = np.asarray(piv_gpu, dtype=np.int64)
+    piv_ref = np.asarray(piv_ref, dtype=np.int64)
+    diff = np.nonzero(piv_gpu != piv_ref)[0]
+    if len(diff) == 0:
+        return {"equal": True, "first_mismatch": None, "tie": None, "ok": True}
+    j = int(diff[0])
+    row = ties[ties[:, 0] == j] if len(ties) else ties
+    if len(row) == 0:
+        return {"equal": False, "first_mismatch": j, "tie": None, "ok": False}
+    _, v1, v2, r2 = row[0]
+    gap = (v1 - v2) / v1
+    ok = bool(gap <= rtol and int(r2) == int(piv_gpu[j]))
+    return {"equal": False, "first_mismatch": j, "tie": {"v1": v1, "v2": v2, "rel_gap": gap,
+            "runner_up_row": int(r2)}, "ok": ok}
 
 
 def step_flops(m: int, n: int, b: int, k: int = 0) -> int:

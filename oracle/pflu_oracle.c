@@ -17,6 +17,8 @@
  *                     accumulator is seeded from C and updated with p ascending, multiply then
  *                     add; a*(-b) == -(a*b) exactly, so this is c - a*b)
  *   orc_getrf      <- factor.py:382-412 (dmf_mtb) with the step body of factor.py:235-285;
+ *   orc_getrf_steps_top2 <- the same, instrumented: per column the winner's and the runner-up's
+ *                     magnitudes of _jit.py:162-170's search (tie classification, north_star);
  *                     dmf_la (factor.py:455-515) is bitwise identical.
  *
  * Storage here is ROW-MAJOR (element (i,j) at a[i*lda+j]); the reference stores column-major
@@ -40,18 +42,25 @@ static int nthreads(void) { return g_threads > 0 ? g_threads : omp_get_max_threa
 /* Unblocked right-looking LU on an m x w panel (row-major, leading dim lda).  Processes the
  * first `steps` columns (steps <= min(m, w); pass -1 for all).  piv[j] = 0-based panel-local
  * pivot row.  Returns 0 or 1 + first column whose pivot was exactly zero (left as is). */
-int64_t orc_lu_unb(double *a, int64_t m, int64_t w, int64_t lda, int64_t *piv, int64_t steps) {
+/* top2 (optional, 3 doubles per column): the tie classifier's record of column j's search --
+ * |winner|, the largest |candidate| among the OTHER rows (-1 if none) and that runner-up's
+ * panel-local row (the smallest such row, as the strict '>' scan would take it).  North_star allows
+ * a pivot mismatch only where these two magnitudes tie within 1e-12 relative. */
+static int64_t lu_unb_impl(double *a, int64_t m, int64_t w, int64_t lda, int64_t *piv, int64_t steps,
+                           double *top2) {
   int64_t kmax = m < w ? m : w;
   if (steps >= 0 && steps < kmax) kmax = steps;
   int64_t info = 0;
   int nt = nthreads();
   for (int64_t j = 0; j < kmax; ++j) {
-    int64_t pbest = j;
-    double vbest = fabs(a[IDX(j, j, lda)]);
+    int64_t pbest = j, p2 = -1;
+    double vbest = fabs(a[IDX(j, j, lda)]), v2 = -1.0;
     for (int64_t i = j + 1; i < m; ++i) {
       double v = fabs(a[IDX(i, j, lda)]);
-      if (v > vbest) { vbest = v; pbest = i; }
+      if (v > vbest) { v2 = vbest; p2 = pbest; vbest = v; pbest = i; }
+      else if (top2 && v > v2) { v2 = v; p2 = i; }
     }
+    if (top2) { top2[3 * j] = vbest; top2[3 * j + 1] = v2; top2[3 * j + 2] = (double)p2; }
     piv[j] = pbest;
     if (vbest == 0.0) {
       if (info == 0) info = j + 1;
@@ -76,6 +85,10 @@ int64_t orc_lu_unb(double *a, int64_t m, int64_t w, int64_t lda, int64_t *piv, i
     }
   }
   return info;
+}
+
+int64_t orc_lu_unb(double *a, int64_t m, int64_t w, int64_t lda, int64_t *piv, int64_t steps) {
+  return lu_unb_impl(a, m, w, lda, piv, steps, NULL);
 }
 
 /* Rows k1..k2-1 swapped with piv[k] (0-based global rows), ascending k, on columns [c0, c1). */
@@ -150,16 +163,21 @@ void orc_gemm_sub(double *c, int64_t ldc, const double *a, int64_t lda, const do
 /* Blocked right-looking LUpp (dmf_mtb order, factor.py:382-412): for each panel k: panel
  * factorization (lu_unb on rows col0.., panel width), left swaps on [0, col0), right swaps +
  * trsm + gemm on [col0+bw, n).  m >= n >= 1 (caller validates).  piv: 0-based global rows. */
-int64_t orc_getrf_steps(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, int64_t *piv, int64_t nsteps) {
+/* top2: NULL, or 3 doubles per column (see lu_unb_impl; the runner-up row made global). */
+int64_t orc_getrf_steps_top2(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, int64_t *piv,
+                             int64_t nsteps, double *top2) {
   int64_t info = 0;
   int64_t step = 0;
   for (int64_t col0 = 0; col0 < n && (nsteps < 0 || step < nsteps); col0 += b, ++step) {
     int64_t bw = n - col0 < b ? n - col0 : b;
     double *panel = a + IDX(col0, col0, lda);
-    int64_t pinfo = orc_lu_unb(panel, m - col0, bw, lda, piv + col0, -1);
+    int64_t pinfo = lu_unb_impl(panel, m - col0, bw, lda, piv + col0, -1, top2 ? top2 + 3 * col0 : NULL);
     if (pinfo && !info) info = col0 + pinfo;
     int64_t kk = (m - col0) < bw ? (m - col0) : bw;
-    for (int64_t j = 0; j < kk; ++j) piv[col0 + j] += col0;
+    for (int64_t j = 0; j < kk; ++j) {
+      piv[col0 + j] += col0;
+      if (top2 && top2[3 * (col0 + j) + 2] >= 0.0) top2[3 * (col0 + j) + 2] += (double)col0;
+    }
     orc_laswp(a, lda, 0, col0, piv, col0, col0 + kk);                 /* left swaps */
     int64_t lo = col0 + bw;
     if (lo < n) {
@@ -171,6 +189,10 @@ int64_t orc_getrf_steps(double *a, int64_t m, int64_t n, int64_t lda, int64_t b,
     }
   }
   return info;
+}
+
+int64_t orc_getrf_steps(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, int64_t *piv, int64_t nsteps) {
+  return orc_getrf_steps_top2(a, m, n, lda, b, piv, nsteps, NULL);
 }
 
 int64_t orc_getrf(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, int64_t *piv) {

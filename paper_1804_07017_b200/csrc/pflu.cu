@@ -179,12 +179,27 @@ static DevCtx g_ctx[64];
 
 static constexpr int PF_MAX_CTAS = PF_THREADS;
 
-static const void* pf_fn(int W, bool cl) {
+#ifdef PFLU_PANEL_EXACT_T
+// hazard re-check build: the exact flag compiled into the panel kernel (see panel_kernel's EX)
+template <int EX>
+static const void* pf_fn_ex(int W, bool cl) {
+  if (cl) return W == 8 ? (const void*)panel_kernel<8, true, EX> : W == 16 ? (const void*)panel_kernel<16, true, EX>
+                                                                           : (const void*)panel_kernel<32, true, EX>;
+  return W == 8 ? (const void*)panel_kernel<8, false, EX> : W == 16 ? (const void*)panel_kernel<16, false, EX>
+                                                                    : (const void*)panel_kernel<32, false, EX>;
+}
+static const void* pf_fn(int W, bool cl, bool exact = false) {
+  return exact ? pf_fn_ex<1>(W, cl) : pf_fn_ex<0>(W, cl);
+}
+#else
+static const void* pf_fn(int W, bool cl, bool exact = false) {
+  (void)exact;
   if (cl) return W == 8 ? (const void*)panel_kernel<8, true> : W == 16 ? (const void*)panel_kernel<16, true>
                                                                        : (const void*)panel_kernel<32, true>;
   return W == 8 ? (const void*)panel_kernel<8, false> : W == 16 ? (const void*)panel_kernel<16, false>
                                                                 : (const void*)panel_kernel<32, false>;
 }
+#endif
 static constexpr int MAX_CHUNKS = 8;
 static constexpr size_t LL_WORDS = PF_LL_WORDS;
 
@@ -232,10 +247,11 @@ static int ctx_get(DevCtx** out) {
                                   (int)(c.smem_optin - fa.sharedSizeBytes));
     };
     for (int W : {8, 16, 32})
-      for (bool cl : {false, true}) {
-        CK(allow(pf_fn(W, cl)));
-        if (cl) CK(cudaFuncSetAttribute(pf_fn(W, cl), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      }
+      for (bool cl : {false, true})
+        for (bool ex : {false, true}) {
+          CK(allow(pf_fn(W, cl, ex)));
+          if (cl) CK(cudaFuncSetAttribute(pf_fn(W, cl, ex), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        }
     CK(allow((const void*)swap_trsm_kernel<8>));
     CK(allow((const void*)swap_trsm_dmma_kernel<256, 32>));
     CK(allow((const void*)swap_trsm_dmma_kernel<256, 16>));
@@ -587,7 +603,7 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
       cfg.attrs = at;
       cfg.numAttrs = 1;
       void* args[] = {&p};
-      CK(cudaLaunchKernelExC(&cfg, pf_fn(W, true), args));
+      CK(cudaLaunchKernelExC(&cfg, pf_fn(W, true, opt.exact != 0), args));
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return PFLU_OK;
     }
@@ -612,7 +628,7 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
       int S_eff = (int)((rows + R - 1) / R);
       p.R = R;
       void* args[] = {&p};
-      CK(cudaLaunchCooperativeKernel(pf_fn(W, false), dim3(S_eff), dim3(PF_THREADS), args, smem, st));
+      CK(cudaLaunchCooperativeKernel(pf_fn(W, false, opt.exact != 0), dim3(S_eff), dim3(PF_THREADS), args, smem, st));
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return PFLU_OK;
     }

@@ -66,6 +66,7 @@ __device__ __forceinline__ unsigned long long key_ord(double k) {
 // lane receives the winner; returns the winning lane (for extra payload).  Rows are >= 0.
 __device__ __forceinline__ int warp_best(double& k, long long& r) {
   const unsigned full = 0xffffffffu;
+  __syncwarp();  // callers may arrive from lane-divergent code: reconverge before the collectives
   const unsigned long long u = key_ord(k);
   const unsigned hi = (unsigned)(u >> 32), lo = (unsigned)u;
   const unsigned mhi = __reduce_max_sync(full, hi);

@@ -203,7 +203,10 @@ struct PanelSmem {
 // CL = true:  the S <= 16 CTAs form one thread-block cluster; candidates and the diagonal row are
 //             pushed into every peer's shared memory with st.async completing on the peer's mbarrier
 //             (no polling, no L2 round trip), and grid syncs are cluster barriers.
-template <int W, bool CL>
+// EX: -1 = exact flag read at run time (p.exact, the shipped build); 0 / 1 = compiled in (the
+// specialisation that once returned wrong pivots on the singular golden case; built with
+// -DPFLU_PANEL_EXACT_T by tools/panel_hazard.sh to re-check it).
+template <int W, bool CL, int EX = -1>
 __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   extern __shared__ __align__(16) double pf_smem[];
   constexpr int LD = W + 1;
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   const int rec = 16 + 2 * W;  // [key line: key, row (16 words = 128 B)][data: 2W words]; 128-B aligned
   unsigned long long* sync_words = p.ll + PF_SBOX_OFFSET;  // [reader 256][writer 256][2 words]
   unsigned long long* mbox = p.ll + PF_MBOX_OFFSET;  // [2][reader 256][writer 256][4 words]
-  const bool exact = p.exact != 0;
+  const bool exact = EX < 0 ? p.exact != 0 : EX != 0;
   const int g_resync = p.resync;
   const bool prof_on = p.prof != nullptr && tid == 0;
   long long prof_t = clock64();
@@ -490,6 +493,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         p.piv[c] = (wkey > 0.0) ? prow : c;
         if (!(wkey > 0.0)) atomicMin(p.info, (unsigned long long)(c + 1));
       }
+      // Thread 0 diverged from its warp just above (piv / info stores).  Reconverge warp 0 explicitly
+      // before the warp collectives below: without it, the exact-as-template build let lane 0 reach
+      // the zero-pivot branch's cta_best on its own and take its own (key, row) as the CTA's winner
+      // (wrong pivot after every zero column; a hang of the grid kernel when CTAs then disagreed).
+      // Independent thread scheduling gives no reconvergence guarantee after a divergent branch;
+      // __syncwarp() is the documented one (tests/test_gpu_panel_stress.py, tools/panel_hazard.sh).
+      __syncwarp();
       if (!(wkey > 0.0)) {
         // exactly-zero pivot: column left untouched (_jit.py:171-174); next candidate from the tile
         ck = -3.0;

@@ -548,7 +548,7 @@ def lu_factor_local(a_loc, n: int, b: int = 256, lookahead: int = 1, exact: bool
 
 
 def local_columns_seeded(n: int, b: int, P: int, r: int, seed: int, dist_name: str = "uniform",
-                         chunk_rows: int = 1024):
+                         chunk_rows: int = 1024, diag_shift: float = 0.0):
     """Rank r's block-cyclic columns of the seeded BASELINE matrix (numpy default_rng(seed), row-major
     draw order), generated in row chunks so no rank ever holds the full n x n matrix."""
     import numpy as np
@@ -564,18 +564,28 @@ def local_columns_seeded(n: int, b: int, P: int, r: int, seed: int, dist_name: s
             w = min(b, n - j * b)
             out[r0:r1, c: c + w] = rows[:, j * b: j * b + w]
             c += w
+    if diag_shift:
+        c = 0
+        for j in blocks:
+            w = min(b, n - j * b)
+            for t in range(w):
+                out[j * b + t, c + t] += diag_shift
+            c += w
     return out
 
 
 # ---------------------------------------------------------------------------------------------
 # bench.py --gpus N (torchrun, one rank per GPU)
 
-def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
+def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak, configs=None, workload=None):
     import json
     import time
 
     import numpy as np
 
+    # the communicator log (nranks per communicator) stays on unless the caller chose otherwise
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if not dist.is_initialized():
         for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"), ("MASTER_ADDR", "127.0.0.1"),
                      ("MASTER_PORT", "29533")):
@@ -589,7 +599,11 @@ def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     n, b, la = args.n, args.b, args.lookahead
-    host_loc = local_columns_seeded(n, b, P, r, seed=3)  # 1/P of the matrix per rank
+    if torch.cuda.device_count() <= local:
+        raise RuntimeError(f"rank {r}: LOCAL_RANK {local} but only {torch.cuda.device_count()} CUDA device(s) visible")
+    cfg = getattr(args, "config", "c4")
+    _, seed, dist_name, _, shift = (configs or {}).get(cfg, (n, 3, "uniform", b, 0.0))
+    host_loc = local_columns_seeded(n, b, P, r, seed=seed, dist_name=dist_name, diag_shift=shift)  # 1/P per rank
     a0 = torch.from_numpy(host_loc).to(dev)
     a = torch.empty_like(a0)
     piv = torch.zeros(n, dtype=torch.int64, device=dev)
@@ -603,7 +617,7 @@ def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local) if r == 0 else None
+    clocks = ClockSampler(local)
     if clocks:
         clocks.start()
         time.sleep(0.3)
@@ -619,8 +633,13 @@ def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
     dist.barrier()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    launches = L.pflu_launch_count() - launches0
+    lt = torch.tensor([L.pflu_launch_count() - launches0], dtype=torch.int64, device=dev)
+    dist.all_reduce(lt)                      # whole job: every rank's kernel launches
+    launches = int(lt.item())
     clk = clocks.stop() if clocks else None
+    # every rank samples its own GPU's clocks; rank 0 reports them all
+    clk_all = [None] * P
+    dist.all_gather_object(clk_all, clk)
     ms_step = float(ms.item()) / args.steps
     value = lu_flops(n) / (ms_step * 1e-3) / 1e9
     peak, peak_src = fp64_peak()
@@ -650,14 +669,14 @@ def bench_dist(args, lu_flops, metric, unit, ClockSampler, fp64_peak):
             "metric": metric, "value": value, "unit": unit, "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C4: LUpp n={n} U[-1,1) numpy seed 3, b={b}, look-ahead {la}", "n": n, "b": b,
+            "config": {"workload": workload or f"C4: LUpp n={n} U[-1,1) numpy seed 3, b={b}, look-ahead {la}", "n": n, "b": b,
                        "lookahead": la, "parallelism": f"1-D block-cyclic columns over {P} GPUs, NCCL panel broadcast",
                        "l2": "inputs larger than L2; local columns restored by a D2D copy inside each step",
                        "fp64_peak_frac": value / 1e3 / (peak * P)},
             "roofline": {"bound": "tensor", "achieved": None, "peak": peak * P, "unit": "TFLOP/s",
                          "frac": value / 1e3 / (peak * P), "traffic": None, "peak_source": peak_src,
                          "note": "aggregate over ranks; per-kernel roofline is reported by the N=1 line"},
-            "clocks": clk, "e2e": e2e, "gpu_launches": launches, "cpu_baseline": None,
+            "clocks": clk, "clocks_per_rank": clk_all, "e2e": e2e, "gpu_launches": launches, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()

@@ -12,7 +12,8 @@ Outputs (committed):
                        float64 bytes), sha256 of the first 256 rows, info, timings
   configs_pivots.npz -- full 0-based pivot vectors for those configs (int32)
 
-Usage: REF_PKG_SRC=/tmp/refpkg/src python tests/golden/make_golden.py [small|c1|c2|c2s|c3 ...]
+Usage: REF_PKG_SRC=/tmp/refpkg/src python tests/golden/make_golden.py [small|c1|c2|c2s|c3|c4 ...]
+(GOLDEN_OUT=dir writes configs.json / configs_pivots.npz there instead; c4 takes ~50 min on 8 cores.)
 """
 from __future__ import annotations
 
@@ -49,6 +50,8 @@ def config_matrix(name: str) -> tuple[np.ndarray, int]:
         return a, 256
     if name == "c3":
         return np.random.default_rng(2).standard_normal((16384, 16384)), 256
+    if name == "c4":
+        return np.random.default_rng(3).uniform(-1.0, 1.0, size=(32768, 32768)), 256
     raise KeyError(name)
 
 
@@ -119,20 +122,25 @@ def gen_small(pool):
     print("small cases:", len([k for k in cases if k.endswith("__a")]))
 
 
+OUT = os.environ.get("GOLDEN_OUT", HERE)
+
+
 def gen_config(name, pool):
     a, b = config_matrix(name)
+    n = int(a.shape[0])
     f, piv, info, dt = run_ref_lu(a, b, pool, depth=1)
-    path = os.path.join(HERE, "configs.json")
+    del a
+    path = os.path.join(OUT, "configs.json")
     meta = json.load(open(path)) if os.path.exists(path) else {}
     meta[name] = {
-        "n": int(a.shape[0]), "b": b, "depth": 1, "info": info,
+        "n": n, "b": b, "depth": 1, "info": info,
         "sha256_factors": sha(f), f"sha256_rows_0_{PREFIX_ROWS}": sha(f[:PREFIX_ROWS]),
         "ref_seconds": round(dt, 2), "ref_threads": pool.t,
         "first_pivots": [int(p) for p in piv[:8]],
         "max_abs_L": float(np.max(np.abs(np.tril(f, -1)))),
     }
     json.dump(meta, open(path, "w"), indent=1, sort_keys=True)
-    pz = os.path.join(HERE, "configs_pivots.npz")
+    pz = os.path.join(OUT, "configs_pivots.npz")
     d = dict(np.load(pz)) if os.path.exists(pz) else {}
     d[name] = piv.astype(np.int32)
     np.savez_compressed(pz, **d)
