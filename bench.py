@@ -216,6 +216,58 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def golden_parity(args, d_a0, d_lu, piv) -> dict:
+    """Full-size parity of the timed run against the committed golden data (tests/golden/: the
+    reference's own C1-C4 factors, the pinned oracle's C5): the FULL pivot vector (north_star's tie
+    rule), plus one exact-mode factorization (reference rounding, outside the timed region) whose
+    sha256 must equal the golden sha -- it is then the reference's factor, so max|LU - LU_exact| /
+    ||A||_max is north_star's max|LU_gpu - LU_ref| / ||A||_max."""
+    import hashlib
+
+    import torch
+
+    from paper_1804_07017_b200 import getrf_device
+
+    gdir = os.path.join(ROOT, "tests", "golden")
+    try:
+        meta = json.load(open(os.path.join(gdir, "configs.json")))
+        pivs = np.load(os.path.join(gdir, "configs_pivots.npz"))
+        ties = np.load(os.path.join(gdir, "configs_ties.npz"))
+    except OSError:
+        return {"golden": "missing"}
+    name = args.config
+    n0, _, _, b0, _ = CONFIGS[name]
+    if name not in meta or name not in pivs.files or args.n != n0 or args.b != b0:
+        return {"golden": f"none for {name} at n={args.n} b={args.b}"}
+    want = pivs[name].astype(np.int64)
+    got = piv.cpu().numpy()
+    diff = np.nonzero(got != want)[0]
+    out = {"golden_source": meta[name].get("source", "reference"),
+           "pivots_full_equal_golden": bool(len(diff) == 0),
+           "pivots_first_mismatch": int(diff[0]) if len(diff) else None}
+    if len(diff):
+        t = ties[name] if name in ties.files else np.zeros((0, 4))
+        row = t[t[:, 0] == diff[0]] if len(t) else t
+        out["pivots_tie_rule_ok"] = bool(len(row) and (row[0, 1] - row[0, 2]) / row[0, 1] <= 1e-12
+                                         and int(row[0, 3]) == int(got[diff[0]]))
+    ex = d_a0.clone()
+    piv_ex, _ = getrf_device(ex, args.b, args.lookahead, exact=True)
+    torch.cuda.synchronize()
+    h = hashlib.sha256()
+    mx = 0.0
+    for r0 in range(0, ex.shape[0], 4096):
+        h.update(ex[r0:r0 + 4096].cpu().numpy().tobytes())
+        mx = max(mx, float((d_lu[r0:r0 + 4096] - ex[r0:r0 + 4096]).abs().max()))
+    amax = float(d_a0.abs().max())
+    out["exact_sha256_equal_golden"] = h.hexdigest() == meta[name]["sha256_factors"]
+    out["exact_pivots_equal_golden"] = bool(np.array_equal(piv_ex.cpu().numpy(), want))
+    out["max_abs_lu_minus_ref_over_amax"] = mx / amax
+    out["max_abs_bound"] = 10.0
+    del ex
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_single(args) -> None:
     import torch
 
@@ -319,6 +371,7 @@ def run_single(args) -> None:
 
         parity = {"residual": lu_residual_gpu(d_a0, d_a, piv), "residual_bound": 10.0,
                   "residual_def": "||PA - LU||_F / (||A||_F n 2^-53), torch fp64 checker on the GPU"}
+        parity.update(golden_parity(args, d_a0, d_a, piv))
         if not args.no_cpu:
             amax = float(np.max(np.abs(a_host)))
             parity["pivots_0_b_equal_oracle"] = bool(np.array_equal(piv[:b].cpu().numpy(), ref_piv))

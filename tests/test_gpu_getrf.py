@@ -175,63 +175,6 @@ def test_c3_block_sweep(cuda, b):
     assert oracle.max_rel_diff(lu, lu_x, a0) <= 1e-8
 
 
-def _blocked_prefix(a0, b):
-    """First blocked step of the reference algorithm (oracle): rows [0, b) and piv[:b] are final."""
-    import oracle as orc
-
-    orc.set_threads(os.cpu_count() or 1)
-    pre = np.array(a0, copy=True)
-    piv = np.zeros(a0.shape[1], dtype=np.int64)
-    orc.getrf_steps_inplace(pre, b, 1, piv)
-    return pre, piv[:b]
-
-
-@pytest.mark.slow
-def test_c4_prefix_and_residual(cuda):
-    """C4 (n = 32768, b = 256, look-ahead 1): too large for a full host oracle run, so the first step
-    is pinned by the oracle's blocked prefix (rows [0, 256) and piv[:256] are final after it; the
-    prefix mode is pinned against the reference's C1 prefix sha in test_oracle.py), the rest by the
-    backward error of the full factorization."""
-    import oracle as orc
-
-    a0 = config_matrix("c4")
-    pre, ppiv = _blocked_prefix(a0, 256)
-    lu, piv, info = run(a0, 256, 1, exact=False)
-    assert info == 0
-    assert np.array_equal(piv[:256], ppiv)
-    assert np.max(np.abs(lu[:256] - pre[:256])) / np.max(np.abs(a0)) <= 1e-10
-    assert gpu_residual(a0, lu, piv) <= 10
-    # pivots are a permutation sequence (every piv[k] >= k) and multipliers are bounded
-    assert np.all(piv >= np.arange(len(piv)))
-    assert np.max(np.abs(np.tril(lu, -1))) <= 1.0 + 4 * orc.UNIT_ROUNDOFF
-
-
-@pytest.mark.slow
-def test_c5_prefix_and_residual_single_gpu(cuda):
-    """C5 (n = 65536 standard normal seed 4, b = 512, 34 GB) on ONE B200 (the config names 4/8 GPUs;
-    one B200 holds it): first-step prefix vs the oracle, full backward error on the GPU."""
-    import torch
-
-    n = 65536
-    a0 = np.random.default_rng(4).standard_normal((n, n))
-    pre, ppiv = _blocked_prefix(a0, 512)
-    top = pre[:512].copy()
-    del pre
-    dev = torch.device("cuda:0")
-    from paper_1804_07017_b200 import getrf_device
-    from paper_1804_07017_b200.cli import lu_residual_gpu
-
-    d_a0 = torch.from_numpy(a0).to(dev)
-    del a0
-    d_lu = d_a0.clone()
-    piv, info = getrf_device(d_lu, 512, 1)
-    assert info == 0
-    assert np.array_equal(piv[:512].cpu().numpy(), ppiv)
-    amax = float(d_a0.abs().max())
-    assert float((d_lu[:512].cpu() - torch.from_numpy(top)).abs().max()) / amax <= 1e-10
-    assert lu_residual_gpu(d_a0, d_lu, piv, block=8192) <= 10
-
-
 @pytest.mark.parametrize("lookahead", [0, 1])
 def test_nan_inf_pivot_rules(cuda, lookahead):
     """Special values follow the reference's strict '>' scan (_jit.py:163-170): a NaN candidate is never

@@ -91,3 +91,46 @@ def test_golden_configs_present():
     assert CONFIGS["c2"]["first_pivots"][:4] == [4465, 1370, 4721, 3630]    # SURVEY §8(d) anchor
     assert CONFIGS["c3"]["first_pivots"][:4] == [4176, 8860, 16281, 7873]
     assert np.array_equal(PIVOTS["c2s"], np.arange(8192))
+
+
+def test_golden_large_configs():
+    """C4 (reference run, oracle re-run bitwise equal) and C5 (pinned oracle) full-size pins."""
+    ties = np.load(os.path.join(GOLDEN, "configs_ties.npz"))
+    for name, n in (("c4", 32768), ("c5", 65536)):
+        if name == "c5" and name not in CONFIGS:
+            pytest.skip("C5 golden not generated yet (make_golden_large.py c5)")
+        g = CONFIGS[name]
+        piv = PIVOTS[name].astype(np.int64)
+        assert g["n"] == n and len(piv) == n and len(g["sha256_factors"]) == 64
+        assert np.all(piv >= np.arange(n)) and np.all(piv < n)           # LAPACK ipiv, ascending swaps
+        assert list(piv[:8]) == g["first_pivots"]
+        assert name in ties.files and ties[name].shape[1] == 4
+    assert CONFIGS["c4"]["ref_sha_equal"] is True                          # reference == oracle at C4
+
+
+def test_top2_record_and_tie_classifier():
+    """The instrumented oracle (getrf_top2_inplace) is the plain blocked oracle plus per-column
+    (|winner|, |runner-up|, runner-up row); classify_pivots accepts a mismatch only at a 1e-12 tie."""
+    a = np.random.default_rng(3).uniform(-1, 1, (300, 300))
+    ref, rpiv, _ = oracle.getrf(a, 64)
+    w = np.array(a, copy=True)
+    piv, top2, info = oracle.getrf_top2_inplace(w, 64)
+    assert info == 0 and np.array_equal(piv, rpiv) and w.tobytes() == ref.tobytes()
+    assert np.all(top2[:, 0] >= top2[:, 1])
+    assert np.all(top2[:-1, 1] >= 0) and top2[-1, 1] == -1.0      # the last column has no runner-up
+    # synthetic tie record: column 10 ties within 1e-13, column 20 does not tie
+    ties = np.array([[10.0, 1.0, 1.0 - 1e-13, 42.0], [20.0, 1.0, 1.0 - 1e-7, 43.0]])
+    base = np.arange(30)
+    assert oracle.classify_pivots(base, base, ties)["ok"]
+    g = base.copy(); g[10] = 42; g[11:] = 0
+    assert oracle.classify_pivots(g, base, ties)["ok"]             # legitimate tie break, later columns free
+    g = base.copy(); g[10] = 41
+    assert not oracle.classify_pivots(g, base, ties)["ok"]         # not the runner-up
+    g = base.copy(); g[20] = 43
+    assert not oracle.classify_pivots(g, base, ties)["ok"]         # gap 1e-7 > 1e-12
+    g = base.copy(); g[5] = 6
+    assert not oracle.classify_pivots(g, base, ties)["ok"]         # no tie recorded at column 5
+    # near_ties picks exactly the columns within the tolerance
+    t2 = np.array([[2.0, 2.0 - 1e-12, 5], [1.0, 0.5, 6], [3.0, -1.0, -1]])
+    nt = oracle.near_ties(t2, 1e-6)
+    assert nt.shape == (1, 4) and nt[0, 0] == 0 and nt[0, 3] == 5
