@@ -384,6 +384,49 @@ static int launch_gemm_tma(const GemmArgs& p, cudaStream_t st, bool* done) {
   return PFLU_OK;
 }
 
+// warp-specialised TMA GEMM (gemm_dmma_ws); same tensor maps as launch_gemm_tma with the box
+// height of the WS tile.  *done = false when the views do not meet TMA's alignment rules.
+template <class C>
+static int launch_gemm_ws(const GemmArgs& p, cudaStream_t st, bool* done) {
+  *done = false;
+  PfnEncodeTiled enc = tma_encoder();
+  if (!enc) return PFLU_OK;
+  if ((reinterpret_cast<uintptr_t>(p.a) & 15) || (reinterpret_cast<uintptr_t>(p.b) & 15) ||
+      (reinterpret_cast<uintptr_t>(p.c) & 15) || (p.lda & 1) || (p.ldb & 1) || (p.ldc & 1) ||
+      p.M >= (int64_t)1 << 31 || p.N >= (int64_t)1 << 31 || p.K >= (int64_t)1 << 31)
+    return PFLU_OK;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(gemm_dmma_ws<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  CUtensorMap ta, tb;
+  const cuuint32_t es[2] = {1, 1};
+  const cuuint64_t da[2] = {(cuuint64_t)p.K, (cuuint64_t)p.M}, sa[1] = {(cuuint64_t)p.lda * 8};
+  const cuuint32_t ba[2] = {8, (cuuint32_t)C::BM};
+  CUresult r = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p.a), da, sa, ba, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(PFLU_ERR_CUDA, "cuTensorMapEncodeTiled(A) failed: %d", (int)r);
+  const cuuint64_t db[2] = {(cuuint64_t)p.N, (cuuint64_t)p.K}, sb[1] = {(cuuint64_t)p.ldb * 8};
+  const cuuint32_t bb[2] = {8, (cuuint32_t)C::BK};
+  r = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p.b), db, sb, bb, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(PFLU_ERR_CUDA, "cuTensorMapEncodeTiled(B) failed: %d", (int)r);
+  const int64_t tm = (p.M + C::BM - 1) / C::BM, tn = (p.N + C::BN - 1) / C::BN;
+  if (tm * tn > INT_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "gemm grid too large");
+  TmaGemmArgs q;
+  q.c = p.c; q.ldc = p.ldc; q.M = p.M; q.N = p.N; q.K = p.K;
+  q.tiles_m = (int)tm; q.tiles_n = (int)tn;
+  gemm_dmma_ws<C><<<(unsigned)(tm * tn), C::THREADS, C::SMEM, st>>>(ta, tb, q);
+  *done = true;
+  return PFLU_OK;
+}
+// PFLU_GEMM_WS: 1 = WS1 (default, the production trailing update), 0 / 2 / 3 = the other ring
+// depths, -1 = the cp.async GEMM (gemm_dmma_t / PFLU_GEMM_VARIANT)
+static int g_gemm_ws = []() { const char* e = getenv("PFLU_GEMM_WS"); return e ? atoi(e) : 1; }();
+
 static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, const double* b, int64_t ldb,
                        int64_t M, int64_t N, int64_t K, bool exact, cudaStream_t st, int pgrid = 0) {
   if (M <= 0 || N <= 0 || K <= 0) return PFLU_OK;
@@ -403,7 +446,14 @@ static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, con
     else gemm_exact_kernel<1><<<grid, GM_THREADS, GM_SMEM, st>>>(p);
   } else {
     bool done = false;
-    if (g_gemm_tma) CKR(launch_gemm_tma<GV6>(p, st, &done));
+    switch (g_gemm_ws) {
+      case 0: CKR(launch_gemm_ws<WS0>(p, st, &done)); break;
+      case 1: CKR(launch_gemm_ws<WS1>(p, st, &done)); break;
+      case 2: CKR(launch_gemm_ws<WS2>(p, st, &done)); break;
+      case 3: CKR(launch_gemm_ws<WS3>(p, st, &done)); break;
+      default: break;
+    }
+    if (!done && g_gemm_tma) CKR(launch_gemm_tma<GV6>(p, st, &done));
     if (!done) switch (g_gemm_variant) {
       case 1: CKR(launch_gemm_t<GV1>(p, v2, st)); break;
       case 2: CKR(launch_gemm_t<GV2>(p, v2, st)); break;

@@ -523,6 +523,159 @@ __global__ void __launch_bounds__(C::THREADS, TmaCfg<C>::MINB)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Warp-specialised TMA GEMM (the production trailing update).  Per CTA: warpgroup 0 = the producer
+// (setmaxnreg.dec; one elected thread streams the A / B stages with cp.async.bulk.tensor into an
+// ST-deep ring of full / empty mbarriers), warpgroup 1 = four DMMA consumer warps of 64 x 32
+// (setmaxnreg.inc) that only wait on "full", read fragments and release the slot on "empty".  Two
+// CTAs per SM: one CTA's C prologue / epilogue overlaps the other's main loop, and the block
+// scheduler can hand SMs to the concurrent panel kernel as tiles retire (the look-ahead's
+// malleability).  Operand layout and the conflict-free k permutation are those of gemm_dmma_tma.
+template <int BM_, int BN_, int BK_, int ST_>
+struct WsCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, ST = ST_;
+  static constexpr int WM = 2, WN = 2, TM = BM / WM, TN = BN / WN, FM = TM / 8, FN = TN / 8;
+  static constexpr int CONSUMERS = WM * WN * 32;
+  static constexpr int THREADS = CONSUMERS + 128;  // + the producer warpgroup
+  static constexpr int ABOX = BM * 8, BBOX = BK * 8;
+  static constexpr int STAGE = BM * BK + BK * BN;            // doubles
+  static constexpr int SMEM = ST * STAGE * 8 + 2 * ST * 8;   // + full / empty barriers
+  static constexpr int PRODUCER_REGS = 24, CONSUMER_REGS = 232;  // 128 x (24 + 232) = 2 CTAs/SM x 32K
+  static_assert(BK % 8 == 0 && BN % 8 == 0 && TN % 8 == 0 && TM % 8 == 0, "8-wide boxes");
+  static_assert(2 * SMEM <= 227 * 1024, "two CTAs per SM");
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 2)
+    gemm_dmma_ws(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, TmaGemmArgs p) {
+  extern __shared__ __align__(1024) double ws_smem[];
+  double* sm = ws_smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ws_smem + C::ST * C::STAGE);
+  uint64_t* empty = full + C::ST;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int tm, tn;
+  tile_coords(blockIdx.x, p.tiles_m, p.tiles_n, tm, tn);
+  const int m0 = tm * C::BM, n0 = tn * C::BN;
+  const int KT = (int)((p.K + C::BK - 1) / C::BK);
+  if (tid == 0) {
+    for (int s = 0; s < C::ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::CONSUMERS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp < 4) {
+    // ---- producer warpgroup: one thread issues every stage, the others retire
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PRODUCER_REGS));
+    if (warp == 0 && lane == 0) {
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % C::ST;
+        if (kt >= C::ST) mbar_wait(&empty[s], (unsigned)((kt / C::ST - 1) & 1));
+        double* st = sm + s * C::STAGE;
+        mbar_expect_tx(&full[s], (unsigned)(C::STAGE * 8));
+        const int k0 = kt * C::BK;
+#pragma unroll
+        for (int kb = 0; kb < C::BK / 8; ++kb) tma_load_2d(st + kb * C::ABOX, &ta, k0 + kb * 8, m0, &full[s]);
+#pragma unroll
+        for (int nb = 0; nb < C::BN / 8; ++nb)
+          tma_load_2d(st + C::BM * C::BK + nb * C::BBOX, &tb, n0 + nb * 8, k0, &full[s]);
+      }
+    }
+    return;
+  }
+  // ---- consumer warpgroup
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CONSUMER_REGS));
+  const int cw = warp - 4;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = cw / C::WN, wn = cw % C::WN;
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i) {
+    const int64_t row = m0 + wm * C::TM + i * 8 + g;
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) {
+      const int64_t col = n0 + wn * C::TN + j * 8 + 2 * t;
+      const double* cp = p.c + row * p.ldc + col;
+      if (row < p.M && col + 1 < p.N) {
+        const double2 v = *reinterpret_cast<const double2*>(cp);
+        acc[i][j][0] = v.x;
+        acc[i][j][1] = v.y;
+      } else {
+        acc[i][j][0] = (row < p.M && col < p.N) ? cp[0] : 0.0;
+        acc[i][j][1] = (row < p.M && col + 1 < p.N) ? cp[1] : 0.0;
+      }
+    }
+  }
+  // fragment offsets: see gemm_dmma_tma (k slot of thread t in quad q of an 8-group:
+  // kl = 2q + (t & 1) + 4 (t >> 1); 64-byte swizzle chunk = (kl >> 1) ^ ((row >> 1) & 3))
+  const int tlo = t & 1, thi = t >> 1;
+  const int a_base = (wm * C::TM + g) * 8 + tlo;
+  const int b_base = (wn * C::TN / 8) * C::BBOX + (g & 1);
+  int xa[2], xb[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int h2 = q + 2 * thi;
+    xa[q] = ((h2 ^ (g >> 1)) << 1);
+    xb[q] = (2 * q + tlo + 4 * thi) * 8 + (((g >> 1) ^ h2) << 1);
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % C::ST;
+    mbar_wait(&full[s], (unsigned)((kt / C::ST) & 1));
+    const double* cA = sm + s * C::STAGE + a_base;
+    const double* cB = sm + s * C::STAGE + C::BM * C::BK + b_base;
+#pragma unroll
+    for (int kb = 0; kb < C::BK / 8; ++kb) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        double af[C::FM], bf[C::FN];
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i) af[i] = cA[kb * C::ABOX + i * 64 + xa[q]];
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) bf[j] = -cB[j * C::BBOX + kb * 64 + xb[q]];
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    }
+    // release the slot to the producer's next TMA write: the fragment reads above are generic-proxy
+    // loads that the compiler issues ahead of their DMMAs (and of this arrive), the refill is an
+    // async-proxy write -- order them across proxies first (without the fence, the refill overwrote
+    // slots still being read: random wrong 8-row groups with 4+ stages)
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i) {
+    const int64_t row = m0 + wm * C::TM + i * 8 + g;
+    if (row >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) {
+      const int64_t col = n0 + wn * C::TN + j * 8 + 2 * t;
+      double* cp = p.c + row * p.ldc + col;
+      if (col + 1 < p.N) {
+        *reinterpret_cast<double2*>(cp) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else if (col < p.N) {
+        cp[0] = acc[i][j][0];
+      }
+    }
+  }
+}
+
+// measured at the C4 step-0 shape 32512 x 32512 x 256 (tools/gemm_ws_probe.py, profiles/r05_gemm_ws.log):
+// WS1 35.4 TFLOP/s (production), WS2 35.2, WS0 35.0, WS3 34.3; cp.async GV6 33.7.  An L2 prefetch of
+// the C tile by the idle producer warps made WS1 / WS0 slower (34.1 / 33.8).
+using WS0 = WsCfg<128, 64, 16, 4>;  // 4 stages of K = 16 (24 KB each), 2 CTAs/SM
+using WS1 = WsCfg<128, 64, 32, 2>;  // 2 stages of K = 32 (48 KB each) -- production
+using WS2 = WsCfg<128, 64, 16, 3>;  // 3 stages of K = 16
+using WS3 = WsCfg<128, 64, 8, 8>;   // 8 stages of K = 8
+
 // variants swept by tools/gemm_once.py (PFLU_GEMM_VARIANT); the production choice is GV6
 // (K stage 32 double-buffered: 33.6 TFLOP/s at the C4 step-0 shape vs 32.4 for GV0)
 using GV0 = GemmCfg<128, 64, 16, 4, 2, 2>;   // 4 warps of 64x32, 2 CTAs/SM
