@@ -384,7 +384,7 @@ def run_single(args) -> None:
                    "n": n, "b": b, "lookahead": la, "parallelism": "single GPU",
                    "l2": "inputs (8.6 GB) larger than L2; pristine matrix restored by a D2D copy inside each step",
                    "fp64_peak_frac": value / 1e3 / peak},
-        "roofline": {"bound": "tensor", "kernel": "gemm_dmma_t<128x64x32, 2 stages> (trailing update A22 -= L21*U12)",
+        "roofline": {"bound": "tensor", "kernel": "gemm_dmma_ws<128x64x32, 2-stage TMA ring, producer warpgroup + 4 DMMA warps> (trailing update A22 -= L21*U12)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": peak_src, "traffic_source": traffic_src,

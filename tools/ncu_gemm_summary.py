@@ -8,7 +8,9 @@ import sys
 
 rep, out, kernel, shape = sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4]
 M, N, K = (int(x) for x in shape.split("x"))
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = open(rep).read() if rep.endswith(".csv") else \
+    subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = raw[raw.index('"ID"'):] if '"ID"' in raw else raw
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
 want = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum", "launch__grid_size",
