@@ -1,8 +1,8 @@
 # In-tree build of libpflu.so (sm_100a) and the CPU oracle; __graft_entry__.build() does the same.
 NVCC ?= /usr/local/cuda/bin/nvcc
-NVFLAGS = -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -std=c++17 --shared -Xcompiler -fPIC
+NVFLAGS = -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -std=c++17 --shared -Xcompiler -fPIC -ldl
 SRC = paper_1804_07017_b200/csrc/pflu.cu
-HDR = paper_1804_07017_b200/csrc/pflu_kernels.cuh paper_1804_07017_b200/csrc/pflu_panel.cuh paper_1804_07017_b200/csrc/pflu_gemm.cuh paper_1804_07017_b200/csrc/pflu_qr.cuh include/pflu.h
+HDR = paper_1804_07017_b200/csrc/pflu_mg.cuh paper_1804_07017_b200/csrc/pflu_kernels.cuh paper_1804_07017_b200/csrc/pflu_panel.cuh paper_1804_07017_b200/csrc/pflu_gemm.cuh paper_1804_07017_b200/csrc/pflu_qr.cuh include/pflu.h
 
 all: paper_1804_07017_b200/libpflu.so oracle/liboracle.so
 

@@ -25,6 +25,8 @@
  *   pflu_trsm                       <- trsm_llnu (kernels.py:225-246; _jit.py:104-113)
  *   pflu_gemm_update                <- the gemm(A22, A21, -A12) of _update_columns
  *                                      (factor.py:278-285; kernels.py:173-218; _jit.py:54-80)
+ *   pflu_init / pflu_getrf_mg /     <- the same dmf_la / dmf_mtb call on every GPU of the node
+ *   pflu_finalize                      (optional init/finalize holding the comms)
  */
 #ifndef PFLU_H
 #define PFLU_H
@@ -58,6 +60,7 @@ typedef struct pflu_options {
 #define PFLU_TRACE_TU_L 2 /* update of panel k+1's columns (lookahead 1) */
 #define PFLU_TRACE_TU_R 3 /* remaining trailing update (lookahead 1)     */
 #define PFLU_TRACE_GEMM 4 /* the DMMA GEMM inside TU / TU_R (roofline)   */
+#define PFLU_TRACE_BCAST 5 /* multi-GPU: receipt of step k's panel + pivots (pflu_getrf_mg) */
 typedef struct pflu_trace_event {
   int32_t label;
   int32_t k;
@@ -80,6 +83,33 @@ int pflu_device_count(void);
  * The device copy is a grow-only workspace kept for the next call (see pflu_release_workspace). */
 int pflu_getrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int lookahead,
                int64_t* ipiv, int64_t* info, const pflu_options* opt);
+
+/* ---------------------------------------------------------------------------------------------
+ * Multi-GPU: one process, P devices, one host thread per rank.
+ * Reference interface replaced: the in-process dmf_la / dmf_mtb call (factor.py:455-456, 382-383)
+ * reaching every GPU of the node.  1-D block-cyclic columns (block j on rank j % P), per step ONE
+ * message (the owner's factored (n - kb) x b panel + its pivots) sent with ncclBroadcast over
+ * NVLink (communicators from ncclCommInitAll; NCCL is dlopen'ed, not linked), look-ahead 1 across
+ * ranks.  Ranks that share a device (tests on one GPU) exchange by device-to-device copies. */
+
+/* Create (or re-create) the P-rank context: ranks on devices[0 .. P) (NULL: devices 0 .. P-1; a
+ * device may repeat -- then the copy transport is used).  Holds the NCCL communicators, per-rank
+ * streams and grow-only workspaces until pflu_finalize. */
+int pflu_init(int n_gpus, const int* devices);
+/* Destroy the communicators and free every rank's workspace. */
+int pflu_finalize(void);
+/* Ranks of the current multi-GPU context (0 if none); 1 if it uses NCCL, 0 for the copy transport. */
+int pflu_mg_size(void);
+int pflu_mg_uses_nccl(void);
+/* Block-cyclic bookkeeping (host only): columns rank r of P stores for an n x n matrix, block b. */
+int64_t pflu_mg_local_cols(int64_t n, int64_t b, int n_gpus, int rank);
+
+/* Whole factorization of a square HOST matrix (n x n row-major, lda >= n, overwritten with L\U) on
+ * n_gpus ranks; ipiv int64[n] host.  n_gpus == 1 is pflu_getrf (unless PFLU_MG_FORCE=1); n_gpus > 1
+ * uses the current pflu_init context when it has n_gpus ranks, else creates one on devices
+ * 0 .. n_gpus-1.  trace (optional): rank 0's PF / TU_L / TU_R (TU at look-ahead 0) / BCAST records. */
+int pflu_getrf_mg(double* a, int64_t n, int64_t lda, int64_t b, int lookahead, int n_gpus, int64_t* ipiv,
+                  int64_t* info, const pflu_options* opt, pflu_trace_event* trace, int trace_cap, int* trace_len);
 
 /* Frees pflu_getrf's device workspace (synchronizes the device). */
 int pflu_release_workspace(void);

@@ -5,7 +5,8 @@ A from-scratch sm_100a implementation of the hot path of the reference package `
 (depth 0), and the Kind.QR (Householder) factorization of the same drivers.  Compute runs only in libpflu.so (C ABI: include/pflu.h); see DESIGN.md.
 """
 from .api import (CacheConfig, Kind, LuOutput, Matrix, Strategy, TraceEvent, dmf_la, dmf_mtb, flops,
-                  getrf_device, getrf_host, lu_factor, QrOutput, geqrf_device, geqrf_host, qr_factor)
+                  getrf_device, getrf_host, lu_factor, QrOutput, geqrf_device, geqrf_host, qr_factor,
+                  init_gpus, finalize_gpus, getrf_mg)
 from . import _lib
 
 __version__ = "0.1.0"
@@ -13,5 +14,5 @@ __version__ = "0.1.0"
 __all__ = [
     "CacheConfig", "Kind", "LuOutput", "Matrix", "Strategy", "TraceEvent", "dmf_la", "dmf_mtb", "flops",
     "getrf_device", "getrf_host", "lu_factor", "QrOutput", "geqrf_device", "geqrf_host", "qr_factor",
-    "__version__",
+    "init_gpus", "finalize_gpus", "getrf_mg", "__version__",
 ]

@@ -17,7 +17,7 @@ PFLU_ERR_CUDA = 1
 PFLU_ERR_NOMEM = 2
 PFLU_ERR_UNSUPPORTED = 3
 
-TRACE_LABELS = {0: "PF", 1: "TU", 2: "TU_L", 3: "TU_R", 4: "GEMM"}
+TRACE_LABELS = {0: "PF", 1: "TU", 2: "TU_L", 3: "TU_R", 4: "GEMM", 5: "BCAST"}
 
 #: every symbol include/pflu.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
@@ -26,6 +26,7 @@ EXPORTS = (
     "pflu_trsm", "pflu_gemm_update", "pflu_info_reset", "pflu_info_read", "pflu_pivot_plan",
     "pflu_swap_trsm_plan", "pflu_copy2d", "pflu_release_workspace", "pflu_diag_inv", "pflu_swap_trsm_inv",
     "pflu_geqrf", "pflu_geqrf_device", "pflu_qr_panel", "pflu_larft", "pflu_apply_block_reflector",
+    "pflu_init", "pflu_finalize", "pflu_mg_size", "pflu_mg_uses_nccl", "pflu_mg_local_cols", "pflu_getrf_mg",
 )
 
 
@@ -112,6 +113,20 @@ def load():
         L.pflu_larft.argtypes = [_vp, _i64, _i64, _i64, _pd, _pd, _i64, _vp]
         L.pflu_apply_block_reflector.restype = ctypes.c_int
         L.pflu_apply_block_reflector.argtypes = [_vp, _i64, _i64, _i64, _pd, _vp, _i64, _i64, _vp]
+        L.pflu_init.restype = ctypes.c_int
+        L.pflu_init.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.pflu_finalize.restype = ctypes.c_int
+        L.pflu_finalize.argtypes = []
+        L.pflu_mg_size.restype = ctypes.c_int
+        L.pflu_mg_size.argtypes = []
+        L.pflu_mg_uses_nccl.restype = ctypes.c_int
+        L.pflu_mg_uses_nccl.argtypes = []
+        L.pflu_mg_local_cols.restype = ctypes.c_int64
+        L.pflu_mg_local_cols.argtypes = [_i64, _i64, ctypes.c_int, ctypes.c_int]
+        L.pflu_getrf_mg.restype = ctypes.c_int
+        L.pflu_getrf_mg.argtypes = [_vp, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp, _pi64,
+                                    ctypes.POINTER(Options), ctypes.POINTER(TraceEvent), ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_int)]
         _lib = L
         return L
 

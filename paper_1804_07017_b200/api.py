@@ -198,6 +198,63 @@ def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int
     return piv, int(info.value)
 
 
+def init_gpus(n_gpus: int, devices=None) -> None:
+    """pflu_init: hold a multi-GPU context (NCCL communicators, per-rank streams and workspaces) for
+    ``n_gpus`` ranks on ``devices`` (default 0 .. n_gpus-1; a repeated device makes ranks share it
+    and exchange by copies -- the single-GPU test setup)."""
+    L = _lib.load()
+    devs = list(range(n_gpus)) if devices is None else [int(d) for d in devices]
+    if len(devs) != n_gpus:
+        raise ValueError("devices must list one device per rank")
+    arr = (ctypes.c_int * n_gpus)(*devs)
+    _lib.check(L.pflu_init(int(n_gpus), arr), "pflu_init")
+
+
+def finalize_gpus() -> None:
+    """pflu_finalize: destroy the multi-GPU context."""
+    _lib.check(_lib.load().pflu_finalize(), "pflu_finalize")
+
+
+def getrf_mg(a: np.ndarray, b: int, lookahead: int, n_gpus: int, exact: bool = False, trace=None):
+    """pflu_getrf_mg on a square row-major float64 HOST array (in place).  Returns (piv, info);
+    ``trace`` (a list) receives rank 0's PF / TU_L / TU_R / TU / BCAST records."""
+    L = _lib.load()
+    n = a.shape[0]
+    if a.ndim != 2 or a.shape[1] != n or a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise ValueError("the multi-GPU path factors square row-major float64 matrices")
+    piv = np.empty(n, dtype=np.int64)
+    info = ctypes.c_int64(0)
+    opt = _lib.options(exact=exact)
+    tbuf, tcap, tlen = None, 0, ctypes.c_int(0)
+    if trace is not None:
+        tcap = 8 * (-(-n // max(1, min(b, n)))) + 32
+        tbuf = (_lib.TraceEvent * tcap)()
+    rc = L.pflu_getrf_mg(a.ctypes.data, n, a.strides[0] // 8, int(b), int(lookahead), int(n_gpus),
+                         piv.ctypes.data, ctypes.byref(info), ctypes.byref(opt), tbuf, tcap, ctypes.byref(tlen))
+    _lib.check(rc, "pflu_getrf_mg")
+    if trace is not None:
+        for i in range(tlen.value):
+            e = tbuf[i]
+            lab = _lib.TRACE_LABELS.get(e.label, str(e.label))
+            trace.append(TraceEvent(lab, int(e.k), e.k + 1 if lab == "TU_L" else None, e.start_ms * 1e-3,
+                                    e.end_ms * 1e-3, None, float(e.flop)))
+    return piv, int(info.value)
+
+
+def _lu_factor_mg(a, b, lookahead, n_gpus, exact, return_info, overwrite_a):
+    arr = np.asarray(a.cpu().numpy() if _is_torch(a) else a)
+    if arr.ndim != 2 or arr.shape[0] != arr.shape[1]:
+        raise ValueError("the multi-GPU path factors square matrices")
+    if overwrite_a and arr is a and arr.dtype == np.float64 and arr.flags.c_contiguous and arr.flags.writeable:
+        work = arr
+    else:
+        work = np.array(arr, dtype=np.float64, order="C", copy=True)
+    piv, info = getrf_mg(work, b, lookahead, n_gpus, exact=exact)
+    if info:
+        warnings.warn(f"exactly singular: zero pivot in column {info} (1-based)", RuntimeWarning, stacklevel=3)
+    return (work, piv, info) if return_info else (work, piv)
+
+
 def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a: bool = True,
               exact: bool = False, return_info: bool = False, panel_ctas: int = 0, panel_kernel: int = 0):
     """Blocked right-looking LU with partial pivoting on the B200.
@@ -206,8 +263,10 @@ def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a:
     pflu_getrf) or a CUDA torch tensor (device buffers, current stream).  ``lookahead`` 1 is the
     reference's dmf_la, 0 its dmf_mtb.  ``exact=True`` reproduces the reference's rounding in
     every update (bitwise-equal factors); the default runs the trailing update on DMMA tensor
-    cores.  ``n_gpus > 1`` runs the 1-D block-cyclic multi-GPU driver (requires an initialised
-    torch.distributed NCCL process group with one rank per GPU).  ``panel_kernel`` forces the
+    cores.  ``n_gpus > 1`` runs the 1-D block-cyclic multi-GPU driver: inside an initialised
+    torch.distributed group of several processes (one rank per GPU) the torch.distributed driver,
+    otherwise -- one process, as the reference's in-process call -- pflu_getrf_mg over n_gpus
+    devices (NCCL broadcast per step).  ``panel_kernel`` forces the
     panel factorization of every step (0 automatic, 1 cooperative grid, 2 cluster, 3 recursive).
 
     Returns ``(lu, piv)`` (``(lu, piv, info)`` with ``return_info``): packed unit-lower L below
@@ -218,9 +277,15 @@ def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a:
     if b < 1:
         raise ValueError("block size must be >= 1")
     if n_gpus > 1:
-        from .dist import lu_factor_dist
+        import torch.distributed as tdist
 
-        return lu_factor_dist(a, b=b, lookahead=lookahead, exact=exact, return_info=return_info)
+        if tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() > 1:
+            # one process per GPU (torchrun): the torch.distributed driver
+            from .dist import lu_factor_dist
+
+            return lu_factor_dist(a, b=b, lookahead=lookahead, exact=exact, return_info=return_info)
+        # one process, n_gpus devices: the C ABI's multi-GPU driver (pflu_getrf_mg, NCCL)
+        return _lu_factor_mg(a, b, lookahead, n_gpus, exact, return_info, overwrite_a)
     if _is_torch(a):
         import torch
 

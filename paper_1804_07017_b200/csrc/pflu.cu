@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -91,7 +92,7 @@ static std::atomic<long long> g_launches{0};
 static unsigned long long* g_prof = nullptr;  // device buffer for panel-kernel phase clocks (tools only)
 static int g_pf_cap = []() { const char* e = getenv("PFLU_PANEL_CAP"); return e ? atoi(e) : 32; }();
 static int g_gemm_variant = []() { const char* e = getenv("PFLU_GEMM_VARIANT"); return e ? atoi(e) : 0; }();
-static DevCtx* g_dc = nullptr;  // context of the current call (set by ctx_get)
+static thread_local DevCtx* g_dc = nullptr;  // context of the current call (set by ctx_get)
 static int g_leaf = []() { const char* e = getenv("PFLU_LEAF"); return e ? atoi(e) : 0; }();
 // cluster panel: max CTAs per cluster (0 = LL kernel only), min rows per CTA, max panel rows
 static int g_cluster = []() { const char* e = getenv("PFLU_CLUSTER"); return e ? atoi(e) : 16; }();
@@ -174,7 +175,8 @@ struct Tracer {
   }
 };
 
-static std::mutex g_mu;
+static std::mutex g_mu;      // one public call at a time (the library is not re-entrant)
+static std::mutex g_ctx_mu;  // device-context creation (pflu_getrf_mg drives devices from several threads)
 static DevCtx g_ctx[64];
 
 static constexpr int PF_MAX_CTAS = PF_THREADS;
@@ -208,6 +210,8 @@ static int ctx_get(DevCtx** out) {
   CK(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return set_err(PFLU_ERR_UNSUPPORTED, "device index %d", dev);
   DevCtx& c = g_ctx[dev];
+  std::unique_lock<std::mutex> init_lock(g_ctx_mu, std::defer_lock);
+  if (!c.ready) init_lock.lock();  // several host threads may drive one device (pflu_getrf_mg)
   if (!c.ready) {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, dev));
@@ -286,7 +290,10 @@ static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t
 
 template <class C>
 static int launch_gemm_t(const GemmArgs& p0, bool v2, cudaStream_t st) {
-  static bool attr = false;
+  static bool attr_dev[64] = {};
+  int attr_d = 0;
+  CK(cudaGetDevice(&attr_d));
+  bool& attr = attr_dev[attr_d & 63];
   if (!attr) {
     CK(cudaFuncSetAttribute(gemm_dmma_t<C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     CK(cudaFuncSetAttribute(gemm_dmma_t<C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -305,7 +312,10 @@ static int launch_gemm_t(const GemmArgs& p0, bool v2, cudaStream_t st) {
 // persistent launch: at most `ctas` CTAs (0 = SMs x resident CTAs per SM)
 template <class C, bool PREF = false>
 static int launch_gemm_p(DevCtx& dc, const GemmArgs& p0, bool v2, int ctas, cudaStream_t st) {
-  static bool attr = false;
+  static bool attr_dev[64] = {};
+  int attr_d = 0;
+  CK(cudaGetDevice(&attr_d));
+  bool& attr = attr_dev[attr_d & 63];
   if (!attr) {
     CK(cudaFuncSetAttribute(gemm_dmma_persistent<C, 1, PREF>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     CK(cudaFuncSetAttribute(gemm_dmma_persistent<C, 2, PREF>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -355,7 +365,10 @@ static int launch_gemm_tma(const GemmArgs& p, cudaStream_t st, bool* done) {
       (reinterpret_cast<uintptr_t>(p.c) & 15) || (p.lda & 1) || (p.ldb & 1) || (p.ldc & 1) ||
       p.M >= (int64_t)1 << 31 || p.N >= (int64_t)1 << 31 || p.K >= (int64_t)1 << 31)
     return PFLU_OK;
-  static bool attr = false;
+  static bool attr_dev[64] = {};
+  int attr_d = 0;
+  CK(cudaGetDevice(&attr_d));
+  bool& attr = attr_dev[attr_d & 63];
   if (!attr) {
     CK(cudaFuncSetAttribute(gemm_dmma_tma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, TmaCfg<C>::SMEM));
     attr = true;
@@ -395,7 +408,10 @@ static int launch_gemm_ws(const GemmArgs& p, cudaStream_t st, bool* done) {
       (reinterpret_cast<uintptr_t>(p.c) & 15) || (p.lda & 1) || (p.ldb & 1) || (p.ldc & 1) ||
       p.M >= (int64_t)1 << 31 || p.N >= (int64_t)1 << 31 || p.K >= (int64_t)1 << 31)
     return PFLU_OK;
-  static bool attr = false;
+  static bool attr_dev[64] = {};
+  int attr_d = 0;
+  CK(cudaGetDevice(&attr_d));
+  bool& attr = attr_dev[attr_d & 63];
   if (!attr) {
     CK(cudaFuncSetAttribute(gemm_dmma_ws<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
@@ -573,6 +589,8 @@ static int64_t pf_swap_doubles(int W, int w) {
 
 // can a cluster of S panel CTAs (W, full shared memory) be resident?  cached per (W, S)
 static int pf_cluster_ok(DevCtx& c, int W, int S, bool* ok) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   static int cache[3][PF_CL_MAX + 1];
   static bool init = false;
   if (!init) {
@@ -1050,6 +1068,7 @@ static int finish_info(DevCtx& c, cudaStream_t st, int64_t* info) {
 
 }  // namespace pflu
 
+#include "pflu_mg.cuh"
 #include "pflu_qr.cuh"
 
 using namespace pflu;
@@ -1210,6 +1229,56 @@ int pflu_getrf(double* a, int64_t m, int64_t n, int64_t lda, int64_t b, int look
   pflu_default_options(&o);
   if (opt) o = *opt;
   const int rc = getrf_host_impl(a, m, n, lda, b, lookahead, ipiv, info, o);
+  if (rc != PFLU_OK) cudaGetLastError();
+  return rc;
+}
+
+int pflu_init(int n_gpus, const int* devices) {
+  if (n_gpus < 1 || n_gpus > 64) return -1;
+  std::lock_guard<std::mutex> lk(g_mu);
+  const int rc = mg_init(n_gpus, devices);
+  if (rc != PFLU_OK) cudaGetLastError();
+  return rc;
+}
+
+int pflu_finalize(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return mg_finalize();
+}
+
+int pflu_mg_size(void) { return g_mg.P; }
+int pflu_mg_uses_nccl(void) { return g_mg.nccl ? 1 : 0; }
+
+int64_t pflu_mg_local_cols(int64_t n, int64_t b, int n_gpus, int rank) {
+  if (n < 0 || b < 1 || n_gpus < 1 || rank < 0 || rank >= n_gpus) return -1;
+  return mg_local_cols(n, b, n_gpus, rank);
+}
+
+int pflu_getrf_mg(double* a, int64_t n, int64_t lda, int64_t b, int lookahead, int n_gpus, int64_t* ipiv,
+                  int64_t* info, const pflu_options* opt, pflu_trace_event* trace, int trace_cap, int* trace_len) {
+  if (!a) return -1;
+  if (n < 1) return -2;
+  if (lda < n) return -3;
+  if (b < 1) return -4;
+  if (lookahead != 0 && lookahead != 1) return -5;
+  if (n_gpus < 1 || n_gpus > 64) return -6;
+  if (!ipiv) return -7;
+  if (std::min(b, n) > PLAN_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "block size %lld > %d", (long long)b, PLAN_MAX);
+  pflu_options o;
+  pflu_default_options(&o);
+  if (opt) o = *opt;
+  static const bool force = getenv("PFLU_MG_FORCE") && atoi(getenv("PFLU_MG_FORCE")) != 0;
+  if (trace_len) *trace_len = 0;
+  if (n_gpus == 1 && !force) {
+    const int rc = getrf_host_impl(a, n, n, lda, b, lookahead, ipiv, info, o);
+    if (rc != PFLU_OK) cudaGetLastError();
+    return rc;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  int dev0 = 0;
+  cudaGetDevice(&dev0);
+  const int rc = mg_getrf(a, n, lda, b, lookahead, n_gpus, ipiv, info, o, trace, trace_cap, trace_len);
+  cudaSetDevice(dev0);
   if (rc != PFLU_OK) cudaGetLastError();
   return rc;
 }

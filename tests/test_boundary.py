@@ -79,3 +79,25 @@ def test_no_device_fails_loudly():
         qr_factor(np.eye(8), b=4)
     with pytest.raises(RuntimeError):
         dmf_la(Matrix.zeros(8, 8), CacheConfig(b=4), None, Kind.QR)
+
+
+def test_mg_bookkeeping_matches_dist():
+    """pflu_mg_local_cols (the C++ multi-GPU driver's block-cyclic layout) == dist.local_cols (the
+    torch.distributed driver's), and the multi-GPU entry point validates its arguments on CPU."""
+    from paper_1804_07017_b200 import _lib, dist
+
+    L = _lib.load()
+    for n, b, P in [(1, 1, 1), (97, 16, 3), (2048, 128, 8), (32768, 256, 8), (65536, 512, 4), (48, 16, 4)]:
+        cols = [L.pflu_mg_local_cols(n, b, P, r) for r in range(P)]
+        assert cols == [dist.local_cols(n, b, P, r) for r in range(P)]
+        assert sum(cols) == n
+    assert L.pflu_mg_local_cols(10, 2, 2, 2) == -1
+    a = np.zeros((8, 8))
+    piv = np.zeros(8, dtype=np.int64)
+    info = ctypes.c_int64(0)
+    opt = _lib.options()
+    assert L.pflu_getrf_mg(None, 8, 8, 2, 1, 2, piv.ctypes.data, ctypes.byref(info), ctypes.byref(opt), None, 0, None) == -1
+    assert L.pflu_getrf_mg(a.ctypes.data, 8, 4, 2, 1, 2, piv.ctypes.data, ctypes.byref(info), ctypes.byref(opt), None, 0, None) == -3
+    assert L.pflu_getrf_mg(a.ctypes.data, 8, 8, 2, 2, 2, piv.ctypes.data, ctypes.byref(info), ctypes.byref(opt), None, 0, None) == -5
+    assert L.pflu_getrf_mg(a.ctypes.data, 8, 8, 2, 1, 0, piv.ctypes.data, ctypes.byref(info), ctypes.byref(opt), None, 0, None) == -6
+    assert L.pflu_init(0, None) == -1
