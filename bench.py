@@ -177,11 +177,95 @@ def cpu_sample(n: int, b: int, threads: int | None = None, cfg: str = "c4"):
             piv[:b].copy(), a[:b].copy())
 
 
+REF_SLAB = 4096  # columns of the bounded CPU sample: the first blocked step of the config's left n x 4096 slab
+
+
+def _import_reference():
+    """The UNMODIFIED reference package installed in baseline/_ref (pip --target); its
+    numba cache goes to /tmp, never into the tree.  Returns the module or None."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "panelforge")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/pflu_numba_cache")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import panelforge  # noqa: F401
+    except Exception:  # noqa: BLE001  (numba missing etc.: reported as unavailable)
+        return None
+    return panelforge
+
+
+def reference_step_sample(pf, pool, a: np.ndarray, b: int):
+    """The reference's OWN code for the first blocked step of dmf_mtb / dmf_la (factor.py:396-411:
+    _factor_panel + _update_columns with the full team) on the row-major n x slab array `a` (the
+    config matrix's left columns).  Returns (seconds, flops, pivots[:b], rows[:b])."""
+    from panelforge import CacheConfig, Kind, Matrix
+    from panelforge import factor as F
+    from panelforge.runtime import MalleableTeam
+
+    import oracle
+
+    n, slab = a.shape
+    m = Matrix.from_array(a)                       # column-major copy, outside the timer (bench.py:125-138)
+    piv = np.zeros(slab, dtype=np.int64)
+    tau = np.zeros(slab)
+    team = MalleableTeam(pool.t, max_size=pool.t) if pool.t > 1 else None
+    t0 = time.perf_counter()
+    pfac, _ = F._factor_panel(Kind.LU, m, 0, 0, b, piv, tau)
+    F._update_columns(Kind.LU, m, pfac, b, slab, CacheConfig(b=b), pool=pool, team=team)
+    dt = time.perf_counter() - t0
+    out = np.ascontiguousarray(m.array)
+    return dt, oracle.step_flops(n, slab, b, 0), piv[:b] - 1, out[:b]
+
+
+def reference_cpu(args) -> dict | None:
+    """cpu_baseline.reference_numba: the reference's own numba code timed on the host cores beside the
+    C port -- the first-step sample above (and the port on the same sample, bitwise-compared), plus
+    a full dmf_la factorization of C1.  None if the reference is not installed (baseline/_ref)."""
+    pf = _import_reference()
+    if pf is None:
+        return None
+    import oracle
+    from panelforge import CacheConfig, Kind, Matrix, Pool
+
+    cores = os.cpu_count() or 1
+    with Pool(cores) as pool:
+        warm = np.random.default_rng(0).uniform(-1, 1, (256, 256))
+        pf.dmf_la(Matrix.from_array(warm), CacheConfig(b=64), pool, Kind.LU)   # numba warm-up (bench.py:125)
+        slab = np.ascontiguousarray(config_matrix(args.config, args.n)[:, :REF_SLAB])
+        dt, fl, rpiv, rrows = reference_step_sample(pf, pool, slab, args.b)
+        a1 = config_matrix("c1")
+        t0 = time.perf_counter()
+        pf.dmf_la(Matrix.from_array(a1), CacheConfig(b=128), pool, Kind.LU)
+        t_c1 = time.perf_counter() - t0
+    oracle.set_threads(cores)
+    port = slab
+    ppiv = np.zeros(REF_SLAB, dtype=np.int64)
+    t0 = time.perf_counter()
+    oracle.getrf_steps_inplace(port, args.b, 1, ppiv)
+    t_port = time.perf_counter() - t0
+    return {"value": fl / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"reference panelforge (baseline/_ref, numba, Pool({cores})): first blocked step "
+                      f"(_factor_panel + _update_columns) of the {args.config.upper()} matrix's left "
+                      f"{args.n}x{REF_SLAB} slab, {fl / 1e9:.1f} GFLOP in {dt:.2f} s",
+            "port_same_sample_gflops": fl / t_port / 1e9,
+            "port_bitwise_equal_on_sample": bool(np.array_equal(rpiv, ppiv[:args.b]) and
+                                                 rrows.tobytes() == port[:args.b].tobytes()),
+            "c1_dmf_la_seconds": t_c1, "c1_dmf_la_gflops": lu_flops(2048) / t_c1 / 1e9}
+
+
 def run_reference(args) -> None:
-    """--impl reference: the reference algorithm's CPU implementation (oracle port) timed on the
-    host cores, on bounded samples of the same workload (the first blocked step of C4)."""
+    """--impl reference: the reference's CPU implementation timed on the host cores, on bounded
+    samples of the same workload.  With the reference installed (baseline/_ref) every step is ITS
+    OWN code for the first blocked step of the config matrix's left n x 4096 slab (reference
+    numba, Pool(all host threads)); otherwise the oracle port on the full first blocked step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        return
+    pf = _import_reference()
+    if pf is not None:
+        run_reference_numba(args, pf)
         return
     import oracle
 
@@ -266,6 +350,35 @@ def golden_parity(args, d_a0, d_lu, piv) -> dict:
     del ex
     torch.cuda.empty_cache()
     return out
+
+
+def run_reference_numba(args, pf) -> None:
+    from panelforge import CacheConfig, Kind, Matrix, Pool
+
+    cores = os.cpu_count() or 1
+    slab = np.ascontiguousarray(config_matrix(args.config, args.n)[:, :REF_SLAB])
+    times, fl = [], 0.0
+    with Pool(cores) as pool:
+        warm = np.random.default_rng(0).uniform(-1, 1, (256, 256))
+        pf.dmf_la(Matrix.from_array(warm), CacheConfig(b=64), pool, Kind.LU)
+        for it in range(args.warmup + args.steps):
+            dt, fl, _, _ = reference_step_sample(pf, pool, slab, args.b)
+            if it >= args.warmup:
+                times.append(dt)
+    tot = sum(times)
+    value = fl * len(times) / tot / 1e9
+    sample = (f"reference panelforge (baseline/_ref, numba, Pool({cores})): first blocked step "
+              f"(_factor_panel + _update_columns) of the {args.config.upper()} matrix's left {args.n}x{REF_SLAB} "
+              f"slab ({fl / 1e9:.1f} GFLOP) per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args), "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
 
 
 def run_single(args) -> None:
@@ -364,6 +477,8 @@ def run_single(args) -> None:
     parity = None
     if not args.no_cpu:
         cpu, ref_piv, ref_rows = cpu_sample(n, b, cfg=args.config)
+        if not args.no_ref_cpu:
+            cpu["reference_numba"] = reference_cpu(args)
     if not args.no_check:
         # parity of the timed run's own output (last step): the oracle's first blocked step (pivots
         # and factor rows [0, b) are final after it) and the full backward error on the GPU
@@ -591,6 +706,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip the parity check of the timed run's output")
+    ap.add_argument("--no-ref-cpu", action="store_true", help="skip timing the reference's own numba code")
     ap.add_argument("--dist", action="store_true", help="force the block-cyclic multi-GPU path (testing at N=1)")
     ap.add_argument("--kind", default="lu", choices=["lu", "qr"], help="qr: the Householder QR path (one GPU)")
     args = ap.parse_args()
