@@ -205,8 +205,59 @@ class CudaKernels:
 # ---------------------------------------------------------------------------------------------
 # the distributed driver
 
+class _Trace:
+    """PF / TU / TU_L / TU_R / BCAST records of one rank (the reference's trace hook, factor.py:104-122;
+    SURVEY.md §8(b) adds BCAST): CUDA-event pairs on the stream the work runs on, or host wall
+    clock for the CPU test backend."""
+
+    def __init__(self, kernels, out):
+        self.k = kernels
+        self.out = out
+        self.recs = []
+        self.cuda = getattr(kernels, "is_cuda", False)
+        self.t0 = self._stamp("P")
+
+    def _stamp(self, which):
+        if self.cuda:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(self.k.sP if which == "P" else self.k.sU)
+            return e
+        import time
+
+        return time.perf_counter()
+
+    def begin(self, label, k, which):
+        return (label, k, which, self._stamp(which))
+
+    def end(self, tok):
+        label, k, which, s = tok
+        self.recs.append((label, k, s, self._stamp(which)))
+
+    def finish(self):
+        from .api import TraceEvent
+
+        if self.cuda:
+            torch.cuda.synchronize()
+            rel = lambda e: self.t0.elapsed_time(e) * 1e-3  # noqa: E731
+        else:
+            rel = lambda t: t - self.t0  # noqa: E731
+        for label, k, s, e in self.recs:
+            self.out.append(TraceEvent(label, k, k + 1 if label == "TU_L" else None, rel(s), rel(e), None, 0.0))
+
+
+class _NoTrace:
+    def begin(self, *a):
+        return None
+
+    def end(self, tok):
+        pass
+
+    def finish(self):
+        pass
+
+
 def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, kernels=None, group=None,
-                       piv: torch.Tensor | None = None, row_sink=None):
+                       piv: torch.Tensor | None = None, row_sink=None, trace=None):
     """Factor the block-cyclic distributed n x n matrix in place.
 
     ``row_sink(r0, r1, events)`` (CUDA only, optional) is called once per step as soon as local rows
@@ -216,6 +267,7 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
     ``a_loc``: this rank's local columns (row-major, n rows, ``local_cols(n, b, P, rank)`` columns).
     Returns ``(piv, info)``: the full 0-based pivot vector (identical on every rank) and the
     1-based first zero-pivot column (0 if none), agreed over all ranks.
+    ``trace`` (a list, optional) receives this rank's PF / TU / TU_L / TU_R / BCAST records.
     """
     P = dist.get_world_size(group)
     r = dist.get_rank(group)
@@ -237,6 +289,7 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
     ev_bc = [kernels.event() for _ in range(2)]
     ev_tu = [kernels.event() for _ in range(2)]
     kernels.begin()
+    tr = _Trace(kernels, trace) if trace is not None else _NoTrace()
     with kernels.stream("P"):
         kernels.info_reset()
 
@@ -254,13 +307,17 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
         pv = msg[rows * bw:].view(torch.int64)
         if r == o:
             lc = local_col_of_block(k, b, P)
+            t = tr.begin("PF", k, "P")
             kernels.panel(a_loc, n, col0, lc, bw, piv)
+            tr.end(t)
             buf.copy_(a_loc[col0:, lc: lc + bw])
             pv.copy_(piv[col0: col0 + bw])
         if P > 1:
+            t = tr.begin("BCAST", k, "P")
             dist.broadcast(msg, src=o, group=group)  # one message per step: panel + pivots
             if r != o:
                 piv[col0: col0 + bw].copy_(pv)
+            tr.end(t)
         kernels.plan(piv, col0, bw, plans[k % 2])
         if fast:
             kernels.diag_inv(buf[:bw, :bw], invs[k % 2])
@@ -289,8 +346,10 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
         for k in range(nblk):
             with kernels.stream("P"):
                 buf = pf_pack_bcast(k)
+                t = tr.begin("TU", k, "P")
                 left_swaps(k)
                 update(k, buf, cols_before(k + 1), ncl)
+                tr.end(t)
                 if row_sink is not None:
                     e = kernels.event()
                     kernels.record(e, "P")
@@ -307,8 +366,10 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
             lo_r = cols_before(k + 2) if own_next else cols_before(k + 1)
             with kernels.stream("U"):
                 kernels.wait(ev_bc[k % 2], "U")
+                t = tr.begin("TU_R", k, "U")
                 update(k, bufs[k], lo_r, ncl)
                 left_swaps(k)
+                tr.end(t)
                 kernels.record(ev_tu[k % 2], "U")
             e_tl = None
             if nxt:
@@ -316,7 +377,9 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
                     if k > 0:
                         kernels.wait(ev_tu[(k - 1) % 2], "P")
                     if own_next:
+                        t = tr.begin("TU_L", k, "P")
                         update(k, bufs[k], cols_before(k + 1), cols_before(k + 2))
+                        tr.end(t)
                         if row_sink is not None:
                             e_tl = kernels.event()
                             kernels.record(e_tl, "P")
@@ -331,6 +394,7 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
             bufs.pop(k - 1, None)
     if kernels.is_cuda:
         kernels.join()
+    tr.finish()
     with kernels.stream("P"):
         info = kernels.info_read()
     if P > 1:

@@ -67,6 +67,48 @@ def test_block_cyclic_matches_reference_bitwise(tmp_path, world, n, b, lookahead
     assert lu.tobytes() == ref.tobytes()
 
 
+def _trace_worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from dist_oracle_backend import OracleKernels
+    from paper_1804_07017_b200 import dist as pd
+
+    n, b = 96, 16
+    a = np.random.default_rng(0).uniform(-1.0, 1.0, (n, n))
+    for la in (0, 1):
+        loc = pd.scatter_columns(torch.from_numpy(a), b, world, rank)
+        tr = []
+        pd.getrf_block_cyclic(loc, n, b, la, OracleKernels(), trace=tr)
+        np.save(os.path.join(out_dir, f"trace_{la}_{rank}.npy"),
+                np.array([(e.label, e.k, e.start, e.end) for e in tr], dtype=object), allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_block_cyclic_trace_records(tmp_path):
+    """The distributed driver's trace hook: every rank records BCAST for every step, PF for the
+    blocks it owns, TU_R (look-ahead 1) / TU (look-ahead 0) per step, TU_L where it owns block k+1."""
+    world = 2
+    mp.spawn(_trace_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for la in (0, 1):
+        for rank in range(world):
+            recs = np.load(tmp_path / f"trace_{la}_{rank}.npy", allow_pickle=True)
+            by = {}
+            for label, k, s_, e_ in recs:
+                by.setdefault(label, []).append(int(k))
+                assert e_ >= s_
+            assert sorted(by["BCAST"]) == list(range(6))
+            assert sorted(by["PF"]) == list(range(rank, 6, world))
+            if la == 0:
+                assert sorted(by["TU"]) == list(range(6))
+            else:
+                assert sorted(by["TU_R"]) == list(range(6))
+                assert sorted(by["TU_L"]) == [k for k in range(5) if (k + 1) % world == rank]
+
+
 def test_block_cyclic_singular_info(tmp_path):
     import oracle
 

@@ -181,3 +181,37 @@ def test_dist_cuda_qr(cuda, tmp_path, world, backend, n, b, lookahead):
     assert np.abs(tau - rtau).max() <= 1e-10
     back, orth = oracle.qr_residual(a, f, tau)
     assert back <= 10 and orth <= 10
+
+
+def _trace_worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1804_07017_b200 import dist as pd
+
+    dev = torch.device("cuda:0")
+    n, b = 1024, 128
+    a = np.random.default_rng(4).uniform(-1.0, 1.0, (n, n))
+    loc = pd.scatter_columns(torch.from_numpy(a), b, world, rank).to(dev)
+    tr = []
+    pd.getrf_block_cyclic(loc, n, b, 1, pd.CudaKernels(dev), trace=tr)
+    np.save(os.path.join(out_dir, f"tr_{rank}.npy"), np.array([(e.label, e.k, e.start, e.end) for e in tr],
+                                                              dtype=object), allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_dist_cuda_trace(cuda, tmp_path):
+    """CUDA-event trace of the distributed driver (2 ranks on cuda:0, gloo): PF on the owned blocks,
+    BCAST / TU_R on every step, TU_L where the rank owns block k+1; times non-negative, ordered."""
+    mp.spawn(_trace_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    for rank in range(2):
+        recs = np.load(tmp_path / f"tr_{rank}.npy", allow_pickle=True)
+        by = {}
+        for label, k, s_, e_ in recs:
+            by.setdefault(label, []).append(int(k))
+            assert 0 <= s_ <= e_
+        assert sorted(by["PF"]) == list(range(rank, 8, 2))
+        assert sorted(by["BCAST"]) == list(range(8)) and sorted(by["TU_R"]) == list(range(8))
