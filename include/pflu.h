@@ -51,7 +51,14 @@ typedef struct pflu_options {
                        cluster (DSMEM exchange; PFLU_ERR_UNSUPPORTED if the panel does not fit),
                        3 recursive: halves split down to 32-column leaves (persistent kernel), the
                        halves joined by swap+TRSM and a full-height DMMA GEMM */
-  int reserved[4];
+  int malleable;    /* look-ahead 1 trailing update (the reference's LA / LA_MB, runtime.py:99-113):
+                       0 dynamic: one CTA per GEMM tile, the block scheduler hands the panel's SMs
+                         back to pending tiles as soon as the panel kernel exits (default);
+                       1 LA: SM-partitioned -- a persistent GEMM on every SM but the ones the panel
+                         kernel occupies (recorded from PF(0)); those stay with the panel chain;
+                       2 LA_MB: as 1, and after PF(k+1) a join grid on the panel's SMs takes tiles of
+                         TU_R(k) from the same atomic tile queue (the panel worker rejoining the team) */
+  int reserved[3];
 } pflu_options;
 
 /* Trace record, one per timed task (labels as the reference's TraceEvent, factor.py:104-122). */

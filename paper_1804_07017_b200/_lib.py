@@ -32,7 +32,8 @@ EXPORTS = (
 
 class Options(ctypes.Structure):
     _fields_ = [("exact", ctypes.c_int), ("panel_ctas", ctypes.c_int),
-                ("leaf_width", ctypes.c_int), ("panel_kernel", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
+                ("leaf_width", ctypes.c_int), ("panel_kernel", ctypes.c_int), ("malleable", ctypes.c_int),
+                ("reserved", ctypes.c_int * 3)]
 
 
 class TraceEvent(ctypes.Structure):
@@ -145,11 +146,17 @@ def check(rc: int, what: str) -> None:
 PANEL_AUTO, PANEL_GRID, PANEL_CLUSTER, PANEL_RECURSIVE = 0, 1, 2, 3
 
 
-def options(exact: bool = False, panel_ctas: int = 0, leaf_width: int = 0, panel_kernel: int = PANEL_AUTO) -> Options:
+#: pflu_options.malleable: dynamic tile scheduling (default), SM-partitioned LA, LA_MB (join grid)
+SCHED_DYNAMIC, SCHED_LA, SCHED_LA_MB = 0, 1, 2
+
+
+def options(exact: bool = False, panel_ctas: int = 0, leaf_width: int = 0, panel_kernel: int = PANEL_AUTO,
+            malleable: int = SCHED_DYNAMIC) -> Options:
     o = Options()
     load().pflu_default_options(ctypes.byref(o))
     o.exact = 1 if exact else 0
     o.panel_ctas = int(panel_ctas)
     o.leaf_width = int(leaf_width)
     o.panel_kernel = int(panel_kernel)
+    o.malleable = int(malleable)
     return o

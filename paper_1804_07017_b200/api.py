@@ -151,14 +151,15 @@ def _is_torch(x) -> bool:
 
 
 def getrf_host(a: np.ndarray, b: int, lookahead: int, exact: bool = False, panel_ctas: int = 0,
-               panel_kernel: int = 0):
+               panel_kernel: int = 0, malleable: int = 0):
     """Factor a row-major C-contiguous float64 host array in place through pflu_getrf.
-    Returns (piv0 int64[n], info)."""
+    ``malleable``: the look-ahead-1 trailing-update schedule (pflu_options.malleable: 0 dynamic tiles,
+    1 SM-partitioned LA, 2 LA_MB = partition + join grid).  Returns (piv0 int64[n], info)."""
     L = _lib.load()
     m, n = a.shape
     piv = np.empty(n, dtype=np.int64)
     info = ctypes.c_int64(0)
-    opt = _lib.options(exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel)
+    opt = _lib.options(exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel, malleable=malleable)
     rc = L.pflu_getrf(a.ctypes.data, m, n, a.strides[0] // 8, int(b), int(lookahead), piv.ctypes.data,
                       ctypes.byref(info), ctypes.byref(opt))
     _lib.check(rc, "pflu_getrf")
@@ -166,7 +167,7 @@ def getrf_host(a: np.ndarray, b: int, lookahead: int, exact: bool = False, panel
 
 
 def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int = 0, piv=None, trace=None,
-                 panel_kernel: int = 0):
+                 panel_kernel: int = 0, malleable: int = 0):
     """Factor a row-major CUDA float64 torch tensor in place through pflu_getrf_device on the
     current torch stream.  Returns (piv0 int64 CUDA tensor, info).  If ``trace`` is a list, it
     receives :class:`TraceEvent` records (labels PF / TU / TU_L / TU_R / GEMM, seconds from the
@@ -178,7 +179,7 @@ def getrf_device(a, b: int, lookahead: int, exact: bool = False, panel_ctas: int
     if piv is None:
         piv = torch.empty(n, dtype=torch.int64, device=a.device)
     info = ctypes.c_int64(0)
-    opt = _lib.options(exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel)
+    opt = _lib.options(exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel, malleable=malleable)
     stream = torch.cuda.current_stream(a.device).cuda_stream
     tbuf, tcap, tlen = None, 0, ctypes.c_int(0)
     if trace is not None:
@@ -256,7 +257,8 @@ def _lu_factor_mg(a, b, lookahead, n_gpus, exact, return_info, overwrite_a):
 
 
 def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a: bool = True,
-              exact: bool = False, return_info: bool = False, panel_ctas: int = 0, panel_kernel: int = 0):
+              exact: bool = False, return_info: bool = False, panel_ctas: int = 0, panel_kernel: int = 0,
+              malleable: int = 0):
     """Blocked right-looking LU with partial pivoting on the B200.
 
     ``a``: float64 m x n (m >= n) row-major -- a numpy array (host buffers: staged through
@@ -268,6 +270,11 @@ def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a:
     otherwise -- one process, as the reference's in-process call -- pflu_getrf_mg over n_gpus
     devices (NCCL broadcast per step).  ``panel_kernel`` forces the
     panel factorization of every step (0 automatic, 1 cooperative grid, 2 cluster, 3 recursive).
+    ``malleable`` selects the look-ahead-1 trailing-update schedule: 0 dynamic (one CTA per GEMM
+    tile; the block scheduler hands the panel's SMs back as soon as it exits), 1 SM-partitioned (the
+    reference's LA: the panel's SMs stay with the panel chain), 2 LA_MB (partitioned, plus a join
+    grid that puts the panel's SMs on the remaining tiles after PF(k+1)).  All three give bitwise
+    identical factors.
 
     Returns ``(lu, piv)`` (``(lu, piv, info)`` with ``return_info``): packed unit-lower L below
     the diagonal and U on/above it, and 0-based LAPACK pivots (row i swapped with piv[i]).
@@ -295,7 +302,8 @@ def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a:
         if not a.is_cuda:
             raise ValueError("torch input must be a CUDA tensor (use a numpy array for host buffers)")
         work = a if (overwrite_a and a.stride(1) == 1) else a.contiguous().clone()
-        piv, info = getrf_device(work, b, lookahead, exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel)
+        piv, info = getrf_device(work, b, lookahead, exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel,
+                                 malleable=malleable)
     else:
         arr = np.asarray(a)
         if arr.dtype != np.float64 or arr.ndim != 2:
@@ -307,7 +315,8 @@ def lu_factor(a, b: int = 256, lookahead: int = 1, n_gpus: int = 1, overwrite_a:
             work = arr
         else:
             work = np.array(arr, dtype=np.float64, order="C", copy=True)
-        piv, info = getrf_host(work, b, lookahead, exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel)
+        piv, info = getrf_host(work, b, lookahead, exact=exact, panel_ctas=panel_ctas, panel_kernel=panel_kernel,
+                               malleable=malleable)
     if info:
         warnings.warn(f"exactly singular: zero pivot in column {info} (1-based)", RuntimeWarning, stacklevel=2)
     return (work, piv, info) if return_info else (work, piv)
@@ -394,7 +403,8 @@ def qr_factor(a, b: int = 256, lookahead: int = 1, overwrite_a: bool = True, n_g
     return work, geqrf_host(work, b, lookahead)
 
 
-def _factor_matrix(a, cfg: CacheConfig, kind: Kind, lookahead: int, strategy: Strategy, trace):
+def _factor_matrix(a, cfg: CacheConfig, kind: Kind, lookahead: int, strategy: Strategy, trace,
+                   malleable: int = 0):
     if isinstance(a, Matrix):
         mat = a
     else:
@@ -417,22 +427,25 @@ def _factor_matrix(a, cfg: CacheConfig, kind: Kind, lookahead: int, strategy: St
             tau = geqrf_device(t, cfg.b, lookahead, trace=trace).cpu().numpy()
             mat.array[...] = t.cpu().numpy()
             return QrOutput(mat, tau, strategy)
-        piv, info = getrf_device(t, cfg.b, lookahead, trace=trace)
+        piv, info = getrf_device(t, cfg.b, lookahead, trace=trace, malleable=malleable)
         mat.array[...] = t.cpu().numpy()
         return LuOutput(mat, piv.cpu().numpy() + 1, strategy, info)
     if kind is Kind.QR:
         tau = geqrf_host(work, cfg.b, lookahead)
         mat.array[...] = work
         return QrOutput(mat, tau, strategy)
-    piv0, info = getrf_host(work, cfg.b, lookahead)
+    piv0, info = getrf_host(work, cfg.b, lookahead, malleable=malleable)
     mat.array[...] = work
     return LuOutput(mat, piv0 + 1, strategy, info)
 
 
 def dmf_la(a, cfg: CacheConfig, pool=None, kind: Kind = Kind.LU, malleable: bool = False, trace=None):
     """Static look-ahead driver (depth 1), reference factor.py:455-515.  ``pool`` is accepted
-    for signature compatibility (the two sections run as two CUDA streams)."""
-    return _factor_matrix(a, cfg, kind, 1, Strategy.LA_MB if malleable else Strategy.LA, trace)
+    for signature compatibility (the two sections run as two CUDA streams).  ``malleable=True``
+    (LA_MB) runs the SM-partitioned trailing update with the join grid (the panel's SMs rejoin the
+    GEMM's tile queue after PF(k+1), runtime.py:99-113); ``False`` the dynamic tile schedule."""
+    return _factor_matrix(a, cfg, kind, 1, Strategy.LA_MB if malleable else Strategy.LA, trace,
+                          malleable=_lib.SCHED_LA_MB if malleable else _lib.SCHED_DYNAMIC)
 
 
 def dmf_mtb(a, cfg: CacheConfig, pool=None, kind: Kind = Kind.LU, trace=None):

@@ -12,9 +12,12 @@
   ||A - QR||_F / (n u ||A||_F) (oracle.py:113-127, Q formed on the GPU by torch as the checker).
 * CSV: ``kind,strategy,n,b,threads,seconds,gflops,residual`` (bench.py:32, 219-234); the
   ``threads`` column carries the GPU count.
-* Strategies: mtb (look-ahead 0), la (look-ahead 1), la-mb (look-ahead 1: the hardware block scheduler
-  already hands the panel's SMs back to pending GEMM CTAs, which is what the malleable team does on
-  the CPU).  rtm is not offered (out of scope; racy in the reference).
+* Strategies: mtb (look-ahead 0), la (look-ahead 1, dynamic tile schedule: the block scheduler hands
+  the panel's SMs back to pending GEMM tiles), la-static (look-ahead 1, SM-partitioned: the panel's
+  SMs stay with the panel chain -- the reference's non-malleable LA), la-mb (partitioned + a join grid
+  that puts the panel's SMs on the trailing GEMM's remaining tiles after PF(k+1): the reference's
+  malleable team, runtime.py:99-113).  rtm is not offered (out of scope; racy in the reference,
+  SURVEY.md App. A.4).
 """
 from __future__ import annotations
 
@@ -26,7 +29,8 @@ import numpy as np
 
 CSV_HEADER = "kind,strategy,n,b,threads,seconds,gflops,residual"
 _KINDS = ("lu", "qr", "gemm")
-_STRATEGIES = {"mtb": ("MTB", 0), "la": ("LA", 1), "la-mb": ("LA_MB", 1)}
+# strategy -> (CSV label, look-ahead depth, pflu_options.malleable)
+_STRATEGIES = {"mtb": ("MTB", 0, 0), "la": ("LA", 1, 0), "la-static": ("LA_STATIC", 1, 1), "la-mb": ("LA_MB", 1, 2)}
 UNIT_ROUNDOFF = 2.0 ** -53
 
 
@@ -75,7 +79,7 @@ def lu_residual_gpu(a0, lu, piv, block: int = 4096) -> float:
     return err if norm_a == 0.0 else err / (max(n, 1) * UNIT_ROUNDOFF * norm_a)
 
 
-def time_factor(a_host: np.ndarray, b: int, lookahead: int, reps: int, check: bool):
+def time_factor(a_host: np.ndarray, b: int, lookahead: int, reps: int, check: bool, malleable: int = 0):
     import torch
 
     from .api import getrf_device
@@ -90,7 +94,7 @@ def time_factor(a_host: np.ndarray, b: int, lookahead: int, reps: int, check: bo
         work.copy_(pristine)
         torch.cuda.synchronize()
         e0.record()
-        getrf_device(work, b, lookahead, piv=piv)
+        getrf_device(work, b, lookahead, piv=piv, malleable=malleable)
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) * 1e-3
@@ -151,12 +155,12 @@ def run_sweep(kind: str, strategies, sizes, b: int, reps: int, seed: int, check:
     for n in sizes:
         a = make_instance(seed, kind, n)
         for s in strategies:
-            label, la = _STRATEGIES[s]
+            label, la, mall = _STRATEGIES[s]
             if kind == "qr":
                 seconds, residual = time_factor_qr(a, b, la, reps, check)
                 fl = flops(Kind.QR, n)
             else:
-                seconds, residual = time_factor(a, b, la, reps, check)
+                seconds, residual = time_factor(a, b, la, reps, check, malleable=mall)
                 fl = flops(Kind.LU, n)
             records.append(BenchRecord(kind.upper(), label, n, b, gpus, seconds, fl / seconds / 1e9, residual))
     return records

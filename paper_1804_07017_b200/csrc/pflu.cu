@@ -86,6 +86,12 @@ struct DevCtx {
   size_t hbuf_cap = 0;
   int64_t* hpiv = nullptr;
   size_t hpiv_cap = 0;
+  // SM-partitioned look-ahead (pflu_options.malleable): SMs of the panel kernel, per-step tile queues
+  unsigned* sm_mask = nullptr;   // 8 words (device)
+  unsigned* rec_mask = nullptr;  // host-side switch: the next panel launch records its SMs here
+  int* tile_ctr = nullptr;
+  size_t tile_ctr_cap = 0;
+  std::vector<cudaEvent_t> swev;  // per step: TU_R(k)'s swap + solve done (the join grid waits on it)
 };
 
 static std::atomic<long long> g_launches{0};
@@ -441,6 +447,51 @@ static int launch_gemm_ws(const GemmArgs& p, cudaStream_t st, bool* done) {
 }
 // PFLU_GEMM_WS: 1 = WS1 (default, the production trailing update), 0 / 2 / 3 = the other ring
 // depths, -1 = the cp.async GEMM (gemm_dmma_t / PFLU_GEMM_VARIANT)
+// persistent, SM-budgeted WS GEMM over an atomic tile queue (gemm_dmma_ws_pers): grid CTAs; views
+// that TMA cannot describe fall back to the dynamic tile-per-CTA GEMM (correct, not partitioned)
+template <class C>
+static int launch_gemm_pers(const GemmArgs& p, const WsCtl& ctl, int grid, cudaStream_t st, bool* done) {
+  *done = false;
+  PfnEncodeTiled enc = tma_encoder();
+  if (!enc) return PFLU_OK;
+  if ((reinterpret_cast<uintptr_t>(p.a) & 15) || (reinterpret_cast<uintptr_t>(p.b) & 15) ||
+      (reinterpret_cast<uintptr_t>(p.c) & 15) || (p.lda & 1) || (p.ldb & 1) || (p.ldc & 1) ||
+      p.M >= (int64_t)1 << 31 || p.N >= (int64_t)1 << 31 || p.K >= (int64_t)1 << 31)
+    return PFLU_OK;
+  constexpr int SMEM = C::SMEM + 64;  // + the per-stage tile indices
+  static bool attr_dev[64] = {};
+  int attr_d = 0;
+  CK(cudaGetDevice(&attr_d));
+  if (!attr_dev[attr_d & 63]) {
+    CK(cudaFuncSetAttribute(gemm_dmma_ws_pers<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    attr_dev[attr_d & 63] = true;
+  }
+  CUtensorMap ta, tb;
+  const cuuint32_t es[2] = {1, 1};
+  const cuuint64_t da[2] = {(cuuint64_t)p.K, (cuuint64_t)p.M}, sa[1] = {(cuuint64_t)p.lda * 8};
+  const cuuint32_t ba[2] = {8, (cuuint32_t)C::BM};
+  CUresult r = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p.a), da, sa, ba, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(PFLU_ERR_CUDA, "cuTensorMapEncodeTiled(A) failed: %d", (int)r);
+  const cuuint64_t db[2] = {(cuuint64_t)p.N, (cuuint64_t)p.K}, sb[1] = {(cuuint64_t)p.ldb * 8};
+  const cuuint32_t bb[2] = {8, (cuuint32_t)C::BK};
+  r = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(p.b), db, sb, bb, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(PFLU_ERR_CUDA, "cuTensorMapEncodeTiled(B) failed: %d", (int)r);
+  const int64_t tm = (p.M + C::BM - 1) / C::BM, tn = (p.N + C::BN - 1) / C::BN;
+  if (tm * tn > INT_MAX) return set_err(PFLU_ERR_UNSUPPORTED, "gemm grid too large");
+  TmaGemmArgs q;
+  q.c = p.c; q.ldc = p.ldc; q.M = p.M; q.N = p.N; q.K = p.K;
+  q.tiles_m = (int)tm; q.tiles_n = (int)tn;
+  gemm_dmma_ws_pers<C><<<(unsigned)std::max(1, grid), C::THREADS, SMEM, st>>>(ta, tb, q, ctl);
+  CK(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  *done = true;
+  return PFLU_OK;
+}
+
 static int g_gemm_ws = []() { const char* e = getenv("PFLU_GEMM_WS"); return e ? atoi(e) : 1; }();
 
 static int launch_gemm(double* c, int64_t ldc, const double* a, int64_t lda, const double* b, int64_t ldb,
@@ -637,6 +688,7 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
   p.prof = g_prof;
   p.resync = g_resync;
   p.swcap = 0;
+  p.sm_mask = c.rec_mask;
   // one thread-block cluster (DSMEM exchange) when the rows fit its CTAs' shared memory
   const bool want_cl = opt.panel_kernel == 2 || (opt.panel_kernel == 0 && g_cluster > 0 && rows <= g_cl_rows);
   if (want_cl) {
@@ -794,6 +846,39 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     CK(cudaMalloc(&c.dinv, sizeof(double) * c.dinv_cap));
   }
   auto inv_of = [&](int k) { return c.dinv + inv_words * k; };
+  // SM-partitioned look-ahead (pflu_options.malleable 1 = LA, 2 = LA_MB; DMMA mode, look-ahead 1):
+  // TU_R(k)'s GEMM is a persistent kernel over tile queue k that leaves the panel's SMs alone
+  const int sched = (lookahead == 1 && !exact && !g_tur_split && !g_emu_ranks) ? std::max(0, std::min(2, opt.malleable)) : 0;
+  if (sched) {
+    if (!c.sm_mask) CK(cudaMalloc(&c.sm_mask, 8 * sizeof(unsigned)));
+    if (c.tile_ctr_cap < (size_t)count) {
+      if (c.tile_ctr) CK(cudaFree(c.tile_ctr));
+      c.tile_ctr = nullptr;
+      c.tile_ctr_cap = 0;
+      CK(cudaMalloc(&c.tile_ctr, sizeof(int) * count));
+      c.tile_ctr_cap = count;
+    }
+    CK(cudaMemsetAsync(c.sm_mask, 0, 8 * sizeof(unsigned), user));
+    CK(cudaMemsetAsync(c.tile_ctr, 0, sizeof(int) * count, user));
+    while (c.swev.size() < (size_t)count) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c.swev.push_back(e);
+    }
+  }
+  // the trailing GEMM of TU_R(k) on [lo, hi) as a persistent kernel (main grid or the join grid)
+  auto tur_gemm_pers = [&](int k, int64_t lo, int64_t hi, bool joiner, cudaStream_t st, bool* done) -> int {
+    *done = false;
+    const Step s = grid[k];
+    const int64_t below = s.col0 + s.bw;
+    if (hi <= lo || below >= m) return PFLU_OK;
+    GemmArgs gp;
+    gp.c = a + below * lda + lo; gp.a = a + below * lda + s.col0; gp.b = a + s.col0 * lda + lo;
+    gp.ldc = lda; gp.lda = lda; gp.ldb = lda;
+    gp.M = m - below; gp.N = hi - lo; gp.K = s.bw;
+    const WsCtl ctl{c.tile_ctr + k, c.sm_mask, joiner ? 1 : 0};
+    return launch_gemm_pers<WS1>(gp, ctl, joiner ? 2 * PF_CL_MAX : 2 * c.sms, st, done);
+  };
   auto update_cols = [&](int k, int64_t lo, int64_t hi, cudaStream_t st, int label) -> int {
     // TU of step k on storage columns [lo, hi): laswp + trsm (fused), then the DMMA update
     if (hi <= lo) return PFLU_OK;
@@ -808,8 +893,14 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
       if (label != PFLU_TRACE_TU_L)
         CKR(tr.begin(PFLU_TRACE_GEMM, k, st, &t_g, 2.0 * (double)(m - below) * (double)(hi - lo) * (double)s.bw));
       const int pg = label == PFLU_TRACE_TU ? -1 : (label == PFLU_TRACE_TU_R ? g_tur_grid : 0);
-      CKR(launch_gemm(a + below * lda + lo, lda, a + below * lda + s.col0, lda, a + s.col0 * lda + lo, lda,
-                      m - below, hi - lo, s.bw, exact, st, pg));
+      bool done = false;
+      if (sched && label == PFLU_TRACE_TU_R) {
+        CK(cudaEventRecord(c.swev[k], st));  // the join grid may take tiles once U12 is solved
+        CKR(tur_gemm_pers(k, lo, hi, false, st, &done));
+      }
+      if (!done)
+        CKR(launch_gemm(a + below * lda + lo, lda, a + below * lda + s.col0, lda, a + s.col0 * lda + lo, lda,
+                        m - below, hi - lo, s.bw, exact, st, pg));
       CKR(tr.end(t_g, st));
     }
     return tr.end(t_tu, st);
@@ -833,7 +924,10 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     // = dist.py: the owner's tall panels on the grid kernel from 8 ranks up (chain-bound there)
     if (g_emu_ranks >= g_emu_grid_ranks && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;
     if (g_pf_force >= 0 && opt.panel_kernel == 0) popt.panel_kernel = g_pf_force;
-    CKR(panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, popt, st));
+    if (sched && k == 0) c.rec_mask = c.sm_mask;  // PF(0) runs alone: its SMs become the panel's partition
+    const int prc = panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, popt, st);
+    c.rec_mask = nullptr;
+    CKR(prc);
     const int np = (int)std::min(s.bw, m - s.col0);
     CKR(launch_plan(piv, s.col0, np, plan_of(k), st));
     if (use_dinv) CKR(launch_diag_inv(a + s.col0 * lda + s.col0, lda, np, inv_of(k), st));
@@ -967,7 +1061,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   // C2 31.9 -> 31.6 ms: the panel stream only waits for the chunk that holds block k+1); one stream
   // above (C4 unchanged, its concurrent chunk GEMMs interfere); PFLU_CHUNKS overrides
   const int dflt = g_chunks_env > 0 ? g_chunks_env : (n <= 16384 ? 6 : 1);
-  const int nch = std::max(1, std::min({hin ? std::max(dflt, hin->chunks) : dflt, MAX_CHUNKS, count}));
+  const int nch = sched ? 1 : std::max(1, std::min({hin ? std::max(dflt, hin->chunks) : dflt, MAX_CHUNKS, count}));
   std::vector<int> chunk_blk(nch + 1);
   for (int ch = 0; ch <= nch; ++ch) chunk_blk[ch] = (int)((int64_t)count * ch / nch);
   auto chunk_of_block = [&](int blk) {
@@ -1032,6 +1126,13 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
       CKR(update_cols(k, grid[k + 1].col0, grid[k + 1].col0 + grid[k + 1].bw, c.sP, PFLU_TRACE_TU_L));
       CK(cudaEventRecord(ev_tul(k), c.sP));
       CKR(pf(k + 1, c.sP));
+      if (sched == 2 && lo_r < hi_r && grid[k].col0 + grid[k].bw < m) {
+        // LA_MB: the panel's SMs rejoin TU_R(k) -- a join grid on the same tile queue (it runs once
+        // U12 of step k is solved; ev_pf(k+1), recorded after it, orders every later reader)
+        CK(cudaStreamWaitEvent(c.sP, c.swev[k], 0));
+        bool done = false;
+        CKR(tur_gemm_pers(k, lo_r, hi_r, true, c.sP, &done));
+      }
       CK(cudaEventRecord(ev_pf(k + 1), c.sP));
     } else {
       CK(cudaEventRecord(ev_tul(k), c.sP));

@@ -668,6 +668,160 @@ __global__ void __launch_bounds__(C::THREADS, 2)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// The same warp-specialised GEMM as a PERSISTENT kernel over an atomic tile queue, for the
+// SM-partitioned look-ahead (pflu_options.malleable, the reference's LA / LA_MB):
+//   * main grid (ctl.joiner = 0): two CTAs per SM; a CTA on an SM flagged in ctl.mask (the SMs the
+//     panel kernel occupies) exits at once, so the panel chain keeps those SMs;
+//   * join grid (ctl.joiner = 1, launched on the panel stream after PF(k+1)): the panel's SMs take
+//     the remaining tiles of the same queue -- the reference's panel worker rejoining the GEMM team
+//     at the next tile boundary (runtime.py:99-113, factor.py:503-504).
+// The producer thread pops a tile, streams its K stages through the ring and publishes the tile
+// index with the first stage; an exhausted queue is signalled by a data-less arrive on "full".
+struct WsCtl {
+  int* counter;          // tile queue head (zeroed before the main launch)
+  const unsigned* mask;  // reserved-SM bitmask (NULL: none)
+  int joiner;
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 2)
+    gemm_dmma_ws_pers(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, TmaGemmArgs p,
+                      WsCtl ctl) {
+  extern __shared__ __align__(1024) double ws_smem[];
+  double* sm = ws_smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ws_smem + C::ST * C::STAGE);
+  uint64_t* empty = full + C::ST;
+  int* tile_of = reinterpret_cast<int*>(empty + C::ST);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (!ctl.joiner && ctl.mask) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
+    if ((ctl.mask[smid >> 5] >> (smid & 31)) & 1u) return;  // this SM belongs to the panel chain
+  }
+  const int ntiles = p.tiles_m * p.tiles_n;
+  const int KT = (int)((p.K + C::BK - 1) / C::BK);
+  if (tid == 0) {
+    for (int s = 0; s < C::ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::CONSUMERS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::PRODUCER_REGS));
+    if (warp == 0 && lane == 0) {
+      int g = 0;
+      for (;;) {
+        const int tile = atomicAdd(ctl.counter, 1);
+        const bool done = tile >= ntiles;
+        int tm = 0, tn = 0;
+        if (!done) tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+        for (int kt = 0; kt < (done ? 1 : KT); ++kt, ++g) {
+          const int s = g % C::ST;
+          if (g >= C::ST) mbar_wait(&empty[s], (unsigned)((g / C::ST - 1) & 1));
+          if (kt == 0) tile_of[s] = done ? -1 : tile;
+          if (done) {
+            mbar_arrive(&full[s]);
+            break;
+          }
+          double* st = sm + s * C::STAGE;
+          mbar_expect_tx(&full[s], (unsigned)(C::STAGE * 8));
+          const int k0 = kt * C::BK;
+#pragma unroll
+          for (int kb = 0; kb < C::BK / 8; ++kb) tma_load_2d(st + kb * C::ABOX, &ta, k0 + kb * 8, tm * C::BM, &full[s]);
+#pragma unroll
+          for (int nb = 0; nb < C::BN / 8; ++nb)
+            tma_load_2d(st + C::BM * C::BK + nb * C::BBOX, &tb, tn * C::BN + nb * 8, k0, &full[s]);
+        }
+        if (done) break;
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::CONSUMER_REGS));
+  const int cw = warp - 4;
+  const int g8 = lane >> 2, t = lane & 3;
+  const int wm = cw / C::WN, wn = cw % C::WN;
+  const int tlo = t & 1, thi = t >> 1;
+  const int a_base = (wm * C::TM + g8) * 8 + tlo;
+  const int b_base = (wn * C::TN / 8) * C::BBOX + (g8 & 1);
+  int xa[2], xb[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int h2 = q + 2 * thi;
+    xa[q] = ((h2 ^ (g8 >> 1)) << 1);
+    xb[q] = (2 * q + tlo + 4 * thi) * 8 + (((g8 >> 1) ^ h2) << 1);
+  }
+  int g = 0;
+  for (;;) {
+    mbar_wait(&full[g % C::ST], (unsigned)((g / C::ST) & 1));
+    const int tile = tile_of[g % C::ST];
+    if (tile < 0) break;
+    int tm, tn;
+    tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+    const int m0 = tm * C::BM, n0 = tn * C::BN;
+    double acc[C::FM][C::FN][2];
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i) {
+      const int64_t row = m0 + wm * C::TM + i * 8 + g8;
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) {
+        const int64_t col = n0 + wn * C::TN + j * 8 + 2 * t;
+        const double* cp = p.c + row * p.ldc + col;
+        if (row < p.M && col + 1 < p.N) {
+          const double2 v = *reinterpret_cast<const double2*>(cp);
+          acc[i][j][0] = v.x;
+          acc[i][j][1] = v.y;
+        } else {
+          acc[i][j][0] = (row < p.M && col < p.N) ? cp[0] : 0.0;
+          acc[i][j][1] = (row < p.M && col + 1 < p.N) ? cp[1] : 0.0;
+        }
+      }
+    }
+    for (int kt = 0; kt < KT; ++kt, ++g) {
+      const int s = g % C::ST;
+      if (kt > 0) mbar_wait(&full[s], (unsigned)((g / C::ST) & 1));
+      const double* cA = sm + s * C::STAGE + a_base;
+      const double* cB = sm + s * C::STAGE + C::BM * C::BK + b_base;
+#pragma unroll
+      for (int kb = 0; kb < C::BK / 8; ++kb) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          double af[C::FM], bf[C::FN];
+#pragma unroll
+          for (int i = 0; i < C::FM; ++i) af[i] = cA[kb * C::ABOX + i * 64 + xa[q]];
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j) bf[j] = -cB[j * C::BBOX + kb * 64 + xb[q]];
+#pragma unroll
+          for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+            for (int j = 0; j < C::FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // see gemm_dmma_ws
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i) {
+      const int64_t row = m0 + wm * C::TM + i * 8 + g8;
+      if (row >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) {
+        const int64_t col = n0 + wn * C::TN + j * 8 + 2 * t;
+        double* cp = p.c + row * p.ldc + col;
+        if (col + 1 < p.N) {
+          *reinterpret_cast<double2*>(cp) = make_double2(acc[i][j][0], acc[i][j][1]);
+        } else if (col < p.N) {
+          cp[0] = acc[i][j][0];
+        }
+      }
+    }
+  }
+}
+
 // measured at the C4 step-0 shape 32512 x 32512 x 256 (tools/gemm_ws_probe.py, profiles/r05_gemm_ws.log):
 // WS1 35.4 TFLOP/s (production), WS2 35.2, WS0 35.0, WS3 34.3; cp.async GV6 33.7.  An L2 prefetch of
 // the C tile by the idle producer warps made WS1 / WS0 slower (34.1 / 33.8).

@@ -48,6 +48,8 @@ struct PanelArgs {
   unsigned long long* prof;  // optional: per-phase clock64 totals of CTA 0 (tools/ only)
   int resync;                // re-align all CTAs every `resync` columns (0 = never)
   int swcap;                 // cluster kernel: doubles of dedicated row-swap staging (0 = use the L block)
+  unsigned* sm_mask;         // optional: every CTA ORs in the bit of its SM (the SM-partitioned look-ahead
+                             // reserves these SMs for the panel chain)
 };
 
 // key polling: spin this many misses before backing off with __nanosleep (whose granularity is
@@ -250,6 +252,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   __shared__ long long s_wrow;
 
   const unsigned epoch = CL ? 0u : *(volatile unsigned*)p.epoch;
+  if (p.sm_mask && tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
+    atomicOr(p.sm_mask + (smid >> 5), 1u << (smid & 31));
+  }
   // LL layout: [2 parities][S + 1 records][16 + 2W words], then S sync words
   const int rec = 16 + 2 * W;  // [key line: key, row (16 words = 128 B)][data: 2W words]; 128-B aligned
   unsigned long long* sync_words = p.ll + PF_SBOX_OFFSET;  // [reader 256][writer 256][2 words]

@@ -268,3 +268,40 @@ def test_multipliers_bounded(cuda):
     lu, piv, _ = run(a0, 128, 1, exact=False)
     low = np.tril(lu, -1)
     assert np.max(np.abs(low)) <= 1.0 + 4 * oracle.UNIT_ROUNDOFF
+
+
+@pytest.mark.parametrize("mode", [1, 2], ids=["la_static", "la_mb"])
+@pytest.mark.parametrize("n,b", [(777, 100), (2048, 128), (5000, 256), (8192, 256)])
+def test_malleable_schedules_bitwise_equal_dynamic(cuda, mode, n, b):
+    """The SM-partitioned look-ahead (persistent trailing GEMM over an atomic tile queue, the panel's
+    SMs reserved; LA_MB adds the join grid) computes every tile with the same instructions as the
+    dynamic tile-per-CTA schedule: factors and pivots BITWISE equal, pivots = the oracle's."""
+    import torch
+
+    from paper_1804_07017_b200 import getrf_device
+
+    a0 = np.random.default_rng(n + b).uniform(-1.0, 1.0, (n, n))
+    d0 = torch.from_numpy(a0).to(cuda)
+    ref = d0.clone()
+    piv_r, info_r = getrf_device(ref, b, 1)
+    for rep in range(2):
+        x = d0.clone()
+        piv, info = getrf_device(x, b, 1, malleable=mode)
+        torch.cuda.synchronize()
+        assert info == info_r == 0
+        assert torch.equal(piv, piv_r)
+        assert bitwise_equal(x.cpu().numpy(), ref.cpu().numpy())
+    if n <= 2048:
+        _, wpiv, _ = oracle.getrf(a0, b)
+        assert np.array_equal(piv_r.cpu().numpy(), wpiv)
+
+
+def test_dmf_la_malleable_runs_la_mb(cuda, golden_small):
+    """dmf_la(malleable=True) -> Strategy.LA_MB on the partitioned + join schedule, same result."""
+    from paper_1804_07017_b200 import CacheConfig, Kind, Matrix, dmf_la
+
+    a0 = golden_small["u300__a"]
+    out = dmf_la(Matrix.from_array(a0.copy()), CacheConfig(b=32), None, Kind.LU, malleable=True)
+    assert out.strategy.name == "LA_MB"
+    assert np.array_equal(np.asarray(out.pivots) - 1, golden_small["u300__piv"])
+    assert oracle.max_rel_diff(np.ascontiguousarray(out.matrix.array), golden_small["u300__f"], a0) <= 1e-10
