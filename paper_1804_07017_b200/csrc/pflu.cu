@@ -1060,7 +1060,9 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   // device buffers: 6 chunks up to n = 16384, where the panel chain still shows (C3 117.2 -> 115.1 ms,
   // C2 31.9 -> 31.6 ms: the panel stream only waits for the chunk that holds block k+1); one stream
   // above (C4 unchanged, its concurrent chunk GEMMs interfere); PFLU_CHUNKS overrides
-  const int dflt = g_chunks_env > 0 ? g_chunks_env : (n <= 16384 ? 6 : 1);
+  // r05 (WS GEMM) re-measure, profiles/r05_chunks_sweep.log: C4 1 chunk 723.2 ms, 2: 723.1, 3: 721.0,
+  // 4: 719.8, 6: 720.0; C3 114.3 / 112.8 / 112.6 / 112.4 / 112.4 -> 6 up to 16384, 4 above
+  const int dflt = g_chunks_env > 0 ? g_chunks_env : (n <= 16384 ? 6 : 4);
   const int nch = sched ? 1 : std::max(1, std::min({hin ? std::max(dflt, hin->chunks) : dflt, MAX_CHUNKS, count}));
   std::vector<int> chunk_blk(nch + 1);
   for (int ch = 0; ch <= nch; ++ch) chunk_blk[ch] = (int)((int64_t)count * ch / nch);

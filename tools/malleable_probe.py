@@ -16,7 +16,12 @@ for n in sizes:
     d0 = torch.empty(n, n, dtype=torch.float64, device=dev).uniform_(-1, 1)
     x = torch.empty_like(d0)
     row = {"n": n, "b": b}
-    for mode, name in [(0, "dynamic"), (1, "la_static"), (2, "la_mb")]:
+    import os
+
+    modes = [(0, "dynamic"), (1, "la_static"), (2, "la_mb")]
+    if os.environ.get("PROBE_DYNAMIC_ONLY"):
+        modes = modes[:1]
+    for mode, name in modes:
         best = 1e9
         for rep in range(3):
             x.copy_(d0)
