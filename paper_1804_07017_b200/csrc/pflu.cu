@@ -187,8 +187,8 @@ static DevCtx g_ctx[64];
 
 static constexpr int PF_MAX_CTAS = PF_THREADS;
 
-#ifdef PFLU_PANEL_EXACT_T
-// hazard re-check build: the exact flag compiled into the panel kernel (see panel_kernel's EX)
+#ifndef PFLU_PANEL_EXACT_RUNTIME
+// the exact flag compiled into the panel kernel (see panel_kernel's EX)
 template <int EX>
 static const void* pf_fn_ex(int W, bool cl) {
   if (cl) return W == 8 ? (const void*)panel_kernel<8, true, EX> : W == 16 ? (const void*)panel_kernel<16, true, EX>

@@ -205,9 +205,9 @@ struct PanelSmem {
 // CL = true:  the S <= 16 CTAs form one thread-block cluster; candidates and the diagonal row are
 //             pushed into every peer's shared memory with st.async completing on the peer's mbarrier
 //             (no polling, no L2 round trip), and grid syncs are cluster barriers.
-// EX: -1 = exact flag read at run time (p.exact, the shipped build); 0 / 1 = compiled in (the
-// specialisation that once returned wrong pivots on the singular golden case; built with
-// -DPFLU_PANEL_EXACT_T by tools/panel_hazard.sh to re-check it).
+// EX: 0 / 1 = the exact flag compiled in (production since round 2: DMMA mode's in-leaf updates are
+// single FMAs; this specialisation exposed the zero-pivot reconvergence hazard fixed below);
+// -1 = read at run time from p.exact (-DPFLU_PANEL_EXACT_RUNTIME, the round-1 build).
 template <int W, bool CL, int EX = -1>
 __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   extern __shared__ __align__(16) double pf_smem[];
@@ -262,6 +262,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   unsigned long long* sync_words = p.ll + PF_SBOX_OFFSET;  // [reader 256][writer 256][2 words]
   unsigned long long* mbox = p.ll + PF_MBOX_OFFSET;  // [2][reader 256][writer 256][4 words]
   const bool exact = EX < 0 ? p.exact != 0 : EX != 0;
+  // in-leaf rank-1 updates and the U solve: the reference's rounding (multiply, round, subtract) in
+  // exact mode; one FMA in DMMA mode (whose trailing GEMM is an FMA chain anyway)
+  auto upd = [&](double x, double l, double u) -> double {
+    if constexpr (EX == 0) return fma(-l, u, x);
+    else return sub_mul_exact(x, l, u);
+  };
   const int g_resync = p.resync;
   const bool prof_on = p.prof != nullptr && tid == 0;
   long long prof_t = clock64();
@@ -547,12 +553,15 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           __syncwarp();
         }
       }
+      // DMMA mode scales by the reciprocal (one division per thread); exact mode divides every row
+      // (the reference's _jit.py:180-182)
+      const double rpiv = EX == 0 ? 1.0 / pivot : 0.0;
       for (int64_t r = p1 + tid; r < nrows; r += PF_THREADS) {
         double* tr = tile + r * LD;
-        const double l = __ddiv_rn(tr[j], pivot);
+        const double l = EX == 0 ? tr[j] * rpiv : __ddiv_rn(tr[j], pivot);
         tr[j] = l;
         if (j + 1 < wb) {
-          const double x = sub_mul_exact(tr[j + 1], l, uj1);
+          const double x = upd(tr[j + 1], l, uj1);
           tr[j + 1] = x;
           if (nxt) {
             const double k = pivot_key(x, rbeg + r == c + 1);
@@ -570,7 +579,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       auto finish_row = [&](long long row) {
         double* tr = tile + (row - rbeg) * LD;
         const double l = tr[j];
-        for (int cc = j + 2 + lane; cc < wb; cc += 32) tr[cc] = sub_mul_exact(tr[cc], l, ucur[cc]);
+        for (int cc = j + 2 + lane; cc < wb; cc += 32) tr[cc] = upd(tr[cc], l, ucur[cc]);
         __syncwarp();
       };
       // cluster: the diagonal row is finished and staged by warp 1 in parallel with warp 0's candidate
@@ -603,7 +612,18 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           if ((cand_own && gr == cr) || (diag_own && gr == c + 1)) continue;
           double* tr = tile + r * LD;
           const double l = tr[j];
-          for (int cc = j + 2; cc < wb; ++cc) tr[cc] = sub_mul_exact(tr[cc], l, ucur[cc]);
+          // four columns per round with every load issued before the stores (tr and ucur may alias
+          // as far as the compiler knows, so it would not reorder them itself)
+          int cc = j + 2;
+          for (; cc + 3 < wb; cc += 4) {
+            const double a0 = tr[cc], a1 = tr[cc + 1], a2 = tr[cc + 2], a3 = tr[cc + 3];
+            const double u0 = ucur[cc], u1 = ucur[cc + 1], u2 = ucur[cc + 2], u3 = ucur[cc + 3];
+            tr[cc] = upd(a0, l, u0);
+            tr[cc + 1] = upd(a1, l, u1);
+            tr[cc + 2] = upd(a2, l, u2);
+            tr[cc + 3] = upd(a3, l, u3);
+          }
+          for (; cc < wb; ++cc) tr[cc] = upd(tr[cc], l, ucur[cc]);
         }
       }
       __syncthreads();
@@ -745,7 +765,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
 #pragma unroll
         for (int i = 0; i < K; ++i) {
 #pragma unroll
-          for (int r = i + 1; r < K; ++r) x[r] = sub_mul_exact(x[r], ljj[r * K + i], x[i]);
+          for (int r = i + 1; r < K; ++r) x[r] = upd(x[r], ljj[r * K + i], x[i]);
         }
 #pragma unroll
         for (int i = 0; i < K; ++i) ubuf[i * ldu + col] = x[i];

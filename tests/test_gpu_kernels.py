@@ -271,7 +271,7 @@ def test_cli_sweep_with_check(cuda, capsys):
     assert cli.main(["--kind", "lu", "--strategy", "all", "--n-min", "300", "--n-max", "600", "--n-step", "300",
                      "--b", "64", "--reps", "1", "--check"]) == 0
     recs = cli.parse_csv(capsys.readouterr().out)
-    assert len(recs) == 6 and {r.strategy for r in recs} == {"MTB", "LA", "LA_MB"}
+    assert len(recs) == 8 and {r.strategy for r in recs} == {"MTB", "LA", "LA_STATIC", "LA_MB"}
     for r in recs:
         assert r.gflops > 0 and 0 < r.residual <= 50      # reference test_factor.py:391-398 bound
 
