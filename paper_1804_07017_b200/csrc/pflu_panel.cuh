@@ -556,18 +556,24 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       // DMMA mode scales by the reciprocal (one division per thread); exact mode divides every row
       // (the reference's _jit.py:180-182)
       const double rpiv = EX == 0 ? 1.0 / pivot : 0.0;
-      for (int64_t r = p1 + tid; r < nrows; r += PF_THREADS) {
-        double* tr = tile + r * LD;
-        const double l = EX == 0 ? tr[j] * rpiv : __ddiv_rn(tr[j], pivot);
-        tr[j] = l;
-        if (j + 1 < wb) {
-          const double x = upd(tr[j + 1], l, uj1);
-          tr[j + 1] = x;
-          if (nxt) {
-            const double k = pivot_key(x, rbeg + r == c + 1);
-            if (key_better(k, rbeg + r, ck, cr)) { ck = k; cr = rbeg + r; }
+      {
+        // 32-bit local rows in the hot loop (smaller local row <=> smaller global row)
+        const int diag_l = (int)(c + 1 - rbeg);
+        int crl = INT_MAX;
+        for (int r = (int)p1 + tid; r < nrows; r += PF_THREADS) {
+          double* tr = tile + r * LD;
+          const double l = EX == 0 ? tr[j] * rpiv : __ddiv_rn(tr[j], pivot);
+          tr[j] = l;
+          if (j + 1 < wb) {
+            const double x = upd(tr[j + 1], l, uj1);
+            tr[j + 1] = x;
+            if (nxt) {
+              const double k = pivot_key(x, r == diag_l);
+              if (k > ck || (k == ck && r < crl)) { ck = k; crl = r; }
+            }
           }
         }
+        if (crl != INT_MAX) cr = rbeg + crl;
       }
       PF_PROF_MARK(10);
       if (nxt) cta_best(ck, cr);
@@ -607,9 +613,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       // pass 2 (warps 1..7): remaining columns (mul then sub, _jit.py:183-186)
       if (j + 2 < wb && warp > 0) {
         constexpr int NT2 = PF_THREADS - 32;
-        for (int64_t r = max((int64_t)0, c + 1 - rbeg) + (tid - 32); r < nrows; r += NT2) {
-          const long long gr = rbeg + r;
-          if ((cand_own && gr == cr) || (diag_own && gr == c + 1)) continue;
+        const int skip_c = cand_own ? (int)(cr - rbeg) : -1, skip_d = diag_own ? (int)(c + 1 - rbeg) : -1;
+        for (int r = (int)max((int64_t)0, c + 1 - rbeg) + (tid - 32); r < nrows; r += NT2) {
+          if (r == skip_c || r == skip_d) continue;
           double* tr = tile + r * LD;
           const double l = tr[j];
           // four columns per round with every load issued before the stores (tr and ucur may alias
