@@ -125,14 +125,15 @@ def getrf_steps_inplace(a: np.ndarray, b: int, nsteps: int, piv: np.ndarray | No
 
 def getrf_top2_inplace(a: np.ndarray, b: int, piv: np.ndarray | None = None):
     """The full blocked factorization in place (row-major, any size that fits in host memory), with
-    the tie classifier's record: top2[j] = (|winner|, |runner-up|, runner-up row) of column j's pivot
-    search (reference _jit.py:162-170, strict '>' so the smallest row wins).  Returns (piv, top2, info)."""
+    the tie classifier's record: top2[j] = (|winner|, |runner-up|, runner-up row, number of candidates
+    within 1e-12 relative of the winner) of column j's pivot search (reference _jit.py:162-170, strict
+    '>' so the smallest row wins).  Returns (piv, top2, info)."""
     m, n = a.shape
     if not a.flags.c_contiguous or a.dtype != np.float64:
         raise ValueError("row-major float64 array required (in place)")
     if piv is None:
         piv = np.zeros(n, dtype=np.int64)
-    top2 = np.full((n, 3), -1.0)
+    top2 = np.full((n, 4), -1.0)
     info = int(lib().orc_getrf_steps_top2(_dp(a), m, n, n, int(b), _ip(piv), -1, _dp(top2)))
     return piv, top2, info
 
@@ -142,14 +143,16 @@ TIE_RTOL = 1e-12
 
 
 def near_ties(top2: np.ndarray, rtol: float = 1e-6) -> np.ndarray:
-    """Rows (col, |winner|, |runner-up|, runner-up row) of every column whose relative top-two gap
-    (v1 - v2) / v1 is <= rtol (the columns where a correctly rounded factorization could pick another
-    pivot).  Committed per config so a GPU pivot mismatch can be classified without a host re-run."""
+    """Rows (col, |winner|, |runner-up|, runner-up row[, tied candidates]) of every column whose
+    relative top-two gap (v1 - v2) / v1 is <= rtol (the columns where a correctly rounded factorization
+    could pick another pivot).  Committed per config so a GPU pivot mismatch can be classified without
+    a host re-run."""
     v1, v2 = top2[:, 0], top2[:, 1]
     with np.errstate(divide="ignore", invalid="ignore"):
         gap = np.where(v1 > 0, (v1 - v2) / v1, np.inf)
     cols = np.nonzero((v2 >= 0) & (gap <= rtol))[0]
-    return np.column_stack([cols.astype(np.float64), v1[cols], v2[cols], top2[cols, 2]])
+    extra = [top2[cols, 3]] if top2.shape[1] > 3 else []
+    return np.column_stack([cols.astype(np.float64), v1[cols], v2[cols], top2[cols, 2]] + extra)
 
 
 def classify_pivots(piv_gpu, piv_ref, ties: np.ndarray, rtol: float = TIE_RTOL) -> dict:
@@ -165,11 +168,14 @@ def classify_pivots(piv_gpu, piv_ref, ties: np.ndarray, rtol: float = TIE_RTOL) 
     row = ties[ties[:, 0] == j] if len(ties) else ties
     if len(row) == 0:
         return {"equal": False, "first_mismatch": j, "tie": None, "ok": False}
-    _, v1, v2, r2 = row[0]
+    _, v1, v2, r2 = row[0][:4]
+    nties = int(row[0][4]) if len(row[0]) > 4 else 2
     gap = (v1 - v2) / v1
-    ok = bool(gap <= rtol and int(r2) == int(piv_gpu[j]))
+    # a two-way tie must have been broken towards the runner-up; with three or more tied candidates
+    # any of them is a legitimate choice (only the runner-up's row is recorded)
+    ok = bool(gap <= rtol and (int(r2) == int(piv_gpu[j]) or nties > 2))
     return {"equal": False, "first_mismatch": j, "tie": {"v1": v1, "v2": v2, "rel_gap": gap,
-            "runner_up_row": int(r2)}, "ok": ok}
+            "runner_up_row": int(r2), "tied_candidates": nties}, "ok": ok}
 
 
 def step_flops(m: int, n: int, b: int, k: int = 0) -> int:

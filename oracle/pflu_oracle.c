@@ -42,10 +42,11 @@ static int nthreads(void) { return g_threads > 0 ? g_threads : omp_get_max_threa
 /* Unblocked right-looking LU on an m x w panel (row-major, leading dim lda).  Processes the
  * first `steps` columns (steps <= min(m, w); pass -1 for all).  piv[j] = 0-based panel-local
  * pivot row.  Returns 0 or 1 + first column whose pivot was exactly zero (left as is). */
-/* top2 (optional, 3 doubles per column): the tie classifier's record of column j's search --
- * |winner|, the largest |candidate| among the OTHER rows (-1 if none) and that runner-up's
- * panel-local row (the smallest such row, as the strict '>' scan would take it).  North_star allows
- * a pivot mismatch only where these two magnitudes tie within 1e-12 relative. */
+/* top2 (optional, 4 doubles per column): the tie classifier's record of column j's search --
+ * |winner|, the largest |candidate| among the OTHER rows (-1 if none), that runner-up's panel-local
+ * row (the smallest such row, as the strict '>' scan would take it), and the number of candidates
+ * within 1e-12 relative of the winner (the winner included).  North_star allows a pivot mismatch only
+ * where the top two magnitudes tie within 1e-12 relative. */
 static int64_t lu_unb_impl(double *a, int64_t m, int64_t w, int64_t lda, int64_t *piv, int64_t steps,
                            double *top2) {
   int64_t kmax = m < w ? m : w;
@@ -60,7 +61,12 @@ static int64_t lu_unb_impl(double *a, int64_t m, int64_t w, int64_t lda, int64_t
       if (v > vbest) { v2 = vbest; p2 = pbest; vbest = v; pbest = i; }
       else if (top2 && v > v2) { v2 = v; p2 = i; }
     }
-    if (top2) { top2[3 * j] = vbest; top2[3 * j + 1] = v2; top2[3 * j + 2] = (double)p2; }
+    if (top2) {
+      int64_t nt = 0;
+      const double lim = vbest * (1.0 - 1e-12);
+      for (int64_t i = j; i < m; ++i) nt += fabs(a[IDX(i, j, lda)]) >= lim;
+      top2[4 * j] = vbest; top2[4 * j + 1] = v2; top2[4 * j + 2] = (double)p2; top2[4 * j + 3] = (double)nt;
+    }
     piv[j] = pbest;
     if (vbest == 0.0) {
       if (info == 0) info = j + 1;
@@ -163,7 +169,7 @@ void orc_gemm_sub(double *c, int64_t ldc, const double *a, int64_t lda, const do
 /* Blocked right-looking LUpp (dmf_mtb order, factor.py:382-412): for each panel k: panel
  * factorization (lu_unb on rows col0.., panel width), left swaps on [0, col0), right swaps +
  * trsm + gemm on [col0+bw, n).  m >= n >= 1 (caller validates).  piv: 0-based global rows. */
-/* top2: NULL, or 3 doubles per column (see lu_unb_impl; the runner-up row made global). */
+/* top2: NULL, or 4 doubles per column (see lu_unb_impl; the runner-up row made global). */
 int64_t orc_getrf_steps_top2(double *a, int64_t m, int64_t n, int64_t lda, int64_t b, int64_t *piv,
                              int64_t nsteps, double *top2) {
   int64_t info = 0;
@@ -171,12 +177,12 @@ int64_t orc_getrf_steps_top2(double *a, int64_t m, int64_t n, int64_t lda, int64
   for (int64_t col0 = 0; col0 < n && (nsteps < 0 || step < nsteps); col0 += b, ++step) {
     int64_t bw = n - col0 < b ? n - col0 : b;
     double *panel = a + IDX(col0, col0, lda);
-    int64_t pinfo = lu_unb_impl(panel, m - col0, bw, lda, piv + col0, -1, top2 ? top2 + 3 * col0 : NULL);
+    int64_t pinfo = lu_unb_impl(panel, m - col0, bw, lda, piv + col0, -1, top2 ? top2 + 4 * col0 : NULL);
     if (pinfo && !info) info = col0 + pinfo;
     int64_t kk = (m - col0) < bw ? (m - col0) : bw;
     for (int64_t j = 0; j < kk; ++j) {
       piv[col0 + j] += col0;
-      if (top2 && top2[3 * (col0 + j) + 2] >= 0.0) top2[3 * (col0 + j) + 2] += (double)col0;
+      if (top2 && top2[4 * (col0 + j) + 2] >= 0.0) top2[4 * (col0 + j) + 2] += (double)col0;
     }
     orc_laswp(a, lda, 0, col0, piv, col0, col0 + kk);                 /* left swaps */
     int64_t lo = col0 + bw;

@@ -305,3 +305,32 @@ def test_dmf_la_malleable_runs_la_mb(cuda, golden_small):
     assert out.strategy.name == "LA_MB"
     assert np.array_equal(np.asarray(out.pivots) - 1, golden_small["u300__piv"])
     assert oracle.max_rel_diff(np.ascontiguousarray(out.matrix.array), golden_small["u300__f"], a0) <= 1e-10
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_integer_matrices_exact_ties(cuda, seed):
+    """Small-integer matrices: many candidates tie EXACTLY in the pivot search (the strict '>' scan of
+    _jit.py:163-170 takes the smallest row).  Exact mode must be bitwise the oracle; DMMA mode's pivots
+    must equal the oracle's or first differ at a column whose top-two candidates tie within 1e-12 with
+    the runner-up taken (north_star's tie rule, classified from the instrumented oracle's record)."""
+    from paper_1804_07017_b200 import lu_factor
+
+    rng = np.random.default_rng(100 + seed)
+    n, b = 300, 32
+    a0 = rng.integers(-2, 3, (n, n)).astype(np.float64)
+    a0 += np.eye(n) * 0.5          # keep it nonsingular-ish; ties stay exact in early columns
+    want, wpiv, winfo = oracle.getrf(a0, b)
+    w = np.array(a0, copy=True)
+    piv_t, top2, _ = oracle.getrf_top2_inplace(w, b)
+    assert np.array_equal(piv_t, wpiv) and w.tobytes() == want.tobytes()
+    ties = oracle.near_ties(top2, 1e-6)
+    assert len(ties) > 0                         # the case really has (near-)ties
+    for la in (0, 1):
+        lu, piv, info = lu_factor(a0.copy(), b=b, lookahead=la, exact=True, return_info=True)
+        assert info == winfo and np.array_equal(piv, wpiv) and bitwise_equal(lu, want)
+        lu2, piv2 = lu_factor(a0.copy(), b=b, lookahead=la)
+        verdict = oracle.classify_pivots(piv2, wpiv, ties)
+        assert verdict["ok"], verdict
+        if verdict["equal"]:
+            assert oracle.max_rel_diff(lu2, want, a0) <= 1e-8
+        assert oracle.lu_residual(a0, lu2, piv2) <= 10

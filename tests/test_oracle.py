@@ -134,3 +134,18 @@ def test_top2_record_and_tie_classifier():
     t2 = np.array([[2.0, 2.0 - 1e-12, 5], [1.0, 0.5, 6], [3.0, -1.0, -1]])
     nt = oracle.near_ties(t2, 1e-6)
     assert nt.shape == (1, 4) and nt[0, 0] == 0 and nt[0, 3] == 5
+
+
+def test_top2_counts_exact_ties_and_classifier_accepts_multiway():
+    """Column 0 of an integer matrix with three rows of magnitude 2: the record counts 3 tied candidates,
+    and classify_pivots then accepts any of them (only the runner-up's row is recorded)."""
+    a = np.array([[1.0, 4.0, 0.0, 1.0], [2.0, 1.0, 1.0, 0.0], [-2.0, 0.0, 3.0, 1.0], [2.0, 1.0, 1.0, 5.0]])
+    w = a.copy()
+    piv, top2, info = oracle.getrf_top2_inplace(w, 2)
+    assert piv[0] == 1 and top2[0, 0] == 2.0 and top2[0, 1] == 2.0 and top2[0, 2] == 2 and top2[0, 3] == 3
+    ties = oracle.near_ties(top2, 1e-6)
+    assert ties.shape[1] == 5 and ties[0, 0] == 0 and ties[0, 4] == 3
+    g = piv.copy()
+    g[0] = 3                                   # the third tied row
+    g[1:] = 0
+    assert oracle.classify_pivots(g, piv, ties)["ok"]
