@@ -257,7 +257,7 @@ class _NoTrace:
 
 
 def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, kernels=None, group=None,
-                       piv: torch.Tensor | None = None, row_sink=None, trace=None):
+                       piv: torch.Tensor | None = None, row_sink=None, trace=None, emulate: int = 0):
     """Factor the block-cyclic distributed n x n matrix in place.
 
     ``row_sink(r0, r1, events)`` (CUDA only, optional) is called once per step as soon as local rows
@@ -268,13 +268,21 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
     Returns ``(piv, info)``: the full 0-based pivot vector (identical on every rank) and the
     1-based first zero-pivot column (0 if none), agreed over all ranks.
     ``trace`` (a list, optional) receives this rank's PF / TU / TU_L / TU_R / BCAST records.
+    ``emulate=Q`` (single rank only; the scaling model of tools/emu_scaling.py --driver dist): run the
+    critical path of one rank of a Q-rank job with THIS schedule and kernels -- the rank owns and
+    factors every panel (as each step's owner would, packing it into the message as for a broadcast)
+    but updates only ~1/Q of every trailing matrix and of the left columns; the factors are then not
+    a factorization of the input (timing only).
     """
     P = dist.get_world_size(group)
     r = dist.get_rank(group)
     if kernels is None:
         kernels = CudaKernels(a_loc.device)
+    if emulate and P != 1:
+        raise ValueError("emulate is a single-rank scaling model")
+    Q = max(1, int(emulate or 1))  # the rank count whose critical path runs
     if getattr(kernels, "is_cuda", False) and kernels.grid_rows is None:
-        kernels.grid_rows = kernels.GRID_PANEL_ROWS if P >= kernels.GRID_MIN_RANKS else 1 << 62
+        kernels.grid_rows = kernels.GRID_PANEL_ROWS if max(P, Q) >= kernels.GRID_MIN_RANKS else 1 << 62
     dev = a_loc.device
     if a_loc.shape[0] != n or a_loc.shape[1] != local_cols(n, b, P, r) or a_loc.stride(1) != 1:
         raise ValueError("a_loc must be the row-major local block-cyclic columns (n x local_cols)")
@@ -336,10 +344,16 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
         if col0 + bw < n:
             kernels.gemm(a_loc[col0 + bw:, c0:c1], buf[bw:, :], a_loc[col0: col0 + bw, c0:c1])
 
+    def share(lo, hi):
+        """Emulation: the part of [lo, hi) one of Q ranks updates (~1/Q, block-aligned)."""
+        if Q == 1 or hi <= lo:
+            return hi
+        return min(hi, lo + -(-((hi - lo + Q - 1) // Q) // b) * b)
+
     def left_swaps(k):
         col0 = k * b
         bw = min(b, n - col0)
-        kernels.swap_trsm(a_loc, col0, bw, plans[k % 2], 0, cols_before(k), None)
+        kernels.swap_trsm(a_loc, col0, bw, plans[k % 2], 0, share(0, cols_before(k)), None)
 
     ncl = a_loc.shape[1]
     if lookahead == 0:
@@ -348,7 +362,7 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
                 buf = pf_pack_bcast(k)
                 t = tr.begin("TU", k, "P")
                 left_swaps(k)
-                update(k, buf, cols_before(k + 1), ncl)
+                update(k, buf, cols_before(k + 1), share(cols_before(k + 1), ncl))
                 tr.end(t)
                 if row_sink is not None:
                     e = kernels.event()
@@ -367,7 +381,7 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
             with kernels.stream("U"):
                 kernels.wait(ev_bc[k % 2], "U")
                 t = tr.begin("TU_R", k, "U")
-                update(k, bufs[k], lo_r, ncl)
+                update(k, bufs[k], lo_r, share(lo_r, ncl))
                 left_swaps(k)
                 tr.end(t)
                 kernels.record(ev_tu[k % 2], "U")

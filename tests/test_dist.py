@@ -192,3 +192,29 @@ def test_qr_block_cyclic_matches_oracle_bitwise(tmp_path, world, n, b, lookahead
         assert tau[zero_col] == 0.0
     rf, rtau = oracle.geqrf(a, b)
     assert f.tobytes() == rf.tobytes() and tau.tobytes() == rtau.tobytes()
+
+
+def _emu_worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from dist_oracle_backend import OracleKernels
+    from paper_1804_07017_b200 import dist as pd
+
+    n, b = 96, 16
+    a = torch.from_numpy(np.random.default_rng(0).uniform(-1.0, 1.0, (n, n)))
+    tr = []
+    pd.getrf_block_cyclic(a.clone(), n, b, 1, OracleKernels(), trace=tr, emulate=4)
+    np.save(os.path.join(out_dir, "emu.npy"), np.array([(e.label, e.k) for e in tr], dtype=object), allow_pickle=True)
+    dist.destroy_process_group()
+
+
+def test_block_cyclic_emulation_mode(tmp_path):
+    """emulate=Q (the scaling model on dist.py's own k-loop): one rank factors every panel (PF and TU_L on
+    every step, as each step's owner) and runs TU_R on its share; refused at world size > 1."""
+    mp.spawn(_emu_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    recs = np.load(tmp_path / "emu.npy", allow_pickle=True)
+    labels = [str(r[0]) for r in recs]
+    assert labels.count("PF") == 6 and labels.count("TU_L") == 5 and labels.count("TU_R") == 6
