@@ -102,6 +102,7 @@ static thread_local DevCtx* g_dc = nullptr;  // context of the current call (set
 static int g_leaf = []() { const char* e = getenv("PFLU_LEAF"); return e ? atoi(e) : 0; }();
 // cluster panel: max CTAs per cluster (0 = LL kernel only), min rows per CTA, max panel rows
 static int g_cluster = []() { const char* e = getenv("PFLU_CLUSTER"); return e ? atoi(e) : 16; }();
+static int g_pf_v2 = []() { const char* e = getenv("PFLU_PANEL_V2"); return e ? atoi(e) : 1; }();
 static int g_cl_minrows = []() { const char* e = getenv("PFLU_CL_MINROWS"); return e ? std::max(1, atoi(e)) : 128; }();
 static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
 static int g_trsm_dmma = []() { const char* e = getenv("PFLU_TRSM_DMMA"); return e ? atoi(e) : 1; }();
@@ -190,18 +191,21 @@ static constexpr int PF_MAX_CTAS = PF_THREADS;
 #ifndef PFLU_PANEL_EXACT_RUNTIME
 // the exact flag compiled into the panel kernel (see panel_kernel's EX)
 template <int EX>
-static const void* pf_fn_ex(int W, bool cl) {
+static const void* pf_fn_ex(int W, bool cl, bool v2) {
+  if (cl && v2) return W == 8 ? (const void*)panel_kernel<8, true, EX, true> : W == 16 ? (const void*)panel_kernel<16, true, EX, true>
+                                                                                   : (const void*)panel_kernel<32, true, EX, true>;
   if (cl) return W == 8 ? (const void*)panel_kernel<8, true, EX> : W == 16 ? (const void*)panel_kernel<16, true, EX>
                                                                            : (const void*)panel_kernel<32, true, EX>;
   return W == 8 ? (const void*)panel_kernel<8, false, EX> : W == 16 ? (const void*)panel_kernel<16, false, EX>
                                                                     : (const void*)panel_kernel<32, false, EX>;
 }
-static const void* pf_fn(int W, bool cl, bool exact = false) {
-  return exact ? pf_fn_ex<1>(W, cl) : pf_fn_ex<0>(W, cl);
+static const void* pf_fn(int W, bool cl, bool exact = false, bool v2 = false) {
+  return exact ? pf_fn_ex<1>(W, cl, v2) : pf_fn_ex<0>(W, cl, v2);
 }
 #else
-static const void* pf_fn(int W, bool cl, bool exact = false) {
+static const void* pf_fn(int W, bool cl, bool exact = false, bool v2 = false) {
   (void)exact;
+  (void)v2;
   if (cl) return W == 8 ? (const void*)panel_kernel<8, true> : W == 16 ? (const void*)panel_kernel<16, true>
                                                                        : (const void*)panel_kernel<32, true>;
   return W == 8 ? (const void*)panel_kernel<8, false> : W == 16 ? (const void*)panel_kernel<16, false>
@@ -258,10 +262,12 @@ static int ctx_get(DevCtx** out) {
     };
     for (int W : {8, 16, 32})
       for (bool cl : {false, true})
-        for (bool ex : {false, true}) {
-          CK(allow(pf_fn(W, cl, ex)));
-          if (cl) CK(cudaFuncSetAttribute(pf_fn(W, cl, ex), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        }
+        for (bool ex : {false, true})
+          for (bool v2 : {false, true}) {
+            if (v2 && !cl) continue;
+            CK(allow(pf_fn(W, cl, ex, v2)));
+            if (cl) CK(cudaFuncSetAttribute(pf_fn(W, cl, ex, v2), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+          }
     CK(allow((const void*)swap_trsm_kernel<8>));
     CK(allow((const void*)swap_trsm_dmma_kernel<256, 32>));
     CK(allow((const void*)swap_trsm_dmma_kernel<256, 16>));
@@ -723,7 +729,8 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
       cfg.attrs = at;
       cfg.numAttrs = 1;
       void* args[] = {&p};
-      CK(cudaLaunchKernelExC(&cfg, pf_fn(W, true, opt.exact != 0), args));
+      // peers: the v2 leaf (dedicated exchange warp, per-warp candidates); a one-CTA cluster has no exchange
+      CK(cudaLaunchKernelExC(&cfg, pf_fn(W, true, opt.exact != 0, g_pf_v2 != 0 && S > 1), args));
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return PFLU_OK;
     }

@@ -194,8 +194,9 @@ struct PanelSmem {
   static size_t bytes(int64_t R, int w, bool cl = false) {
     // tile R x LD, U buffer, L block KM x KM, u / dg W each, plan 4W ints
     // (+ cluster mode: keys [2][PF_CL_MAX][2], published rows [2][W] x 2, 2 mbarriers, alignment)
+    // (v2 exchange: keys [2][PF_CL_MAX][8 slots][2], published rows [2][8 slots][W], diagonal rows [2][W])
     return (size_t)(R * LD + ubuf_doubles(w) + KM * KM + 4 * W) * 8 + 4 * W * 8 + 256 +
-           (cl ? (size_t)(4 * PF_CL_MAX + 4 * W + 2 + 2) * 8 : 0);
+           (cl ? (size_t)(32 * PF_CL_MAX + 18 * W + 2 + 2) * 8 : 0);
   }
   // row-swap staging that would make the cluster kernel's deferred swaps a single batch
   static int64_t swap_doubles(int w) { return (int64_t)2 * W * (w > W ? w - W : 1); }
@@ -208,8 +209,12 @@ struct PanelSmem {
 // EX: 0 / 1 = the exact flag compiled in (production since round 2: DMMA mode's in-leaf updates are
 // single FMAs; this specialisation exposed the zero-pivot reconvergence hazard fixed below);
 // -1 = read at run time from p.exact (-DPFLU_PANEL_EXACT_RUNTIME, the round-1 build).
-template <int W, bool CL, int EX = -1>
+// V2 (cluster kernel with peers only): the per-column exchange is run by a dedicated warp (warp 0) while
+// warps 1..7 own fixed rows; every WORKER WARP pushes its own candidate straight to every peer (no CTA-level
+// arg-max, no block barrier inside a column) -- see the V2 leaf below.
+template <int W, bool CL, int EX = -1, bool V2 = false>
 __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
+  static_assert(!V2 || CL, "the v2 leaf is a cluster exchange");
   extern __shared__ __align__(16) double pf_smem[];
   constexpr int LD = W + 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -230,8 +235,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   // CL: keys pushed by the peers (16-byte aligned for st.async), own published candidate / diagonal
   // rows (pulled by the peers with DSMEM loads), mbarriers; all double-buffered by exchange parity
   double* xkey = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(plan_src_row + 2 * W) + 15) & ~(uintptr_t)15);
-  double* pubrow = xkey + 2 * PF_CL_MAX * 2;  // [2][W]
-  double* pubdiag = pubrow + 2 * W;           // [2][W]
+  double* pubrow = xkey + (V2 ? 2 * PF_CL_MAX * 8 * 2 : 2 * PF_CL_MAX * 2);  // [2][W] (v2: [2][8 slots][W])
+  double* pubdiag = pubrow + (V2 ? 16 * W : 2 * W);                          // [2][W]
   unsigned long long* xbar = reinterpret_cast<unsigned long long*>(pubdiag + 2 * W);  // [2]
   double* swbuf = reinterpret_cast<double*>(xbar + 2);  // CL: p.swcap doubles (may be 0)
   unsigned xs = 0;  // CL: exchanges so far (uniform over the cluster): buffer xs & 1, phase (xs >> 1) & 1
@@ -250,6 +255,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   __shared__ long long blk_piv[32];  // pivots of the current block (every CTA knows them)
   __shared__ double s_wkey;          // winner of the next column (written by warp 0)
   __shared__ long long s_wrow;
+  __shared__ double s_wkey2[2], s_rpiv2[2];  // v2: winner key, reciprocal of the pivot, per exchange parity
+  __shared__ int s_wrow2[2];                 // v2: winner row as an offset from p.r0
 
   const unsigned epoch = CL ? 0u : *(volatile unsigned*)p.epoch;
   if (p.sm_mask && tid == 0) {
@@ -333,6 +340,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     // warp 0; the next diagonal row by warp 1) -> (pass 2) remaining columns, overlapping the
     // exchange.  Every row is owned by one thread, so the swap needs no barrier.
     const int kmax = (int)min((int64_t)wb, p.m - cJ);
+    if constexpr (!V2) {
     auto cta_best = [&](double& bk, long long& br) {
       warp_best(bk, br);
       PF_PROF_MARK(11);
@@ -639,6 +647,197 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       if (nxt) ++xs;
       if (!CL && g_resync > 0 && nxt && ((j + 1) % g_resync) == 0)
         ll_grid_align(sync_words, S, q, sync_flag());
+    }
+    } else {
+      // ---------------- 2 (v2). leaf with a dedicated exchange warp
+      // Warps 1..7 ("workers") own fixed rows of the tile (local row rl -> worker thread rl % 224) through
+      // both passes, so nothing inside a column needs a block barrier: per column a worker warp runs pass 1
+      // on its rows, takes its OWN candidate (warp arg-max), finishes that row (and the next diagonal row
+      // when it owns it), copies it to its publish slot and pushes (key, row) to every peer -- 7 keys per
+      // CTA -- then runs pass 2 and waits on named barrier 2 for the winner.  Warp 0 ("exchange") waits for
+      // the S x 7 keys, reduces them, pulls the winner row (and the old diagonal row when this CTA owns the
+      // winner) from the owners' publish slots, forms the pivot's reciprocal while the pull is in flight,
+      // writes (winner, row, 1 / pivot) for the workers and arrives on barrier 2.  Everything is double
+      // buffered by exchange parity (xs & 1): a buffer is rewritten two exchanges later, which every peer
+      // can only reach after the exchange in between -- i.e. after all readers of the old contents are done.
+      constexpr int NWK = PF_THREADS / 32 - 1, NT2 = NWK * 32;
+      constexpr unsigned FULL = 0xffffffffu;
+      const int base = (int)(rbeg - p.r0);  // row offsets from p.r0 fit 32 bits
+      if (warp > 0) {
+        const int wt = tid - 32, ws = warp - 1;
+        auto own_warp = [&](int rl) { return (int)(((unsigned)rl % (unsigned)NT2) >> 5); };
+        auto first_row = [&](int p1) { return p1 <= wt ? wt : wt + (int)(((unsigned)(p1 - wt) + NT2 - 1) / NT2) * NT2; };
+        // this warp's candidate row crl (key ck; none if ck < -2) and, when the warp owns it, the next
+        // diagonal row dl: finished for column j (fin), copied to the publish slots, then the key goes out
+        auto publish = [&](double ck, int crl, int dl, bool fin, int j, const double* ucur) {
+          const int buf = xs & 1;
+          const bool have = ck > -2.0;
+          if (have && lane < wb) {
+            double* tr = tile + crl * LD;
+            double v = tr[lane];
+            if (fin && lane >= j + 2) {
+              v = upd(v, tr[j], ucur[lane]);
+              tr[lane] = v;
+            }
+            pubrow[(buf * 8 + ws) * W + lane] = v;
+          }
+          if (dl >= 0 && dl < nrows && own_warp(dl) == ws && lane < wb) {
+            double* tr = tile + dl * LD;
+            double v = tr[lane];
+            if (fin && lane >= j + 2 && !(have && crl == dl)) {
+              v = upd(v, tr[j], ucur[lane]);
+              tr[lane] = v;
+            }
+            pubdiag[buf * W + lane] = v;
+          }
+          __syncwarp();
+          if (lane < S)
+            cl_put16(cl_map(smem_addr(xkey + ((buf * PF_CL_MAX + q) * 8 + ws) * 2), lane),
+                     (unsigned long long)__double_as_longlong(ck), (unsigned long long)(have ? rbeg + crl : 0),
+                     cl_map(smem_addr(xbar + buf), lane));
+          ++xs;
+        };
+        // candidate of column jn from the current tile (block start, or after a zero pivot); dl = local
+        // index of that column's diagonal row
+        auto cand_tile = [&](int jn, int dl) {
+          double ck = -3.0;
+          int crl = INT_MAX;
+          for (int r = first_row(max(0, dl)); r < nrows; r += NT2) {
+            const double k = pivot_key(tile[r * LD + jn], r == dl);
+            if (k > ck || (k == ck && r < crl)) { ck = k; crl = r; }
+          }
+          long long cr = crl;
+          warp_best(ck, cr);
+          publish(ck, (int)cr, dl, false, 0, nullptr);
+        };
+        const int cl0 = (int)max((int64_t)-(1 << 30), min((int64_t)(1 << 30), cJ - rbeg));  // local row of column 0's diagonal
+        if (kmax > 0) cand_tile(0, cl0);
+        for (int j = 0; j < kmax; ++j) {
+          __syncwarp();
+          asm volatile("bar.sync 2, 256;\n" ::: "memory");
+          const int rb = (xs - 1) & 1;
+          const double wkey = s_wkey2[rb];
+          const double* ucur = u + rb * W;
+          const double* dcur = dg + rb * W;
+          const bool nxt = j + 1 < kmax;
+          const int cl = cl0 + j;  // local index of the diagonal row (any sign)
+          if (!(wkey > 0.0)) {     // exactly-zero pivot: column untouched (_jit.py:171-174)
+            if (nxt) cand_tile(j + 1, cl + 1);
+            continue;
+          }
+          const int prl = s_wrow2[rb] - base;  // local index of the pivot row (>= cl)
+          if (prl != cl) {  // swap: the winner row into the diagonal row, the old diagonal row into the winner's
+            if (cl >= 0 && cl < nrows && own_warp(cl) == ws && lane < wb) tile[cl * LD + lane] = ucur[lane];
+            if (prl >= 0 && prl < nrows && own_warp(prl) == ws && lane < wb) tile[prl * LD + lane] = dcur[lane];
+            __syncwarp();
+          }
+          const double pivot = ucur[j];
+          const double uj1 = (j + 1 < wb) ? ucur[j + 1] : 0.0;
+          const double rpiv = EX == 0 ? s_rpiv2[rb] : 0.0;
+          const int p1 = max(0, min(cl + 1, nrows));
+          const int r1 = first_row(p1);
+          double ck = -3.0;
+          int crl = INT_MAX;
+          for (int r = r1; r < nrows; r += NT2) {  // pass 1: scale, column j+1, its candidate
+            double* tr = tile + r * LD;
+            const double l = EX == 0 ? tr[j] * rpiv : __ddiv_rn(tr[j], pivot);
+            tr[j] = l;
+            if (j + 1 < wb) {
+              const double x = upd(tr[j + 1], l, uj1);
+              tr[j + 1] = x;
+              if (nxt) {
+                const double k = pivot_key(x, r == cl + 1);
+                if (k > ck || (k == ck && r < crl)) { ck = k; crl = r; }
+              }
+            }
+          }
+          int skip_c = -1, skip_d = -1;
+          if (nxt) {
+            long long cr = crl;
+            warp_best(ck, cr);
+            publish(ck, (int)cr, cl + 1, true, j, ucur);
+            if (ck > -2.0) skip_c = (int)cr;
+            if (cl + 1 >= 0 && cl + 1 < nrows && own_warp(cl + 1) == ws) skip_d = cl + 1;
+          }
+          if (j + 2 < wb) {  // pass 2: the remaining columns of the thread's own rows
+            for (int r = r1; r < nrows; r += NT2) {
+              if (r == skip_c || r == skip_d) continue;
+              double* tr = tile + r * LD;
+              const double l = tr[j];
+              int cc = j + 2;
+              for (; cc + 3 < wb; cc += 4) {
+                const double a0 = tr[cc], a1 = tr[cc + 1], a2 = tr[cc + 2], a3 = tr[cc + 3];
+                const double u0 = ucur[cc], u1 = ucur[cc + 1], u2 = ucur[cc + 2], u3 = ucur[cc + 3];
+                tr[cc] = upd(a0, l, u0);
+                tr[cc + 1] = upd(a1, l, u1);
+                tr[cc + 2] = upd(a2, l, u2);
+                tr[cc + 3] = upd(a3, l, u3);
+              }
+              for (; cc < wb; ++cc) tr[cc] = upd(tr[cc], l, ucur[cc]);
+            }
+          }
+        }
+      } else {
+        // exchange warp: lane handles peer CTA lane / 2, worker slots 4 * (lane & 1) .. + 3
+        const int R32 = (int)p.R;
+        int qd = jb / R32, rem = jb - qd * R32;  // owner CTA of the diagonal row of column jn, kept incrementally
+        for (int jn = 0; jn < kmax; ++jn) {
+          const int buf = xs & 1;
+          const uint32_t bar = smem_addr(xbar + buf);
+          if (lane == 0) cl_expect(bar, (unsigned)(S * NWK) * 16u);
+          cl_wait(bar, (xs >> 1) & 1u);
+          double bk = -3.0;
+          long long br = LLONG_MAX;
+          int bslot = 0;
+          if ((lane >> 1) < S) {
+            const int s0 = (lane & 1) * 4;
+            const double* kk = xkey + ((buf * PF_CL_MAX + (lane >> 1)) * 8 + s0) * 2;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              if (s0 + s < NWK) {
+                const double k = kk[2 * s];
+                const long long rr = __double_as_longlong(kk[2 * s + 1]);
+                if (k > -2.0 && key_better(k, rr, bk, br)) { bk = k; br = rr; bslot = s0 + s; }
+              }
+            }
+          }
+          const int wl = warp_best(bk, br);
+          bslot = __shfl_sync(FULL, bslot, wl);
+          const int noff = jb + jn;  // offset of this column's diagonal row from p.r0
+          const int broff = bk > 0.0 ? (int)(br - p.r0) : noff;
+          if (bk > 0.0) {
+            const int bl = broff - base;
+            const bool need_d = bl >= 0 && bl < nrows && broff != noff;
+            const uint32_t ra = cl_map(smem_addr(pubrow + (buf * 8 + bslot) * W), wl >> 1);
+            const uint32_t rd = cl_map(smem_addr(pubdiag + buf * W), qd);
+            double x = 0.0, y = 0.0;
+            if (lane < wb) {
+              asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(x) : "r"(ra + 8 * lane) : "memory");
+              if (need_d) asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(y) : "r"(rd + 8 * lane) : "memory");
+            }
+            const double rp = EX == 0 ? 1.0 / bk : 0.0;  // |pivot| is the key: the division overlaps the pull
+            if (lane < wb) {
+              u[buf * W + lane] = x;
+              if (need_d) dg[buf * W + lane] = y;
+            }
+            const double pv = __shfl_sync(FULL, x, jn);
+            if (lane == 0) s_rpiv2[buf] = (pv != pv) ? pv : copysign(rp, pv);
+          }
+          if (lane == 0) {
+            s_wkey2[buf] = bk;
+            s_wrow2[buf] = broff;
+            blk_piv[jn] = p.r0 + broff;
+            if (q == 0) {
+              p.piv[cJ + jn] = p.r0 + broff;
+              if (!(bk > 0.0)) atomicMin(p.info, (unsigned long long)(cJ + jn + 1));
+            }
+          }
+          __syncwarp();
+          asm volatile("bar.arrive 2, 256;\n" ::: "memory");
+          ++xs;
+          if (++rem == R32) { rem = 0; ++qd; }
+        }
+      }
     }
     __syncthreads();
     // ---------------- 3. write back own rows >= cJ of the block
