@@ -85,6 +85,33 @@ __device__ __forceinline__ int warp_best(double& k, long long& r) {
   return src;
 }
 
+// Integer pivot keys (the v2 panel exchange): order-preserving for |x|, with "no candidate" < NaN off the
+// diagonal < every magnitude; a NaN on the diagonal ranks as +inf (the scan of _jit.py:163-170 keeps it).
+constexpr unsigned long long ORD_NONE = 0ull, ORD_NAN = 1ull, ORD_ZERO = 0x8000000000000000ull;
+__device__ __forceinline__ unsigned long long pivot_key_ord(double x, bool is_diag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+  if (b > 0x7ff0000000000000ull) return is_diag ? 0xfff0000000000000ull : ORD_NAN;
+  return b | ORD_ZERO;
+}
+// Warp max of a 96-bit (hi, mid, lo) tuple, lexicographic: three redux.sync, the result lands in every
+// lane (uniform registers) without shuffles or a tie branch.  The v2 panel exchange packs (integer key,
+// ~row) so that the largest tuple is the largest key and, among equal keys, the smallest row.
+__device__ __forceinline__ void warp_max96(unsigned& h, unsigned& m, unsigned& l) {
+  const unsigned full = 0xffffffffu;
+  __syncwarp();
+  const unsigned mh = __reduce_max_sync(full, h);
+  const bool e1 = h == mh;
+  const unsigned mm = __reduce_max_sync(full, e1 ? m : 0u);
+  const unsigned ml = __reduce_max_sync(full, (e1 & (m == mm)) ? l : 0u);
+  h = mh; m = mm; l = ml;
+}
+// branch-free lane-local max of two such tuples
+__device__ __forceinline__ void max96(unsigned long long& K, unsigned& l, unsigned long long K2, unsigned l2) {
+  const bool gt = (K2 > K) | ((K2 == K) & (l2 > l));
+  K = gt ? K2 : K;
+  l = gt ? l2 : l;
+}
+
 // ==========================================================================================
 // Pivot plan: composes the ascending LAPACK swaps piv[d..d+np) (global 0-based rows, piv[i] >= i)
 // into a gather.  Output layout (int64): [0] = E (extra rows), [1 .. np] = source row of top row

@@ -56,6 +56,9 @@ struct PanelArgs {
 // coarse, ~1 us: a sleep on the critical path costs a column's worth of time)
 constexpr int PF_POLL_SPINS = 64;
 
+// per-phase clock totals (tools/panel_prof.py): compiled in only with -DPFLU_PANEL_PROF (the 16 counters
+// cost 32 registers in a kernel that already sits at the 255-register limit)
+#ifdef PFLU_PANEL_PROF
 #define PF_PROF_MARK(i)                                              \
   do {                                                              \
     if (prof_on) {                                                  \
@@ -64,6 +67,9 @@ constexpr int PF_POLL_SPINS = 64;
       prof_t = _t;                                                  \
     }                                                               \
   } while (0)
+#else
+#define PF_PROF_MARK(i) do { } while (0)
+#endif
 
 // LL words: high 32 bits = flag, low 32 bits = payload
 __device__ __forceinline__ void ll_put(unsigned long long* p, unsigned payload, unsigned flag) {
@@ -176,6 +182,17 @@ __device__ __forceinline__ void cl_wait(uint32_t bar, unsigned parity) {
                  "selp.u32 %0, 1, 0, p;\n}\n" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
   }
 }
+// The same wait with CTA-scope acquire: enough for data that st.async delivered into THIS CTA's shared
+// memory (its complete_tx is what the phase waits for) and for reads of peers' shared memory afterwards
+// (DSMEM is not cached); the cluster-scope form above makes ptxas emit CCTL.IVALL (an L1 invalidate,
+// hundreds of cycles) after every successful wait.
+__device__ __forceinline__ void cl_wait_cta(uint32_t bar, unsigned parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 "selp.u32 %0, 1, 0, p;\n}\n" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  }
+}
 // all threads of all CTAs of the cluster; release/acquire at cluster scope (global data included)
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -234,7 +251,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   long long* plan_src_row = plan_row + 2 * W;                       // [2W] slot -> source row
   // CL: keys pushed by the peers (16-byte aligned for st.async), own published candidate / diagonal
   // rows (pulled by the peers with DSMEM loads), mbarriers; all double-buffered by exchange parity
-  double* xkey = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(plan_src_row + 2 * W) + 15) & ~(uintptr_t)15);
+  // (offset arithmetic on pf_smem keeps the shared address space: LDS/STS instead of generic accesses)
+  double* xkey = pf_smem + ((p.R * LD + PanelSmem<W>::ubuf_doubles(w) + PanelSmem<W>::KM * PanelSmem<W>::KM + 8 * W + 1) & ~(int64_t)1);
   double* pubrow = xkey + (V2 ? 2 * PF_CL_MAX * 8 * 2 : 2 * PF_CL_MAX * 2);  // [2][W] (v2: [2][8 slots][W])
   double* pubdiag = pubrow + (V2 ? 16 * W : 2 * W);                          // [2][W]
   unsigned long long* xbar = reinterpret_cast<unsigned long long*>(pubdiag + 2 * W);  // [2]
@@ -255,8 +273,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   __shared__ long long blk_piv[32];  // pivots of the current block (every CTA knows them)
   __shared__ double s_wkey;          // winner of the next column (written by warp 0)
   __shared__ long long s_wrow;
-  __shared__ double s_wkey2[2], s_rpiv2[2];  // v2: winner key, reciprocal of the pivot, per exchange parity
-  __shared__ int s_wrow2[2];                 // v2: winner row as an offset from p.r0
+  __shared__ double s_rpiv2[2];  // v2: reciprocal of the pivot (DMMA mode), per exchange parity
+  __shared__ int s_wrow2[2];     // v2: winner row as an offset from p.r0; -1 = no non-zero pivot
 
   const unsigned epoch = CL ? 0u : *(volatile unsigned*)p.epoch;
   if (p.sm_mask && tid == 0) {
@@ -276,9 +294,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     else return sub_mul_exact(x, l, u);
   };
   const int g_resync = p.resync;
-  const bool prof_on = p.prof != nullptr && tid == 0;
+#ifdef PFLU_PANEL_PROF
+  const bool prof_on = p.prof != nullptr && (tid == 0 || (V2 && tid == 32));  // v2: exchange warp + one worker
   long long prof_t = clock64();
   long long prof_acc[16] = {};
+#endif
 
   // grid-sync flags: epoch + w + (running count of syncs in this launch); the sync sequence is the same
   // on every CTA, and the epoch advance below exceeds w + the sync count
@@ -663,15 +683,22 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       constexpr int NWK = PF_THREADS / 32 - 1, NT2 = NWK * 32;
       constexpr unsigned FULL = 0xffffffffu;
       const int base = (int)(rbeg - p.r0);  // row offsets from p.r0 fit 32 bits
+      // Messages, 16 bytes per worker warp: (integer key, ~((row offset from p.r0) << 7 | CTA << 3 | worker
+      // slot)); the largest (key, word) tuple is the largest key and, among equal keys, the smallest row.
       if (warp > 0) {
         const int wt = tid - 32, ws = warp - 1;
         auto own_warp = [&](int rl) { return (int)(((unsigned)rl % (unsigned)NT2) >> 5); };
         auto first_row = [&](int p1) { return p1 <= wt ? wt : wt + (int)(((unsigned)(p1 - wt) + NT2 - 1) / NT2) * NT2; };
-        // this warp's candidate row crl (key ck; none if ck < -2) and, when the warp owns it, the next
+        // lane t pushes to peer t: its key slot and mbarrier in that peer, per parity
+        const int peer = lane < S ? lane : 0;
+        const uint32_t rk0 = cl_map(smem_addr(xkey + ((0 * PF_CL_MAX + q) * 8 + ws) * 2), peer);
+        const uint32_t rk1 = cl_map(smem_addr(xkey + ((1 * PF_CL_MAX + q) * 8 + ws) * 2), peer);
+        const uint32_t rb0 = cl_map(smem_addr(xbar), peer), rb1 = cl_map(smem_addr(xbar + 1), peer);
+        // this warp's candidate row crl (key K; none if K == ORD_NONE) and, when the warp owns it, the next
         // diagonal row dl: finished for column j (fin), copied to the publish slots, then the key goes out
-        auto publish = [&](double ck, int crl, int dl, bool fin, int j, const double* ucur) {
+        auto publish = [&](unsigned long long K, int crl, int dl, bool fin, int j, const double* ucur) {
           const int buf = xs & 1;
-          const bool have = ck > -2.0;
+          const bool have = K != ORD_NONE;
           if (have && lane < wb) {
             double* tr = tile + crl * LD;
             double v = tr[lane];
@@ -692,40 +719,47 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           }
           __syncwarp();
           if (lane < S)
-            cl_put16(cl_map(smem_addr(xkey + ((buf * PF_CL_MAX + q) * 8 + ws) * 2), lane),
-                     (unsigned long long)__double_as_longlong(ck), (unsigned long long)(have ? rbeg + crl : 0),
-                     cl_map(smem_addr(xbar + buf), lane));
+            cl_put16(buf ? rk1 : rk0, K,
+                     (unsigned long long)(have ? ~((unsigned)(base + crl) << 7 | (unsigned)(q << 3 | ws)) : 0u),
+                     buf ? rb1 : rb0);
           ++xs;
         };
         // candidate of column jn from the current tile (block start, or after a zero pivot); dl = local
         // index of that column's diagonal row
         auto cand_tile = [&](int jn, int dl) {
-          double ck = -3.0;
-          int crl = INT_MAX;
+          unsigned long long K = ORD_NONE;
+          unsigned crl = ~0u;
+#pragma unroll 1
           for (int r = first_row(max(0, dl)); r < nrows; r += NT2) {
-            const double k = pivot_key(tile[r * LD + jn], r == dl);
-            if (k > ck || (k == ck && r < crl)) { ck = k; crl = r; }
+            const unsigned long long k = pivot_key_ord(tile[r * LD + jn], r == dl);
+            if (k > K) { K = k; crl = (unsigned)r; }  // rows ascend: strict '>' keeps the smallest row
           }
-          long long cr = crl;
-          warp_best(ck, cr);
-          publish(ck, (int)cr, dl, false, 0, nullptr);
+          {
+            unsigned h = (unsigned)(K >> 32), m = (unsigned)K, l = ~crl;
+            warp_max96(h, m, l);
+            K = ((unsigned long long)h << 32) | m;
+            crl = ~l;
+          }
+          publish(K, (int)crl, dl, false, 0, nullptr);
         };
         const int cl0 = (int)max((int64_t)-(1 << 30), min((int64_t)(1 << 30), cJ - rbeg));  // local row of column 0's diagonal
         if (kmax > 0) cand_tile(0, cl0);
+        int r1 = first_row(max(0, min(cl0 + 1, nrows)));  // this thread's first row below the diagonal, kept per column
         for (int j = 0; j < kmax; ++j) {
+          PF_PROF_MARK(5);
           __syncwarp();
           asm volatile("bar.sync 2, 256;\n" ::: "memory");
           const int rb = (xs - 1) & 1;
-          const double wkey = s_wkey2[rb];
+          const double rpiv = s_rpiv2[rb];  // 0 exactly when the column has no pivot (key <= 0)
           const double* ucur = u + rb * W;
           const double* dcur = dg + rb * W;
           const bool nxt = j + 1 < kmax;
           const int cl = cl0 + j;  // local index of the diagonal row (any sign)
-          if (!(wkey > 0.0)) {     // exactly-zero pivot: column untouched (_jit.py:171-174)
+          const int prl = s_wrow2[rb] - base;  // local index of the pivot row (>= cl); < 0 marks a zero pivot
+          if (s_wrow2[rb] < 0) {               // exactly-zero pivot: column untouched (_jit.py:171-174)
             if (nxt) cand_tile(j + 1, cl + 1);
             continue;
           }
-          const int prl = s_wrow2[rb] - base;  // local index of the pivot row (>= cl)
           if (prl != cl) {  // swap: the winner row into the diagonal row, the old diagonal row into the winner's
             if (cl >= 0 && cl < nrows && own_warp(cl) == ws && lane < wb) tile[cl * LD + lane] = ucur[lane];
             if (prl >= 0 && prl < nrows && own_warp(prl) == ws && lane < wb) tile[prl * LD + lane] = dcur[lane];
@@ -733,11 +767,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           }
           const double pivot = ucur[j];
           const double uj1 = (j + 1 < wb) ? ucur[j + 1] : 0.0;
-          const double rpiv = EX == 0 ? s_rpiv2[rb] : 0.0;
-          const int p1 = max(0, min(cl + 1, nrows));
-          const int r1 = first_row(p1);
-          double ck = -3.0;
-          int crl = INT_MAX;
+          if (r1 < cl + 1) r1 += NT2;  // the diagonal moves down one row per column
+          if (rpiv == 123.456) PF_PROF_MARK(15);  // (forces the result loads before the mark)
+          PF_PROF_MARK(3);
+          unsigned long long K = ORD_NONE;
+          unsigned crl = ~0u;
+#pragma unroll 1
           for (int r = r1; r < nrows; r += NT2) {  // pass 1: scale, column j+1, its candidate
             double* tr = tile + r * LD;
             const double l = EX == 0 ? tr[j] * rpiv : __ddiv_rn(tr[j], pivot);
@@ -746,25 +781,34 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
               const double x = upd(tr[j + 1], l, uj1);
               tr[j + 1] = x;
               if (nxt) {
-                const double k = pivot_key(x, r == cl + 1);
-                if (k > ck || (k == ck && r < crl)) { ck = k; crl = r; }
+                const unsigned long long k = pivot_key_ord(x, r == cl + 1);
+                if (k > K) { K = k; crl = (unsigned)r; }
               }
             }
           }
           int skip_c = -1, skip_d = -1;
+          PF_PROF_MARK(10);
           if (nxt) {
-            long long cr = crl;
-            warp_best(ck, cr);
-            publish(ck, (int)cr, cl + 1, true, j, ucur);
-            if (ck > -2.0) skip_c = (int)cr;
+            {
+              unsigned h = (unsigned)(K >> 32), m = (unsigned)K, l = ~crl;
+              warp_max96(h, m, l);
+              K = ((unsigned long long)h << 32) | m;
+              crl = ~l;
+            }
+            PF_PROF_MARK(11);
+            publish(K, (int)crl, cl + 1, true, j, ucur);
+            PF_PROF_MARK(2);
+            if (K != ORD_NONE) skip_c = (int)crl;
             if (cl + 1 >= 0 && cl + 1 < nrows && own_warp(cl + 1) == ws) skip_d = cl + 1;
           }
           if (j + 2 < wb) {  // pass 2: the remaining columns of the thread's own rows
+#pragma unroll 1
             for (int r = r1; r < nrows; r += NT2) {
               if (r == skip_c || r == skip_d) continue;
               double* tr = tile + r * LD;
               const double l = tr[j];
               int cc = j + 2;
+#pragma unroll 1
               for (; cc + 3 < wb; cc += 4) {
                 const double a0 = tr[cc], a1 = tr[cc + 1], a2 = tr[cc + 2], a3 = tr[cc + 3];
                 const double u0 = ucur[cc], u1 = ucur[cc + 1], u2 = ucur[cc + 2], u3 = ucur[cc + 3];
@@ -778,63 +822,81 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           }
         }
       } else {
-        // exchange warp: lane handles peer CTA lane / 2, worker slots 4 * (lane & 1) .. + 3
+        // exchange warp: lane handles peer CTA lane / 2, worker slots 4 * (lane & 1) .. + 3.  One warp runs
+        // this chain once per column, so its length in instructions is the panel's per-column latency.
         const int R32 = (int)p.R;
         int qd = jb / R32, rem = jb - qd * R32;  // owner CTA of the diagonal row of column jn, kept incrementally
+        const int s0 = (lane & 1) * 4;
+        const bool lane_on = (lane >> 1) < S;
+        const uint32_t key_a = smem_addr(xkey + ((lane >> 1) * 8 + s0) * 2);  // + buf * PF_CL_MAX * 128 bytes
+        const uint32_t pub_a = smem_addr(pubrow) + 8 * lane, dia_a = smem_addr(pubdiag) + 8 * lane;
+        if (kmax > 0 && lane == 0) cl_expect(smem_addr(xbar + (xs & 1)), (unsigned)(S * NWK) * 16u);
         for (int jn = 0; jn < kmax; ++jn) {
           const int buf = xs & 1;
-          const uint32_t bar = smem_addr(xbar + buf);
-          if (lane == 0) cl_expect(bar, (unsigned)(S * NWK) * 16u);
-          cl_wait(bar, (xs >> 1) & 1u);
-          double bk = -3.0;
-          long long br = LLONG_MAX;
-          int bslot = 0;
-          if ((lane >> 1) < S) {
-            const int s0 = (lane & 1) * 4;
-            const double* kk = xkey + ((buf * PF_CL_MAX + (lane >> 1)) * 8 + s0) * 2;
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-              if (s0 + s < NWK) {
-                const double k = kk[2 * s];
-                const long long rr = __double_as_longlong(kk[2 * s + 1]);
-                if (k > -2.0 && key_better(k, rr, bk, br)) { bk = k; br = rr; bslot = s0 + s; }
-              }
-            }
+          PF_PROF_MARK(4);
+          cl_wait_cta(smem_addr(xbar + buf), (xs >> 1) & 1u);
+          PF_PROF_MARK(13);
+          unsigned long long K0 = ORD_NONE, K1 = ORD_NONE, K2 = ORD_NONE, K3 = ORD_NONE, y0 = 0, y1 = 0, y2 = 0, y3 = 0;
+          if (lane_on) {
+            const uint32_t ka = key_a + buf * (PF_CL_MAX * 8 * 16);
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];\n" : "=l"(K0), "=l"(y0) : "r"(ka) : "memory");
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];\n" : "=l"(K1), "=l"(y1) : "r"(ka + 16) : "memory");
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];\n" : "=l"(K2), "=l"(y2) : "r"(ka + 32) : "memory");
+            if (s0 + 3 < NWK) asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];\n" : "=l"(K3), "=l"(y3) : "r"(ka + 48) : "memory");
           }
-          const int wl = warp_best(bk, br);
-          bslot = __shfl_sync(FULL, bslot, wl);
+          unsigned l0 = (unsigned)y0, l1 = (unsigned)y1, l2 = (unsigned)y2, l3 = (unsigned)y3;
+          max96(K0, l0, K1, l1);
+          max96(K2, l2, K3, l3);
+          max96(K0, l0, K2, l2);
+          unsigned bh = (unsigned)(K0 >> 32), bm = (unsigned)K0, bl = l0;
+          warp_max96(bh, bm, bl);
+          PF_PROF_MARK(14);
+          const unsigned r32 = ~bl;
           const int noff = jb + jn;  // offset of this column's diagonal row from p.r0
-          const int broff = bk > 0.0 ? (int)(br - p.r0) : noff;
-          if (bk > 0.0) {
-            const int bl = broff - base;
-            const bool need_d = bl >= 0 && bl < nrows && broff != noff;
-            const uint32_t ra = cl_map(smem_addr(pubrow + (buf * 8 + bslot) * W), wl >> 1);
-            const uint32_t rd = cl_map(smem_addr(pubdiag + buf * W), qd);
+          const bool ok = bh > 0x80000000u || (bh == 0x80000000u && bm != 0u);  // key > ORD_ZERO: a non-zero pivot
+          const int broff = ok ? (int)(r32 >> 7) : noff;
+          if (ok) {
+            const int bloc = broff - base;
+            const bool need_d = bloc >= 0 && bloc < nrows && broff != noff;
+            const uint32_t ra = cl_map(pub_a + (uint32_t)((buf * 8 + (int)(r32 & 7u)) * W * 8), (int)((r32 >> 3) & 15u));
+            const uint32_t rd = cl_map(dia_a + (uint32_t)(buf * W * 8), qd);
             double x = 0.0, y = 0.0;
             if (lane < wb) {
-              asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(x) : "r"(ra + 8 * lane) : "memory");
-              if (need_d) asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(y) : "r"(rd + 8 * lane) : "memory");
+              asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(x) : "r"(ra) : "memory");
+              if (need_d) asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(y) : "r"(rd) : "memory");
             }
-            const double rp = EX == 0 ? 1.0 / bk : 0.0;  // |pivot| is the key: the division overlaps the pull
+            // |pivot| is the key: the division runs while the pull is in flight (the empty asm pins it
+            // between the loads and the stores of their results)
+            double rp = 1.0;
+            if constexpr (EX == 0) {
+              rp = 1.0 / __longlong_as_double((long long)((((unsigned long long)bh << 32) | bm) & 0x7fffffffffffffffull));
+              asm volatile("" : "+d"(rp) : : "memory");
+            }
             if (lane < wb) {
               u[buf * W + lane] = x;
               if (need_d) dg[buf * W + lane] = y;
             }
             const double pv = __shfl_sync(FULL, x, jn);
-            if (lane == 0) s_rpiv2[buf] = (pv != pv) ? pv : copysign(rp, pv);
-          }
-          if (lane == 0) {
-            s_wkey2[buf] = bk;
-            s_wrow2[buf] = broff;
-            blk_piv[jn] = p.r0 + broff;
-            if (q == 0) {
-              p.piv[cJ + jn] = p.r0 + broff;
-              if (!(bk > 0.0)) atomicMin(p.info, (unsigned long long)(cJ + jn + 1));
+            if (lane == 0) {
+              s_rpiv2[buf] = (pv != pv) ? pv : copysign(rp, pv);
+              s_wrow2[buf] = broff;
             }
+            PF_PROF_MARK(15);
+          } else if (lane == 0) {
+            s_wrow2[buf] = -1;
           }
           __syncwarp();
           asm volatile("bar.arrive 2, 256;\n" ::: "memory");
+          // off the critical path: the next exchange's expectation, the pivot record
           ++xs;
+          if (lane == 0) {
+            if (jn + 1 < kmax) cl_expect(smem_addr(xbar + (xs & 1)), (unsigned)(S * NWK) * 16u);
+            blk_piv[jn] = p.r0 + broff;
+            if (q == 0) {
+              p.piv[cJ + jn] = p.r0 + broff;
+              if (!ok) atomicMin(p.info, (unsigned long long)(cJ + jn + 1));
+            }
+          }
           if (++rem == R32) { rem = 0; ++qd; }
         }
       }
@@ -1084,8 +1146,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
     grid_sync();
     write_pend();
   }
+#ifdef PFLU_PANEL_PROF
   if (prof_on)
-    for (int i = 0; i < 16; ++i) p.prof[q * 16 + i] += prof_acc[i];
+    for (int i = 0; i < 16; ++i) p.prof[(tid == 0 ? 0 : 4096 + 256) + q * 16 + i] += prof_acc[i];
+#endif
   // advance the flag base for the next launch (all CTAs read it at their start)
   if constexpr (CL) {
     if (S > 1) cl_sync();  // no CTA may exit while peers can still push into or read its shared memory

@@ -52,6 +52,13 @@ for i, n in enumerate(NAMES):
 
 
 G = prof.cpu()[4096:4096 + w].double() / 1965.0
+WP = prof.cpu()[4096 + 256:4096 + 256 + 4096].view(256, 16)[:nz].double() / 1965.0
+if float(WP.sum()) > 0:
+    print("   v2 worker (warp 1 lane 0): 5 = pass 2 + rest, 3 = barrier wait + top, 10 = pass 1, 11 = warp arg-max, 2 = finish + publish")
+    for i in (5, 3, 10, 11, 2):
+        col = WP[:, i]
+        print(f"   worker[{i:2d}]   {col.min():8.0f} {col.mean():8.0f} {col.max():8.0f}")
+    print("   v2 exchange warp rows above: gather(w0) = post + loop, g:wait keys, g:reduce, g:pull")
 
 print(f"   gather us: mean {G.mean():.2f} median {G.median():.2f} max {G.max():.1f}")
 
