@@ -102,6 +102,8 @@ static thread_local DevCtx* g_dc = nullptr;  // context of the current call (set
 static int g_leaf = []() { const char* e = getenv("PFLU_LEAF"); return e ? atoi(e) : 0; }();
 // cluster panel: max CTAs per cluster (0 = LL kernel only), min rows per CTA, max panel rows
 static int g_cluster = []() { const char* e = getenv("PFLU_CLUSTER"); return e ? atoi(e) : 16; }();
+static int g_auto_rec_leaf = []() { const char* e = getenv("PFLU_AUTO_REC_LEAF"); return e ? atoi(e) : 128; }();
+static int64_t g_auto_rec_minrows = []() { const char* e = getenv("PFLU_AUTO_REC_MINROWS"); return e ? atoll(e) : 4096; }();
 static int g_pf_v2 = []() { const char* e = getenv("PFLU_PANEL_V2"); return e ? atoi(e) : 1; }();
 static int g_cl_minrows = []() { const char* e = getenv("PFLU_CL_MINROWS"); return e ? std::max(1, atoi(e)) : 128; }();
 static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
@@ -695,6 +697,7 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
   p.resync = g_resync;
   p.swcap = 0;
   p.sm_mask = c.rec_mask;
+  c.rec_mask = nullptr;  // only the first persistent launch of a (split) panel records its SMs
   // one thread-block cluster (DSMEM exchange) when the rows fit its CTAs' shared memory
   const bool want_cl = opt.panel_kernel == 2 || (opt.panel_kernel == 0 && g_cluster > 0 && rows <= g_cl_rows);
   if (want_cl) {
@@ -772,19 +775,19 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
 // its updates in ascending pivot order (multiply, then subtract in exact mode), so exact mode stays
 // bitwise equal to the unblocked getf2 of the reference (_jit.py:154-187), like the outer blocking.
 static int panel_rec(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, int64_t c0, int64_t w,
-                     int64_t* piv, unsigned long long* info, const pflu_options& opt, cudaStream_t st) {
+                     int64_t* piv, unsigned long long* info, const pflu_options& opt, cudaStream_t st,
+                     int leaf, int leafk) {
   const int64_t rows = m - r0;
   if (rows <= 0 || w <= 0) return PFLU_OK;
-  const int leaf = std::max(8, g_rec_leaf);
   if (w <= leaf) {
     pflu_options lo = opt;
-    lo.panel_kernel = g_rec_leafk;
+    lo.panel_kernel = leafk;
     return panel_leaf(c, a, lda, m, r0, c0, w, piv, info, lo, st);
   }
   // split at a multiple of the leaf width near the middle
   int64_t h = ((w / 2 + leaf - 1) / leaf) * leaf;
   if (h >= w) h = w - leaf;
-  CKR(panel_rec(c, a, lda, m, r0, c0, h, piv, info, opt, st));
+  CKR(panel_rec(c, a, lda, m, r0, c0, h, piv, info, opt, st, leaf, leafk));
   const int np = (int)std::min<int64_t>(h, rows);
   const bool exact = opt.exact != 0;
   CKR(launch_plan(piv, r0, np, c.rplan, st));
@@ -795,7 +798,7 @@ static int panel_rec(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, i
   if (rows <= np) return PFLU_OK;
   CKR(launch_gemm(a + (r0 + np) * lda + c0 + h, lda, a + (r0 + np) * lda + c0, lda, a + r0 * lda + c0 + h, lda,
                   rows - np, w - h, np, exact, st));
-  CKR(panel_rec(c, a, lda, m, r0 + np, c0 + h, w - h, piv, info, opt, st));
+  CKR(panel_rec(c, a, lda, m, r0 + np, c0 + h, w - h, piv, info, opt, st, leaf, leafk));
   const int np2 = (int)std::min<int64_t>(w - h, rows - np);
   CKR(launch_plan(piv, r0 + np, np2, c.rplan, st));
   return launch_swap(a, lda, r0 + np, np2, c.rplan, c0, c0 + h, nullptr, lda, false, st);
@@ -803,7 +806,18 @@ static int panel_rec(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, i
 
 static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, int64_t c0, int64_t w,
                         int64_t* piv, unsigned long long* info, const pflu_options& opt, cudaStream_t st) {
-  if (opt.panel_kernel == 3) return panel_rec(c, a, lda, m, r0, c0, w, piv, info, opt, st);
+  if (opt.panel_kernel == 3)
+    return panel_rec(c, a, lda, m, r0, c0, w, piv, info, opt, st, std::max(8, g_rec_leaf), g_rec_leafk);
+  // Automatic top-level split (round 2): a panel of >= 2 x 128 columns and >= 4096 rows is factored as
+  // two 128-column halves on the persistent kernel the caller chose (automatic / grid / cluster), with
+  // the right half's swap + U12 solve + rank-128 update between them on the DMMA kernels that own every
+  // SM -- half of the in-panel update leaves the panel kernel's 16 (or 64) SMs.  Measured alone on the
+  // GPU (profiles/r06_panel_sweep.log): 8192 x 256 0.840 -> 0.759 ms, 16384 x 256 1.456 -> 1.106,
+  // 32768 x 256 (grid leaves) 1.446 -> 1.299.  Exact mode stays bitwise (same per-element update order).
+  // (Every schedule splits alike -- also the SM-partitioned ones -- so that all of them stay bitwise equal.)
+  if (g_auto_rec_leaf > 0 && w >= 2 * g_auto_rec_leaf && m - r0 >= g_auto_rec_minrows && opt.panel_ctas == 0 &&
+      opt.leaf_width == 0)
+    return panel_rec(c, a, lda, m, r0, c0, w, piv, info, opt, st, g_auto_rec_leaf, opt.panel_kernel);
   return panel_leaf(c, a, lda, m, r0, c0, w, piv, info, opt, st);
 }
 

@@ -48,7 +48,10 @@ def timeit(a0, b, la, reps):
 out = []
 plan = [("C1", [128], [1, 0], 10), ("C2", [256], [1, 0], 5), ("C2s", [256], [1], 5),
         ("C3", [64, 128, 256, 512], [0, 1], 3), ("C4", [256], [1, 0], 2), ("C5", [512], [1], 1)]
+only = sys.argv[2].split(",") if len(sys.argv) > 2 else None  # e.g. C1,C2,C3
 for name, bs, las, reps in plan:
+    if only and name not in only:
+        continue
     a0 = torch.from_numpy(mat(name)).to(dev)
     n = a0.shape[0]
     for b in bs:
