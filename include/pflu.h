@@ -50,7 +50,9 @@ typedef struct pflu_options {
   int panel_kernel; /* 0 automatic, 1 cooperative grid (LL exchange through L2), 2 one thread-block
                        cluster (DSMEM exchange; PFLU_ERR_UNSUPPORTED if the panel does not fit),
                        3 recursive: halves split down to 32-column leaves (persistent kernel), the
-                       halves joined by swap+TRSM and a full-height DMMA GEMM */
+                       halves joined by swap+TRSM and a full-height DMMA GEMM,
+                       4 several 16-CTA clusters (DSMEM exchange inside a cluster, one LL round through L2
+                       between the clusters per column); panels under 8192 rows fall back to 1 */
   int malleable;    /* look-ahead 1 trailing update (the reference's LA / LA_MB, runtime.py:99-113):
                        0 dynamic: one CTA per GEMM tile, the block scheduler hands the panel's SMs
                          back to pending tiles as soon as the panel kernel exits (default);

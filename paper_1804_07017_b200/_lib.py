@@ -143,7 +143,7 @@ def check(rc: int, what: str) -> None:
     raise RuntimeError(f"{what} failed (code {rc}): {msg}")
 
 
-PANEL_AUTO, PANEL_GRID, PANEL_CLUSTER, PANEL_RECURSIVE = 0, 1, 2, 3
+PANEL_AUTO, PANEL_GRID, PANEL_CLUSTER, PANEL_RECURSIVE, PANEL_MCLUSTER = 0, 1, 2, 3, 4
 
 
 #: pflu_options.malleable: dynamic tile scheduling (default), SM-partitioned LA, LA_MB (join grid)

@@ -104,6 +104,8 @@ static int g_leaf = []() { const char* e = getenv("PFLU_LEAF"); return e ? atoi(
 static int g_cluster = []() { const char* e = getenv("PFLU_CLUSTER"); return e ? atoi(e) : 16; }();
 static int g_auto_rec_leaf = []() { const char* e = getenv("PFLU_AUTO_REC_LEAF"); return e ? atoi(e) : 128; }();
 static int64_t g_auto_rec_minrows = []() { const char* e = getenv("PFLU_AUTO_REC_MINROWS"); return e ? atoll(e) : 4096; }();
+static int64_t g_mc_minrows = []() { const char* e = getenv("PFLU_MC_MINROWS"); return e ? atoll(e) : 8192; }();
+static int64_t g_mc_rows = []() { const char* e = getenv("PFLU_MC_ROWS"); return e ? std::max<int64_t>(512, atoll(e)) : 8192; }();  // rows per cluster
 static int g_pf_v2 = []() { const char* e = getenv("PFLU_PANEL_V2"); return e ? atoi(e) : 1; }();
 static int g_cl_minrows = []() { const char* e = getenv("PFLU_CL_MINROWS"); return e ? std::max(1, atoi(e)) : 128; }();
 static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
@@ -193,7 +195,9 @@ static constexpr int PF_MAX_CTAS = PF_THREADS;
 #ifndef PFLU_PANEL_EXACT_RUNTIME
 // the exact flag compiled into the panel kernel (see panel_kernel's EX)
 template <int EX>
-static const void* pf_fn_ex(int W, bool cl, bool v2) {
+static const void* pf_fn_ex(int W, bool cl, bool v2, bool mc = false) {
+  if (cl && v2 && mc) return W == 8 ? (const void*)panel_kernel<8, true, EX, true, true> : W == 16 ? (const void*)panel_kernel<16, true, EX, true, true>
+                                                                                         : (const void*)panel_kernel<32, true, EX, true, true>;
   if (cl && v2) return W == 8 ? (const void*)panel_kernel<8, true, EX, true> : W == 16 ? (const void*)panel_kernel<16, true, EX, true>
                                                                                    : (const void*)panel_kernel<32, true, EX, true>;
   if (cl) return W == 8 ? (const void*)panel_kernel<8, true, EX> : W == 16 ? (const void*)panel_kernel<16, true, EX>
@@ -201,13 +205,14 @@ static const void* pf_fn_ex(int W, bool cl, bool v2) {
   return W == 8 ? (const void*)panel_kernel<8, false, EX> : W == 16 ? (const void*)panel_kernel<16, false, EX>
                                                                     : (const void*)panel_kernel<32, false, EX>;
 }
-static const void* pf_fn(int W, bool cl, bool exact = false, bool v2 = false) {
-  return exact ? pf_fn_ex<1>(W, cl, v2) : pf_fn_ex<0>(W, cl, v2);
+static const void* pf_fn(int W, bool cl, bool exact = false, bool v2 = false, bool mc = false) {
+  return exact ? pf_fn_ex<1>(W, cl, v2, mc) : pf_fn_ex<0>(W, cl, v2, mc);
 }
 #else
-static const void* pf_fn(int W, bool cl, bool exact = false, bool v2 = false) {
+static const void* pf_fn(int W, bool cl, bool exact = false, bool v2 = false, bool mc = false) {
   (void)exact;
   (void)v2;
+  (void)mc;
   if (cl) return W == 8 ? (const void*)panel_kernel<8, true> : W == 16 ? (const void*)panel_kernel<16, true>
                                                                        : (const void*)panel_kernel<32, true>;
   return W == 8 ? (const void*)panel_kernel<8, false> : W == 16 ? (const void*)panel_kernel<16, false>
@@ -269,6 +274,12 @@ static int ctx_get(DevCtx** out) {
             if (v2 && !cl) continue;
             CK(allow(pf_fn(W, cl, ex, v2)));
             if (cl) CK(cudaFuncSetAttribute(pf_fn(W, cl, ex, v2), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+#ifndef PFLU_PANEL_EXACT_RUNTIME
+            if (v2) {
+              CK(allow(pf_fn(W, cl, ex, v2, true)));
+              CK(cudaFuncSetAttribute(pf_fn(W, cl, ex, v2, true), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            }
+#endif
           }
     CK(allow((const void*)swap_trsm_kernel<8>));
     CK(allow((const void*)swap_trsm_dmma_kernel<256, 32>));
@@ -698,6 +709,42 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
   p.swcap = 0;
   p.sm_mask = c.rec_mask;
   c.rec_mask = nullptr;  // only the first persistent launch of a (split) panel records its SMs
+  // several 16-CTA clusters (panel_kernel 4): v2 exchange inside each cluster, one LL round between them
+  if (opt.panel_kernel == 4 && g_pf_v2 != 0 && rows >= g_mc_minrows && opt.panel_ctas == 0) {
+    for (int wi = 0; wi < 3; ++wi) {
+      const int W = Ws[wi];
+      if (W > Wpref) continue;
+      int NC = (int)std::min<int64_t>(PF_MC_MAXCL, std::max<int64_t>(2, (rows + g_mc_rows - 1) / g_mc_rows));
+      const int64_t R = (rows + (int64_t)NC * PF_CL_MAX - 1) / ((int64_t)NC * PF_CL_MAX);
+      const size_t smem = pf_smem_bytes(W, R, (int)w, true);
+      if (smem > smax) continue;
+      NC = (int)((rows + R * PF_CL_MAX - 1) / (R * PF_CL_MAX));  // clusters that own rows
+      if (NC < 2) break;
+      p.R = R;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = PF_CL_MAX;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeCooperative;  // every cluster resident: they wait for one another
+      at[1].val.cooperative = 1;
+      cfg.gridDim = dim3(NC * PF_CL_MAX);
+      cfg.blockDim = dim3(PF_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      void* args[] = {&p};
+      if (cudaLaunchKernelExC(&cfg, pf_fn(W, true, opt.exact != 0, true, true), args) != cudaSuccess) {
+        cudaGetLastError();  // cooperative + cluster launch refused: plain cluster launch (the clusters still
+        cfg.numAttrs = 1;    // all become resident once earlier work drains)
+        CK(cudaLaunchKernelExC(&cfg, pf_fn(W, true, opt.exact != 0, true, true), args));
+      }
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return PFLU_OK;
+    }
+  }
   // one thread-block cluster (DSMEM exchange) when the rows fit its CTAs' shared memory
   const bool want_cl = opt.panel_kernel == 2 || (opt.panel_kernel == 0 && g_cluster > 0 && rows <= g_cl_rows);
   if (want_cl) {

@@ -229,9 +229,16 @@ struct PanelSmem {
 // V2 (cluster kernel with peers only): the per-column exchange is run by a dedicated warp (warp 0) while
 // warps 1..7 own fixed rows; every WORKER WARP pushes its own candidate straight to every peer (no CTA-level
 // arg-max, no block barrier inside a column) -- see the V2 leaf below.
-template <int W, bool CL, int EX = -1, bool V2 = false>
+// MC (v2 only): the grid is several 16-CTA clusters.  Inside a cluster the exchange is the v2 one; the
+// exchange warps then trade their cluster's winner (key, row and the row's data) with the same-rank CTAs of
+// the other clusters through LL words in global memory -- one inter-cluster round per column, per-reader
+// mailboxes -- and the block-level syncs are the grid kernel's LL barrier over all CTAs.
+constexpr size_t PF_MC_MSG = 68;      // LL words per inter-cluster message: key, row word, 32 row elements
+constexpr int PF_MC_MAXCL = 8;        // clusters per panel (<= 128 CTAs)
+template <int W, bool CL, int EX = -1, bool V2 = false, bool MC = false>
 __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   static_assert(!V2 || CL, "the v2 leaf is a cluster exchange");
+  static_assert(!MC || V2, "multi-cluster panels use the v2 leaf");
   extern __shared__ __align__(16) double pf_smem[];
   constexpr int LD = W + 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -276,7 +283,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   __shared__ double s_rpiv2[2];  // v2: reciprocal of the pivot (DMMA mode), per exchange parity
   __shared__ int s_wrow2[2];     // v2: winner row as an offset from p.r0; -1 = no non-zero pivot
 
-  const unsigned epoch = CL ? 0u : *(volatile unsigned*)p.epoch;
+  const unsigned epoch = (CL && !MC) ? 0u : *(volatile unsigned*)p.epoch;
   if (p.sm_mask && tid == 0) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
@@ -307,7 +314,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   // grid-wide barrier with release/acquire for global memory: a cluster barrier (its release is a
   // MEMBAR.GPU, ~2-5 us) only when the cluster has peers; one CTA needs only __syncthreads
   auto grid_sync = [&]() {
-    if constexpr (CL) {
+    if constexpr (CL && !MC) {
       if (S > 1) cl_sync();
       else __syncthreads();
     } else {
@@ -683,6 +690,18 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       constexpr int NWK = PF_THREADS / 32 - 1, NT2 = NWK * 32;
       constexpr unsigned FULL = 0xffffffffu;
       const int base = (int)(rbeg - p.r0);  // row offsets from p.r0 fit 32 bits
+      // cluster-local identities (MC: q / S stay the grid-wide CTA index / count)
+      int CS = S, qc = q;
+      if constexpr (MC) {
+        unsigned a_, b_;
+        asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(a_));
+        asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(b_));
+        CS = (int)a_;
+        qc = (int)b_;
+      }
+      const int cid = MC ? q / CS : 0, NC = MC ? S / CS : 1;
+      unsigned long long* const mc_mb = p.ll + PF_MBOX_OFFSET;  // MC: [2][128 CTAs][PF_MC_MAXCL][PF_MC_MSG]
+      unsigned long long* const mc_dg = p.ll;                   // MC: [2][32] the next diagonal row, LL words
       // Messages, 16 bytes per worker warp: (integer key, ~((row offset from p.r0) << 7 | CTA << 3 | worker
       // slot)); the largest (key, word) tuple is the largest key and, among equal keys, the smallest row.
       if (warp > 0) {
@@ -690,9 +709,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         auto own_warp = [&](int rl) { return (int)(((unsigned)rl % (unsigned)NT2) >> 5); };
         auto first_row = [&](int p1) { return p1 <= wt ? wt : wt + (int)(((unsigned)(p1 - wt) + NT2 - 1) / NT2) * NT2; };
         // lane t pushes to peer t: its key slot and mbarrier in that peer, per parity
-        const int peer = lane < S ? lane : 0;
-        const uint32_t rk0 = cl_map(smem_addr(xkey + ((0 * PF_CL_MAX + q) * 8 + ws) * 2), peer);
-        const uint32_t rk1 = cl_map(smem_addr(xkey + ((1 * PF_CL_MAX + q) * 8 + ws) * 2), peer);
+        const int peer = lane < CS ? lane : 0;
+        const uint32_t rk0 = cl_map(smem_addr(xkey + ((0 * PF_CL_MAX + qc) * 8 + ws) * 2), peer);
+        const uint32_t rk1 = cl_map(smem_addr(xkey + ((1 * PF_CL_MAX + qc) * 8 + ws) * 2), peer);
         const uint32_t rb0 = cl_map(smem_addr(xbar), peer), rb1 = cl_map(smem_addr(xbar + 1), peer);
         // this warp's candidate row crl (key K; none if K == ORD_NONE) and, when the warp owns it, the next
         // diagonal row dl: finished for column j (fin), copied to the publish slots, then the key goes out
@@ -716,11 +735,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
               tr[lane] = v;
             }
             pubdiag[buf * W + lane] = v;
+            if constexpr (MC) ll_put2_d(mc_dg + (buf * 32 + lane) * 2, v, epoch + xs);  // for a winner in another cluster
           }
           __syncwarp();
-          if (lane < S)
+          if (lane < CS)
             cl_put16(buf ? rk1 : rk0, K,
-                     (unsigned long long)(have ? ~((unsigned)(base + crl) << 7 | (unsigned)(q << 3 | ws)) : 0u),
+                     (unsigned long long)(have ? ~((unsigned)(base + crl) << 7 | (unsigned)(qc << 3 | ws)) : 0u),
                      buf ? rb1 : rb0);
           ++xs;
         };
@@ -827,10 +847,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
         const int R32 = (int)p.R;
         int qd = jb / R32, rem = jb - qd * R32;  // owner CTA of the diagonal row of column jn, kept incrementally
         const int s0 = (lane & 1) * 4;
-        const bool lane_on = (lane >> 1) < S;
+        const bool lane_on = (lane >> 1) < CS;
         const uint32_t key_a = smem_addr(xkey + ((lane >> 1) * 8 + s0) * 2);  // + buf * PF_CL_MAX * 128 bytes
         const uint32_t pub_a = smem_addr(pubrow) + 8 * lane, dia_a = smem_addr(pubdiag) + 8 * lane;
-        if (kmax > 0 && lane == 0) cl_expect(smem_addr(xbar + (xs & 1)), (unsigned)(S * NWK) * 16u);
+        if (kmax > 0 && lane == 0) cl_expect(smem_addr(xbar + (xs & 1)), (unsigned)(CS * NWK) * 16u);
         for (int jn = 0; jn < kmax; ++jn) {
           const int buf = xs & 1;
           PF_PROF_MARK(4);
@@ -851,6 +871,43 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           unsigned bh = (unsigned)(K0 >> 32), bm = (unsigned)K0, bl = l0;
           warp_max96(bh, bm, bl);
           PF_PROF_MARK(14);
+          double x = 0.0;  // this lane's element of the winner row
+          if constexpr (MC) {
+            // inter-cluster round: pull this cluster's winner row, send (key, row word, row) to the same-rank
+            // CTA of every other cluster, take theirs, keep the best tuple and its row
+            const unsigned fl = epoch + xs;
+            if ((bh | bm) != 0u && lane < wb) {
+              const unsigned c32 = ~bl;
+              const uint32_t ra = cl_map(pub_a + (uint32_t)((buf * 8 + (int)(c32 & 7u)) * W * 8), (int)((c32 >> 3) & 15u));
+              asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(x) : "r"(ra) : "memory");
+            }
+            unsigned long long* mb = mc_mb + (size_t)buf * (128 * PF_MC_MAXCL * PF_MC_MSG);
+            for (int c2 = 0; c2 < NC; ++c2) {
+              if (c2 == cid) continue;
+              unsigned long long* e = mb + ((size_t)(c2 * CS + qc) * PF_MC_MAXCL + cid) * PF_MC_MSG;
+              if (lane < wb) ll_put2_d(e + 4 + 2 * lane, x, fl);
+              if (lane == 0) {
+                ll_put2(e, bm, bh, fl);
+                ll_put2(e + 2, bl, 0u, fl);
+              }
+            }
+            for (int c2 = 0; c2 < NC; ++c2) {
+              if (c2 == cid) continue;
+              const unsigned long long* e = mb + ((size_t)q * PF_MC_MAXCL + c2) * PF_MC_MSG;
+              unsigned k0 = 0, k1 = 0, l_ = 0, z_ = 0, a_ = 0, b_ = 0;
+              bool o0 = false, o1 = false, o2 = lane >= wb;
+              while (!(o0 && o1 && o2)) {
+                if (!o0) o0 = ll_try2(e, fl, k0, k1);
+                if (!o1) o1 = ll_try2(e + 2, fl, l_, z_);
+                if (!o2) o2 = ll_try2(e + 4 + 2 * lane, fl, a_, b_);
+              }
+              const bool better = (k1 > bh) | ((k1 == bh) & ((k0 > bm) | ((k0 == bm) & (l_ > bl))));
+              if (better) {
+                bh = k1; bm = k0; bl = l_;
+                x = __longlong_as_double(((long long)b_ << 32) | a_);
+              }
+            }
+          }
           const unsigned r32 = ~bl;
           const int noff = jb + jn;  // offset of this column's diagonal row from p.r0
           const bool ok = bh > 0x80000000u || (bh == 0x80000000u && bm != 0u);  // key > ORD_ZERO: a non-zero pivot
@@ -859,11 +916,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
             const int bloc = broff - base;
             const bool need_d = bloc >= 0 && bloc < nrows && broff != noff;
             const uint32_t ra = cl_map(pub_a + (uint32_t)((buf * 8 + (int)(r32 & 7u)) * W * 8), (int)((r32 >> 3) & 15u));
-            const uint32_t rd = cl_map(dia_a + (uint32_t)(buf * W * 8), qd);
-            double x = 0.0, y = 0.0;
+            const bool d_local = !MC || qd / CS == cid;  // the diagonal row's owner sits in this cluster
+            const uint32_t rd = cl_map(dia_a + (uint32_t)(buf * W * 8), MC ? (d_local ? qd - cid * CS : 0) : qd);
+            double y = 0.0;
             if (lane < wb) {
-              asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(x) : "r"(ra) : "memory");
-              if (need_d) asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(y) : "r"(rd) : "memory");
+              if constexpr (!MC) asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(x) : "r"(ra) : "memory");
+              if (need_d && d_local) asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(y) : "r"(rd) : "memory");
+              if (need_d && !d_local) y = ll_get2_d(mc_dg + (buf * 32 + lane) * 2, epoch + xs);
             }
             // |pivot| is the key: the division runs while the pull is in flight (the empty asm pins it
             // between the loads and the stores of their results)
@@ -890,7 +949,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
           // off the critical path: the next exchange's expectation, the pivot record
           ++xs;
           if (lane == 0) {
-            if (jn + 1 < kmax) cl_expect(smem_addr(xbar + (xs & 1)), (unsigned)(S * NWK) * 16u);
+            if (jn + 1 < kmax) cl_expect(smem_addr(xbar + (xs & 1)), (unsigned)(CS * NWK) * 16u);
             blk_piv[jn] = p.r0 + broff;
             if (q == 0) {
               p.piv[cJ + jn] = p.r0 + broff;
@@ -1153,7 +1212,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
   // advance the flag base for the next launch (all CTAs read it at their start)
   if constexpr (CL) {
     if (S > 1) cl_sync();  // no CTA may exit while peers can still push into or read its shared memory
-  } else {
+  }
+  if constexpr (!CL || MC) {
     if (q == 0 && tid == 0) atomicAdd(p.epoch, (unsigned)(2 * w + 4 * ((w + W - 1) / W) + 32));
   }
 }

@@ -229,6 +229,31 @@ def test_panel_bitwise(cuda, m, w, ctas, leaf, kernel):
     assert bitwise_equal(x.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("m,w,zero_cols", [(8192, 64, ()), (20000, 256, ()), (16500, 96, (0, 5, 6, 40)), (9000, 32, (31,)),
+                                            (33000, 128, ())])
+def test_panel_multicluster_bitwise(cuda, m, w, zero_cols):
+    """Multi-cluster panel (panel_kernel 4: v2 exchange inside each 16-CTA cluster, one LL round between the
+    clusters per column) == lu_unb_run on the panel, zero pivots included (_jit.py:154-187)."""
+    import torch
+    from paper_1804_07017_b200 import _lib as lb
+
+    rng = np.random.default_rng(7 * m + w)
+    p0 = rng.uniform(-1, 1, (m, w))
+    for c in zero_cols:
+        p0[:, c] = 0.0
+    want, wpiv, winfo = oracle.lu_unb(p0.copy())
+    for rep in range(3):
+        x = _t(p0, cuda)
+        piv = torch.zeros(w, dtype=torch.int64, device=cuda)
+        info = ctypes.c_int64(0)
+        opt = lb.options(exact=True, panel_kernel=lb.PANEL_MCLUSTER)
+        lb.check(lb.load().pflu_panel(x.data_ptr(), w, m, 0, 0, w, piv.data_ptr(), ctypes.byref(info), _stream(),
+                                      ctypes.byref(opt)), "panel")
+        assert np.array_equal(piv.cpu().numpy()[: len(wpiv)], wpiv)
+        assert info.value == winfo
+        assert bitwise_equal(x.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("m,w", [(300, 64), (5000, 256), (20000, 256), (2048, 512), (100, 200)])
 def test_panel_recursive_dmma(cuda, m, w):
     """Recursive panel in DMMA mode: the oracle's pivots, factors within rounding of getf2's."""
