@@ -106,6 +106,11 @@ static int g_auto_rec_leaf = []() { const char* e = getenv("PFLU_AUTO_REC_LEAF")
 static int64_t g_auto_rec_minrows = []() { const char* e = getenv("PFLU_AUTO_REC_MINROWS"); return e ? atoll(e) : 4096; }();
 static int64_t g_mc_minrows = []() { const char* e = getenv("PFLU_MC_MINROWS"); return e ? atoll(e) : 8192; }();
 static int64_t g_mc_rows = []() { const char* e = getenv("PFLU_MC_ROWS"); return e ? std::max<int64_t>(512, atoll(e)) : 8192; }();  // rows per cluster
+// the kernel of tall panels that sit alone on the critical path (depth 0, multi-rank owners): 4 = multi-cluster
+// (falls back to the grid kernel where it does not fit), 1 = the cooperative grid kernel
+static int g_first_block = []() { const char* e = getenv("PFLU_FIRST_BLOCK"); return e ? atoi(e) : 0; }();
+static int g_tall_kernel = []() { const char* e = getenv("PFLU_TALL_KERNEL"); return e ? atoi(e) : 4; }();
+static int g_mc_maxcl = []() { const char* e = getenv("PFLU_MC_MAXCL"); return e ? std::min(PF_MC_MAXCL, std::max(2, atoi(e))) : 4; }();
 static int g_pf_v2 = []() { const char* e = getenv("PFLU_PANEL_V2"); return e ? atoi(e) : 1; }();
 static int g_cl_minrows = []() { const char* e = getenv("PFLU_CL_MINROWS"); return e ? std::max(1, atoi(e)) : 128; }();
 static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
@@ -714,7 +719,7 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
     for (int wi = 0; wi < 3; ++wi) {
       const int W = Ws[wi];
       if (W > Wpref) continue;
-      int NC = (int)std::min<int64_t>(PF_MC_MAXCL, std::max<int64_t>(2, (rows + g_mc_rows - 1) / g_mc_rows));
+      int NC = (int)std::min<int64_t>(g_mc_maxcl, std::max<int64_t>(2, (rows + g_mc_rows - 1) / g_mc_rows));
       const int64_t R = (rows + (int64_t)NC * PF_CL_MAX - 1) / ((int64_t)NC * PF_CL_MAX);
       const size_t smem = pf_smem_bytes(W, R, (int)w, true);
       if (smem > smax) continue;
@@ -736,10 +741,17 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
       cfg.attrs = at;
       cfg.numAttrs = 2;
       void* args[] = {&p};
+      // The clusters wait for one another: launch only what the device can hold at once (16-CTA clusters
+      // need 16 free SMs inside one GPC) and only cooperatively; otherwise the grid kernel below runs.
+      int max_cl = 0;
+      if (cudaOccupancyMaxActiveClusters(&max_cl, pf_fn(W, true, opt.exact != 0, true, true), &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        max_cl = 0;
+      }
+      if (max_cl < NC) break;
       if (cudaLaunchKernelExC(&cfg, pf_fn(W, true, opt.exact != 0, true, true), args) != cudaSuccess) {
-        cudaGetLastError();  // cooperative + cluster launch refused: plain cluster launch (the clusters still
-        cfg.numAttrs = 1;    // all become resident once earlier work drains)
-        CK(cudaLaunchKernelExC(&cfg, pf_fn(W, true, opt.exact != 0, true, true), args));
+        cudaGetLastError();
+        break;
       }
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return PFLU_OK;
@@ -988,9 +1000,9 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     int t_pf = -1;
     CKR(tr.begin(PFLU_TRACE_PF, k, st, &t_pf));
     pflu_options popt = opt;
-    if (lookahead == 0 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;
+    if (lookahead == 0 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = g_tall_kernel;
     // = dist.py: the owner's tall panels on the grid kernel from 8 ranks up (chain-bound there)
-    if (g_emu_ranks >= g_emu_grid_ranks && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = 1;
+    if (g_emu_ranks >= g_emu_grid_ranks && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = g_tall_kernel;
     if (g_pf_force >= 0 && opt.panel_kernel == 0) popt.panel_kernel = g_pf_force;
     if (sched && k == 0) c.rec_mask = c.sm_mask;  // PF(0) runs alone: its SMs become the panel's partition
     const int prc = panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, popt, st);
@@ -1139,12 +1151,21 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     while (ch + 1 < nch && chunk_blk[ch + 1] <= blk) ++ch;
     return ch;
   };
-  const size_t nev = 2 + (size_t)count * (nch + 2);
+  // per step: PF, TU_L, first trailing block, then the chunks
+  const size_t nev = 2 + (size_t)count * (nch + 3);
   CKR(ctx_events(c, nev + nch + 1));
   cudaEvent_t ev_start = c.ev[0];
-  auto ev_pf = [&](int k) { return c.ev[2 + (size_t)k * (nch + 2)]; };
-  auto ev_tul = [&](int k) { return c.ev[3 + (size_t)k * (nch + 2)]; };
-  auto ev_ck = [&](int ch, int k) { return c.ev[4 + (size_t)k * (nch + 2) + ch]; };
+  auto ev_pf = [&](int k) { return c.ev[2 + (size_t)k * (nch + 3)]; };
+  auto ev_tul = [&](int k) { return c.ev[3 + (size_t)k * (nch + 3)]; };
+  auto ev_first = [&](int k) { return c.ev[4 + (size_t)k * (nch + 3)]; };
+  auto ev_ck = [&](int ch, int k) { return c.ev[5 + (size_t)k * (nch + 3) + ch]; };
+  // PFLU_FIRST_BLOCK=1 (off: measured no gain): TU_R(k) updates block k+2 (the block TU_L(k+1) and PF(k+2)
+  // need) as its own launch at the head of its chunk stream and TU_L(k+1) waits for that piece only.  The
+  // stall it targets (8-rank model, early steps: 25 ms of PF -> TU_L gaps) is not a scheduling artefact: that
+  // block's previous update sits inside the bulk of TU_R(k-1), and the chunk stream is in order, so while a
+  // step's trailing update outlasts its panel the run is update-bound whatever the order (model 189.5 vs
+  // 184.5 ms, C3 108.2 vs 102.8 ms with the extra launches).
+  const bool first_blk = g_first_block != 0 && !sched;
   CK(cudaEventRecord(ev_start, user));
   CK(cudaStreamWaitEvent(c.sP, ev_start, 0));
   CK(cudaStreamWaitEvent(c.sL, ev_start, 0));
@@ -1178,7 +1199,14 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
       const int64_t c_hi = std::min<int64_t>(hi_r, (int64_t)chunk_blk[ch + 1] * b);
       if (c_hi > c_lo) {
         CK(cudaStreamWaitEvent(st, ev_pf(k), 0));
-        CKR(update_cols(k, c_lo, c_hi, st, PFLU_TRACE_TU_R));
+        int64_t lo2 = c_lo;
+        if (first_blk && c_lo == lo_r && k + 2 < count && c_hi > c_lo + grid[k + 2].bw) {
+          lo2 = c_lo + grid[k + 2].bw;
+          CKR(update_cols(k, c_lo, lo2, st, PFLU_TRACE_TU_R));
+          CK(cudaEventRecord(ev_first(k), st));
+        }
+        CKR(update_cols(k, lo2, c_hi, st, PFLU_TRACE_TU_R));
+        if (lo2 == c_lo && c_lo == lo_r) CK(cudaEventRecord(ev_first(k), st));
       }
       CK(cudaEventRecord(ev_ck(ch, k), st));
     }
@@ -1192,7 +1220,7 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
       CKR(left_swaps(k, c.sL));
     }
     if (k + 1 < count) {
-      if (k > 0) CK(cudaStreamWaitEvent(c.sP, ev_ck(chunk_of_block(k + 1), k - 1), 0));
+      if (k > 0) CK(cudaStreamWaitEvent(c.sP, first_blk ? ev_first(k - 1) : ev_ck(chunk_of_block(k + 1), k - 1), 0));
       CKR(update_cols(k, grid[k + 1].col0, grid[k + 1].col0 + grid[k + 1].bw, c.sP, PFLU_TRACE_TU_L));
       CK(cudaEventRecord(ev_tul(k), c.sP));
       CKR(pf(k + 1, c.sP));

@@ -108,7 +108,8 @@ class CudaKernels:
         self.grid_rows = grid_rows
         self.device = device
         self.opt = _lib.options(exact=exact)
-        self.opt_grid = _lib.options(exact=exact, panel_kernel=_lib.PANEL_GRID)
+        # tall owner panels on the chain-bound rank counts: the multi-cluster kernel (grid kernel where it does not fit)
+        self.opt_grid = _lib.options(exact=exact, panel_kernel=int(os.environ.get("PFLU_TALL_KERNEL", _lib.PANEL_MCLUSTER)))
         self.exact = exact
         self.fast_solve = not exact  # U12 solve on DMMA with inverted diagonal blocks
         lo, hi = torch.cuda.Stream.priority_range()
