@@ -108,10 +108,15 @@ static int64_t g_mc_minrows = []() { const char* e = getenv("PFLU_MC_MINROWS"); 
 static int64_t g_mc_rows = []() { const char* e = getenv("PFLU_MC_ROWS"); return e ? std::max<int64_t>(512, atoll(e)) : 8192; }();  // rows per cluster
 // the kernel of tall panels that sit alone on the critical path (depth 0, multi-rank owners): 4 = multi-cluster
 // (falls back to the grid kernel where it does not fit), 1 = the cooperative grid kernel
+static int64_t g_la_tall_rows = []() { const char* e = getenv("PFLU_LA_TALL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
 static int g_first_block = []() { const char* e = getenv("PFLU_FIRST_BLOCK"); return e ? atoi(e) : 0; }();
 static int g_tall_kernel = []() { const char* e = getenv("PFLU_TALL_KERNEL"); return e ? atoi(e) : 4; }();
 static int g_mc_maxcl = []() { const char* e = getenv("PFLU_MC_MAXCL"); return e ? std::min(PF_MC_MAXCL, std::max(2, atoi(e))) : 4; }();
+#ifdef PFLU_PANEL_EXACT_RUNTIME
+static int g_pf_v2 = 0;  // the round-1 runtime-flag build has only the v1 kernels
+#else
 static int g_pf_v2 = []() { const char* e = getenv("PFLU_PANEL_V2"); return e ? atoi(e) : 1; }();
+#endif
 static int g_cl_minrows = []() { const char* e = getenv("PFLU_CL_MINROWS"); return e ? std::max(1, atoi(e)) : 128; }();
 static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
 static int g_trsm_dmma = []() { const char* e = getenv("PFLU_TRSM_DMMA"); return e ? atoi(e) : 1; }();
@@ -1003,6 +1008,8 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     if (lookahead == 0 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = g_tall_kernel;
     // = dist.py: the owner's tall panels on the grid kernel from 8 ranks up (chain-bound there)
     if (g_emu_ranks >= g_emu_grid_ranks && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = g_tall_kernel;
+    // depth 1, single rank: panels taller than PFLU_LA_TALL_ROWS leave the 16-SM cluster for the tall-panel kernel
+    if (lookahead != 0 && popt.panel_kernel == 0 && m - s.col0 > g_la_tall_rows) popt.panel_kernel = g_tall_kernel;
     if (g_pf_force >= 0 && opt.panel_kernel == 0) popt.panel_kernel = g_pf_force;
     if (sched && k == 0) c.rec_mask = c.sm_mask;  // PF(0) runs alone: its SMs become the panel's partition
     const int prc = panel_factor(c, a, lda, m, s.col0, s.col0, s.bw, piv, info, popt, st);

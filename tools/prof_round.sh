@@ -1,7 +1,7 @@
 # Round evidence pack (run under gpurun): bench line, ncu launch list of one factorization, GEMM /
 # panel / TRSM / laswp full captures.  The .ncu-rep files stay on the box (/tmp/prof); their raw
 # pages come back as CSV (gpurun_out/ is capped at 64 MiB).  Usage: bash tools/prof_round.sh r05
-R=${1:-r05}
+R=${1:-r06}
 P=/tmp/prof; mkdir -p $P gpurun_out
 set -x
 python bench.py --e2e-steps 1 > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err
@@ -18,6 +18,7 @@ cap() {  # name kernel-regex command...
   ncu -i $P/${name}_$R.ncu-rep --page source --csv 2>/dev/null | head -c 8000000 > gpurun_out/${name}_${R}_source.csv
 }
 cap gemm gemm_dmma python tools/gemm_once.py 32512 32512 256 1
-cap panel panel_kernel python tools/panel_once.py 32768 256
+cap panel panel_kernel python tools/panel_once.py 2048 256 0 0 2     # v2 cluster leaf (no top-level split below 4096 rows)
+cap panelmc panel_kernel python tools/panel_once.py 32768 128 0 0 4  # multi-cluster kernel, one 128-column half
 cap trsm swap_trsm_dmma python tools/swap_dmma_once.py
 cap lswap swap_trsm_kernel python tools/swap_dmma_once.py
