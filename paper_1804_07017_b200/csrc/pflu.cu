@@ -117,7 +117,7 @@ static int g_pf_v2 = 0;  // the round-1 runtime-flag build has only the v1 kerne
 #else
 static int g_pf_v2 = []() { const char* e = getenv("PFLU_PANEL_V2"); return e ? atoi(e) : 1; }();
 #endif
-static int g_cl_minrows = []() { const char* e = getenv("PFLU_CL_MINROWS"); return e ? std::max(1, atoi(e)) : 128; }();
+static int g_cl_minrows = []() { const char* e = getenv("PFLU_CL_MINROWS"); return e ? std::max(1, atoi(e)) : 32; }();
 static int64_t g_cl_rows = []() { const char* e = getenv("PFLU_CL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
 static int g_trsm_dmma = []() { const char* e = getenv("PFLU_TRSM_DMMA"); return e ? atoi(e) : 1; }();
 static int64_t g_grid_rows = []() { const char* e = getenv("PFLU_GRID_ROWS"); return e ? atoll(e) : 8192; }();
