@@ -81,6 +81,10 @@ typedef struct pflu_trace_event {
 int pflu_version(void);
 /* Cumulative number of kernels this library has launched in the process (bench evidence). */
 long long pflu_launch_count(void);
+/* Which record kinds a trace collects: bit (1 << PFLU_TRACE_x) per kind, default all.  Every record costs
+   two event records on its stream (~2 us of GPU time each): a timed run that only needs the GEMM and PF
+   records (bench.py's roofline) masks the rest.  Returns the previous mask. */
+unsigned pflu_set_trace_mask(unsigned mask);
 const char* pflu_last_error(void);
 void pflu_default_options(pflu_options* opt);
 int pflu_device_count(void);

@@ -21,7 +21,7 @@ TRACE_LABELS = {0: "PF", 1: "TU", 2: "TU_L", 3: "TU_R", 4: "GEMM", 5: "BCAST"}
 
 #: every symbol include/pflu.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
-    "pflu_version", "pflu_launch_count", "pflu_last_error", "pflu_default_options", "pflu_device_count",
+    "pflu_version", "pflu_launch_count", "pflu_set_trace_mask", "pflu_last_error", "pflu_default_options", "pflu_device_count",
     "pflu_getrf", "pflu_getrf_device", "pflu_panel", "pflu_laswp", "pflu_swap_trsm",
     "pflu_trsm", "pflu_gemm_update", "pflu_info_reset", "pflu_info_read", "pflu_pivot_plan",
     "pflu_swap_trsm_plan", "pflu_copy2d", "pflu_release_workspace", "pflu_diag_inv", "pflu_swap_trsm_inv",
@@ -64,6 +64,8 @@ def load():
         L.pflu_version.argtypes = []
         L.pflu_launch_count.restype = ctypes.c_longlong
         L.pflu_launch_count.argtypes = []
+        L.pflu_set_trace_mask.restype = ctypes.c_uint
+        L.pflu_set_trace_mask.argtypes = [ctypes.c_uint]
         L.pflu_last_error.restype = ctypes.c_char_p
         L.pflu_last_error.argtypes = []
         L.pflu_default_options.restype = None

@@ -141,6 +141,7 @@ static int g_emu_grid_ranks = []() { const char* e = getenv("PFLU_EMU_GRID_RANKS
 static int g_tur_split = []() { const char* e = getenv("PFLU_TUR_SPLIT"); return e ? atoi(e) : 0; }();
 
 // Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.
+static std::atomic<unsigned> g_trace_mask{~0u};  // record kinds a trace collects (pflu_set_trace_mask)
 struct Tracer {
   DevCtx* c = nullptr;
   bool on = false;
@@ -165,7 +166,7 @@ struct Tracer {
   }
   int begin(int label, int k, cudaStream_t st, int* idx, double flop = 0.0) {
     *idx = -1;
-    if (!on) return PFLU_OK;
+    if (!on || !((g_trace_mask.load(std::memory_order_relaxed) >> label) & 1u)) return PFLU_OK;
     Rec r{label, k, nullptr, nullptr, flop};
     CKR(ev(&r.e0));
     CKR(ev(&r.e1));
@@ -1287,6 +1288,10 @@ extern "C" {
 int pflu_version(void) { return 1; }
 
 long long pflu_launch_count(void) { return g_launches.load(); }
+unsigned pflu_set_trace_mask(unsigned mask) {
+  const unsigned old = g_trace_mask.exchange(mask);
+  return old;
+}
 
 // Developer hook (not in pflu.h): per-phase clock64 totals of the panel kernel's CTA 0.
 int pflu_debug_panel_profile(void* dev_buf) {
