@@ -109,8 +109,19 @@ static int64_t g_mc_rows = []() { const char* e = getenv("PFLU_MC_ROWS"); return
 // the kernel of tall panels that sit alone on the critical path (depth 0, multi-rank owners): 4 = multi-cluster
 // (falls back to the grid kernel where it does not fit), 1 = the cooperative grid kernel
 static int64_t g_la_tall_rows = []() { const char* e = getenv("PFLU_LA_TALL_ROWS"); return e ? atoll(e) : (int64_t)1 << 40; }();
+static int g_mc_adapt = []() { const char* e = getenv("PFLU_MC_ADAPT"); return e ? atoi(e) : 1; }();
 static int g_first_block = []() { const char* e = getenv("PFLU_FIRST_BLOCK"); return e ? atoi(e) : 0; }();
 static int g_tall_kernel = []() { const char* e = getenv("PFLU_TALL_KERNEL"); return e ? atoi(e) : 4; }();
+// Clusters for a multi-rank owner's tall panel (multi-cluster kernel).  While the rank's own share of the
+// trailing update of this step outlasts the panel + TU_L, the step is bound by SM time, not by the chain:
+// two clusters (32 SMs, ~20% slower panel, 40% less SM time) leave more of the GPU to the update; once the
+// chain is the longer one, every cluster the device holds (8-rank model, C4: 175.2 -> 168 ms).  Times in ms:
+// the update at the in-step DMMA rate, the panel from the measured 0.63 + 1.65e-5 * rows (4 clusters).
+static int tall_panel_ctas(int64_t rows, int64_t local_cols, int64_t bw) {
+  const double t_upd = 2.0 * (double)rows * (double)local_cols * (double)bw / 33.0e12 * 1e3;
+  const double t_chain = 0.83 + 1.65e-5 * (double)rows;
+  return t_upd > t_chain ? 2 * PF_CL_MAX : 0;
+}
 static int g_mc_maxcl = []() { const char* e = getenv("PFLU_MC_MAXCL"); return e ? std::min(PF_MC_MAXCL, std::max(2, atoi(e))) : 4; }();
 #ifdef PFLU_PANEL_EXACT_RUNTIME
 static int g_pf_v2 = 0;  // the round-1 runtime-flag build has only the v1 kernels
@@ -721,11 +732,13 @@ static int panel_leaf(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0, 
   p.sm_mask = c.rec_mask;
   c.rec_mask = nullptr;  // only the first persistent launch of a (split) panel records its SMs
   // several 16-CTA clusters (panel_kernel 4): v2 exchange inside each cluster, one LL round between them
-  if (opt.panel_kernel == 4 && g_pf_v2 != 0 && rows >= g_mc_minrows && opt.panel_ctas == 0) {
+  if (opt.panel_kernel == 4 && g_pf_v2 != 0 && rows >= g_mc_minrows) {
+    // panel_ctas > 0 caps the CTAs, i.e. the clusters (at least two)
+    const int cl_cap = opt.panel_ctas > 0 ? std::max(2, std::min(g_mc_maxcl, opt.panel_ctas / PF_CL_MAX)) : g_mc_maxcl;
     for (int wi = 0; wi < 3; ++wi) {
       const int W = Ws[wi];
       if (W > Wpref) continue;
-      int NC = (int)std::min<int64_t>(g_mc_maxcl, std::max<int64_t>(2, (rows + g_mc_rows - 1) / g_mc_rows));
+      int NC = (int)std::min<int64_t>(cl_cap, std::max<int64_t>(2, (rows + g_mc_rows - 1) / g_mc_rows));
       const int64_t R = (rows + (int64_t)NC * PF_CL_MAX - 1) / ((int64_t)NC * PF_CL_MAX);
       const size_t smem = pf_smem_bytes(W, R, (int)w, true);
       if (smem > smax) continue;
@@ -880,8 +893,8 @@ static int panel_factor(DevCtx& c, double* a, int64_t lda, int64_t m, int64_t r0
   // GPU (profiles/r06_panel_sweep.log): 8192 x 256 0.840 -> 0.759 ms, 16384 x 256 1.456 -> 1.106,
   // 32768 x 256 (grid leaves) 1.446 -> 1.299.  Exact mode stays bitwise (same per-element update order).
   // (Every schedule splits alike -- also the SM-partitioned ones -- so that all of them stay bitwise equal.)
-  if (g_auto_rec_leaf > 0 && w >= 2 * g_auto_rec_leaf && m - r0 >= g_auto_rec_minrows && opt.panel_ctas == 0 &&
-      opt.leaf_width == 0)
+  if (g_auto_rec_leaf > 0 && w >= 2 * g_auto_rec_leaf && m - r0 >= g_auto_rec_minrows &&
+      (opt.panel_ctas == 0 || opt.panel_kernel == 4) && opt.leaf_width == 0)
     return panel_rec(c, a, lda, m, r0, c0, w, piv, info, opt, st, g_auto_rec_leaf, opt.panel_kernel);
   return panel_leaf(c, a, lda, m, r0, c0, w, piv, info, opt, st);
 }
@@ -1008,7 +1021,11 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
     pflu_options popt = opt;
     if (lookahead == 0 && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = g_tall_kernel;
     // = dist.py: the owner's tall panels on the grid kernel from 8 ranks up (chain-bound there)
-    if (g_emu_ranks >= g_emu_grid_ranks && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) popt.panel_kernel = g_tall_kernel;
+    if (g_emu_ranks >= g_emu_grid_ranks && popt.panel_kernel == 0 && m - s.col0 > g_grid_rows) {
+      popt.panel_kernel = g_tall_kernel;
+      if (g_tall_kernel == 4 && popt.panel_ctas == 0 && g_mc_adapt)
+        popt.panel_ctas = tall_panel_ctas(m - s.col0, (n - s.col0 - s.bw) / g_emu_ranks, s.bw);
+    }
     // depth 1, single rank: panels taller than PFLU_LA_TALL_ROWS leave the 16-SM cluster for the tall-panel kernel
     if (lookahead != 0 && popt.panel_kernel == 0 && m - s.col0 > g_la_tall_rows) popt.panel_kernel = g_tall_kernel;
     if (g_pf_force >= 0 && opt.panel_kernel == 0) popt.panel_kernel = g_pf_force;

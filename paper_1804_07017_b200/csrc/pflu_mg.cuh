@@ -326,7 +326,11 @@ static int mg_rank_run(MgRank& R, MgJob& J) {
       const int64_t lc = (int64_t)(k / P) * b;
       int t = tbegin(PFLU_TRACE_PF, k, sP);
       pflu_options popt = J.opt;
-      if (popt.panel_kernel == 0 && P >= g_emu_grid_ranks && rows > g_grid_rows) popt.panel_kernel = g_tall_kernel;
+      if (popt.panel_kernel == 0 && P >= g_emu_grid_ranks && rows > g_grid_rows) {
+        popt.panel_kernel = g_tall_kernel;
+        if (g_tall_kernel == 4 && popt.panel_ctas == 0 && g_mc_adapt)
+          popt.panel_ctas = tall_panel_ctas(rows, (n - col0 - bw) / P, bw);
+      }
       CKR(panel_factor(*c, R.a, ld, n, col0, lc, bw, R.piv, R.info, popt, sP));
       tend(t, sP);
       if (via_msg) {

@@ -110,6 +110,10 @@ class CudaKernels:
         self.opt = _lib.options(exact=exact)
         # tall owner panels on the chain-bound rank counts: the multi-cluster kernel (grid kernel where it does not fit)
         self.opt_grid = _lib.options(exact=exact, panel_kernel=int(os.environ.get("PFLU_TALL_KERNEL", _lib.PANEL_MCLUSTER)))
+        # the same kernel capped at two clusters (32 SMs): for the steps whose trailing update outlasts the panel
+        self.opt_grid2 = _lib.options(exact=exact, panel_ctas=32,
+                                      panel_kernel=int(os.environ.get("PFLU_TALL_KERNEL", _lib.PANEL_MCLUSTER)))
+        self.ranks = 1  # set by the driver: ranks sharing the trailing update (panel() sizes the tall-panel kernel with it)
         self.exact = exact
         self.fast_solve = not exact  # U12 solve on DMMA with inverted diagonal blocks
         lo, hi = torch.cuda.Stream.priority_range()
@@ -154,6 +158,14 @@ class CudaKernels:
     def panel(self, a, m: int, d: int, col: int, w: int, piv):
         gr = self.grid_rows if self.grid_rows is not None else self.GRID_PANEL_ROWS
         opt = self.opt_grid if m - d > gr else self.opt
+        if opt is self.opt_grid and opt.panel_kernel == _lib.PANEL_MCLUSTER and os.environ.get("PFLU_MC_ADAPT", "1") != "0":
+            # = tall_panel_ctas() of csrc/pflu.cu: while this rank's share of the step's trailing update (ms, at
+            # the in-step DMMA rate) outlasts the panel + TU_L (measured 0.83 + 1.65e-5 * rows), the step is
+            # bound by SM time: two clusters instead of four
+            rows = m - d
+            t_upd = 2.0 * rows * ((m - d - w) / max(1, self.ranks)) * w / 33.0e12 * 1e3
+            if t_upd > 0.83 + 1.65e-5 * rows:
+                opt = self.opt_grid2
         rc = self.L.pflu_panel(a.data_ptr(), a.stride(0), m, d, col, w, piv.data_ptr(), None, self._st(),
                                ctypes.byref(opt))
         _lib.check(rc, "pflu_panel")
@@ -282,6 +294,8 @@ def getrf_block_cyclic(a_loc: torch.Tensor, n: int, b: int, lookahead: int = 1, 
     if emulate and P != 1:
         raise ValueError("emulate is a single-rank scaling model")
     Q = max(1, int(emulate or 1))  # the rank count whose critical path runs
+    if getattr(kernels, "is_cuda", False):
+        kernels.ranks = max(P, Q)
     if getattr(kernels, "is_cuda", False) and kernels.grid_rows is None:
         kernels.grid_rows = kernels.GRID_PANEL_ROWS if max(P, Q) >= kernels.GRID_MIN_RANKS else 1 << 62
     dev = a_loc.device
