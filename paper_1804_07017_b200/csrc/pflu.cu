@@ -148,7 +148,7 @@ static int g_emu_ranks = []() { const char* e = getenv("PFLU_EMU_RANKS"); return
 static int g_swap_bn = []() { const char* e = getenv("PFLU_SWAP_BN"); return e ? atoi(e) : 16; }();  // C4: 16 -> 764.5, 32 -> 769.2 ms
 // strip width of the pure row-permutation kernel (deferred left swaps): 16 or 32 columns
 static int g_lswap_tw = []() { const char* e = getenv("PFLU_LSWAP_TW"); return e ? atoi(e) : 16; }();
-static int g_emu_grid_ranks = []() { const char* e = getenv("PFLU_EMU_GRID_RANKS"); return e ? atoi(e) : 8; }();
+static int g_emu_grid_ranks = []() { const char* e = getenv("PFLU_EMU_GRID_RANKS"); return e ? atoi(e) : 4; }();
 static int g_tur_split = []() { const char* e = getenv("PFLU_TUR_SPLIT"); return e ? atoi(e) : 0; }();
 
 // Trace of one factorization: pairs of timing events around PF / TU / TU_L / TU_R / GEMM.

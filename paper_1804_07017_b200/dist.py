@@ -101,7 +101,7 @@ class CudaKernels:
     # when the panel chain, not the per-rank trailing update, bounds the run (many ranks); with few
     # ranks the 16-SM cluster kernel leaves more SMs to the update.  None: decided per call from P.
     GRID_PANEL_ROWS = 8192
-    GRID_MIN_RANKS = int(os.environ.get("PFLU_DIST_GRID_MIN_RANKS", "8"))  # scaling model: 2, 4 -> cluster
+    GRID_MIN_RANKS = int(os.environ.get("PFLU_DIST_GRID_MIN_RANKS", "4"))  # scaling model: 2 ranks -> cluster; from 4 the (adaptive) multi-cluster kernel
 
     def __init__(self, device: torch.device, exact: bool = False, grid_rows: int | None = None):
         self.L = _lib.load()
