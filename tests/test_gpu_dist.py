@@ -215,3 +215,30 @@ def test_dist_cuda_trace(cuda, tmp_path):
             assert 0 <= s_ <= e_
         assert sorted(by["PF"]) == list(range(rank, 8, 2))
         assert sorted(by["BCAST"]) == list(range(8)) and sorted(by["TU_R"]) == list(range(8))
+
+
+@pytest.mark.parametrize("ranks", [1, 8])
+def test_dist_tall_panel_kernel_choice_bitwise(cuda, ranks):
+    """CudaKernels.panel sends panels taller than grid_rows to the multi-cluster kernel -- two clusters while
+    the rank's share of the trailing update would outlast the panel (ranks = 1 here), all of them otherwise
+    (ranks = 8): both must be bitwise the oracle's lu_unb on the panel (exact mode)."""
+    import torch
+
+    import oracle
+    from paper_1804_07017_b200 import _lib
+    from paper_1804_07017_b200 import dist as pd
+
+    m, w = 20000, 256
+    p0 = np.random.default_rng(97).uniform(-1.0, 1.0, (m, w))
+    want, wpiv, winfo = oracle.lu_unb(p0.copy())
+    kern = pd.CudaKernels(cuda, exact=True, grid_rows=8192)
+    kern.ranks = ranks
+    assert kern.opt_grid.panel_kernel == _lib.PANEL_MCLUSTER and kern.opt_grid2.panel_ctas == 32
+    x = torch.from_numpy(p0).to(cuda)
+    piv = torch.zeros(w, dtype=torch.int64, device=cuda)
+    with kern.stream("P"):
+        kern.panel(x, m, 0, 0, w, piv)
+    torch.cuda.synchronize()
+    assert winfo == 0
+    assert np.array_equal(piv.cpu().numpy(), wpiv)
+    assert x.cpu().numpy().tobytes() == want.tobytes()

@@ -148,3 +148,19 @@ print('nccl-ok')
     env = dict(os.environ, PFLU_MG_FORCE="1")
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "nccl-ok" in out.stdout, out.stderr[-3000:]
+
+
+def test_mg_tall_panels_multicluster_exact(cuda, virtual_ranks):
+    """From 4 ranks up the owner factors panels taller than 8192 rows on the multi-cluster kernel (with the
+    adaptive cluster count): n = 9472 puts the first panels there.  Exact mode must stay bitwise the oracle."""
+    from paper_1804_07017_b200 import getrf_mg
+
+    n, b, P = 9472, 256, 4
+    a0 = np.random.default_rng(41).uniform(-1.0, 1.0, (n, n))
+    want, wpiv, winfo = oracle.getrf(a0, b)
+    virtual_ranks(P)
+    a = np.array(a0, copy=True)
+    piv, inf = getrf_mg(a, b, 1, P, exact=True)
+    assert inf == winfo == 0
+    assert np.array_equal(piv, wpiv)
+    assert bitwise_equal(a, want)
