@@ -254,6 +254,38 @@ def test_panel_multicluster_bitwise(cuda, m, w, zero_cols):
         assert bitwise_equal(x.cpu().numpy(), want)
 
 
+def test_panel_multicluster_special_values(cuda):
+    """The multi-cluster exchange keeps the reference's pivot rules for special values (_jit.py:163-170): a NaN
+    below the diagonal is never chosen, a NaN on the diagonal is kept, +-inf wins, exact ties go to the
+    smallest row -- also when the tied rows sit in different clusters."""
+    import warnings
+
+    import torch
+    from paper_1804_07017_b200 import _lib as lb
+
+    m, w = 18000, 64
+    p0 = np.random.default_rng(77).uniform(-1.0, 1.0, (m, w))
+    p0[17000, 3] = np.nan
+    p0[5, 5] = np.nan
+    p0[16000, 20] = np.inf
+    p0[9000, 30] = -np.inf
+    p0[300, 40] = p0[12000, 40] = p0[17500, 40] = 9.0  # one tie across the clusters
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        want, wpiv, winfo = oracle.lu_unb(p0.copy())
+    for exact in (True, False):
+        x = _t(p0, cuda)
+        piv = torch.zeros(w, dtype=torch.int64, device=cuda)
+        info = ctypes.c_int64(0)
+        opt = lb.options(exact=exact, panel_kernel=lb.PANEL_MCLUSTER)
+        lb.check(lb.load().pflu_panel(x.data_ptr(), w, m, 0, 0, w, piv.data_ptr(), ctypes.byref(info), _stream(),
+                                      ctypes.byref(opt)), "panel")
+        assert np.array_equal(piv.cpu().numpy()[: len(wpiv)], wpiv), exact
+        assert info.value == winfo
+        if exact:
+            assert np.array_equal(x.cpu().numpy(), want, equal_nan=True)
+
+
 @pytest.mark.parametrize("m,w", [(300, 64), (5000, 256), (20000, 256), (2048, 512), (100, 200)])
 def test_panel_recursive_dmma(cuda, m, w):
     """Recursive panel in DMMA mode: the oracle's pivots, factors within rounding of getf2's."""
