@@ -1112,7 +1112,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) panel_kernel(PanelArgs p) {
       if (!exact) {
         // DMMA: a warp tile is GR row groups x 64 columns; its C values (and, for L from global
         // memory, its L fragment) are all in flight before the first MMA; K zero padded
-        constexpr int GR = a_tile ? 4 : 2;
+        constexpr int GR = 2;  // r06: 4 row groups for the tile operand cost the short panels 1-2% and the tall ones 4-6% (registers)
         const int ngroups = (nupd + 7) / 8;
         const int ntr = (ngroups + GR - 1) / GR;      // 32-row tiles
         const int nch = (ncols + PF_UCH - 1) / PF_UCH;
