@@ -1167,7 +1167,9 @@ static int getrf_async(DevCtx& c, double* a, int64_t m, int64_t n, int64_t lda, 
   // above (C4 unchanged, its concurrent chunk GEMMs interfere); PFLU_CHUNKS overrides
   // r05 (WS GEMM) re-measure, profiles/r05_chunks_sweep.log: C4 1 chunk 723.2 ms, 2: 723.1, 3: 721.0,
   // 4: 719.8, 6: 720.0; C3 114.3 / 112.8 / 112.6 / 112.4 / 112.4 -> 6 up to 16384, 4 above
-  const int dflt = g_chunks_env > 0 ? g_chunks_env : (n <= 16384 ? 6 : 4);
+  // r06: 5 above 16384 -- same time as 4 (C4 705.9 vs 706.1 ms, C5 5472 vs 5473 ms) with the swap + U12-solve
+  // time that no GEMM covers down from 6.9 to 4.2 ms (tools/exposed_swap.py; 6: 5.4 ms, 8: 4.7 ms but +4 ms)
+  const int dflt = g_chunks_env > 0 ? g_chunks_env : (n <= 16384 ? 6 : 5);
   const int nch = sched ? 1 : std::max(1, std::min({hin ? std::max(dflt, hin->chunks) : dflt, MAX_CHUNKS, count}));
   std::vector<int> chunk_blk(nch + 1);
   for (int ch = 0; ch <= nch; ++ch) chunk_blk[ch] = (int)((int64_t)count * ch / nch);
